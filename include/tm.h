@@ -1,0 +1,161 @@
+/*
+ * tm.h -- C ABI of the B200-native TalkingMachines sparse-causal chunk
+ * attention library (arXiv 2506.03099).  libtm.so, built from
+ * paper_2506_03099_b200/csrc for sm_100a.
+ *
+ * Citations: "P:n" = PAPER.md line n; "S:n" = SPEC.md line n.
+ *
+ * What the library computes (Sec 4.2, Eq 7): the queries of
+ * latent-video chunk c_t attend bidirectionally to all tokens of c_t, to the
+ * cached K/V of the previous chunk c_{t-1} and to the cached K/V of the
+ * reference chunk c_0; "K and V include tokens from {c_0, c_{t-1}, c_t}
+ * only".  The K/V of c_0 and c_{t-1} are cached "for each timestep,
+ * over all transformer blocks", so they are reused across chunks and
+ * across the denoising steps (2 NFE).  Plus the flow-matching Euler
+ * update x <- x + dt*v (Eqs 1-2).
+ *
+ * Conventions
+ *  - All tensors are dense, row-major, TOKEN-MAJOR: [B][L][H][d] (batch of
+ *    independent streams, tokens, heads, head dim).  With world_size P > 1
+ *    (Ulysses sequence parallelism) the caller passes its sequence
+ *    shard [B][L/P][H][d]; the library exchanges to head shards internally.
+ *    L/P is rounded up (shards padded) when P does not divide L.
+ *  - dtype TM_BF16: q, k, v, o are bfloat16; cache bf16.  TM_FP32: fp32
+ *    everywhere (validation mode).
+ *  - Every device pointer is owned by the CALLER (allocated e.g. with torch)
+ *    and must stay valid until the stream reaches the call.  The library
+ *    owns only the opaque host tm_ctx (and, for P > 1, its NCCL
+ *    communicator).  The library never allocates device memory after
+ *    tm_attn_init.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default).
+ *  - Argument, shape and ordering errors are detected on the host before
+ *    any launch; the call then has no side effects.  Device / NCCL errors
+ *    return TM_ERR_CUDA / TM_ERR_NCCL.  tm_last_error() gives a message.
+ *  - Thread-compatible, not thread-safe per ctx.  For P > 1 every call
+ *    except tm_flow_euler_step is collective: all ranks call in the same
+ *    order.
+ */
+#ifndef TM_H_
+#define TM_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    TM_OK = 0,
+    TM_ERR_INVALID_ARG = 1,     /* null pointer, bad enum, bad index            */
+    TM_ERR_SHAPE = 2,           /* dimension error                        */
+    TM_ERR_DEGENERATE_MASK = 3, /* an empty attend set                    */
+    TM_ERR_STREAM_ORDER = 4,    /* cache miss / chunk out of order       */
+    TM_ERR_REF_IMMUTABLE = 5,   /* reference rewrite after stream start  */
+    TM_ERR_NONFINITE = 6,       /* NaN/Inf output, TM_DEBUG=1 only        */
+    TM_ERR_UNSUPPORTED = 7,     /* valid but not implemented configuration       */
+    TM_ERR_CUDA = 8,
+    TM_ERR_NCCL = 9
+} tm_status;
+
+typedef enum { TM_BF16 = 0, TM_FP32 = 1 } tm_dtype;
+
+typedef struct {
+    int32_t heads;         /* H, global number of attention heads (MHA; H_kv == H)   */
+    int32_t head_dim;      /* d in {64, 128}                                          */
+    int32_t ref_tokens;    /* Lr: tokens of the reference chunk c_0 (>= 1)            */
+    int32_t chunk_tokens;  /* Lc: tokens per generated chunk (frames x tokens/frame)  */
+    int32_t num_layers;    /* transformer blocks whose K/V are cached (40 for WAN)    */
+    int32_t num_steps;     /* denoising steps (NFE) per chunk with a cache slot (2)   */
+    int32_t batch;         /* B independent streams (>= 1)                            */
+    int32_t dtype;         /* tm_dtype                                                */
+    float softmax_scale;   /* 0 -> 1/sqrt(d), Eq 7                                    */
+    int32_t world_size;    /* P, Ulysses group size; H % P == 0                       */
+    int32_t rank;          /* this process's rank in [0, P)                           */
+    int32_t device;        /* CUDA device ordinal used by this ctx                    */
+} tm_config;
+
+typedef struct tm_ctx tm_ctx;
+
+/* Version of the ABI (major * 100 + minor). */
+int32_t tm_version(void);
+
+/* Thread-local message for the last non-OK status returned on this thread. */
+const char* tm_last_error(void);
+
+/* Bytes of the per-rank KV cache: for each (layer, step) the reference
+ * K and V ([B][Lr][H/P][d]) and two rotating chunk slots of K and V
+ * ([B][Lc][H/P][d] each), every region 1024-byte aligned.  A closed form of
+ * the config, independent of stream length.  0 on invalid config. */
+size_t tm_kvcache_bytes(const tm_config* cfg);
+
+/* Bytes of device workspace: Ulysses staging when world_size > 1, plus a
+ * small debug/scratch area.  0 is never returned for a valid config. */
+size_t tm_workspace_bytes(const tm_config* cfg);
+
+/* NCCL unique id for world_size > 1 (rank 0 calls it; the harness
+ * broadcasts the 128 bytes, e.g. with torch.distributed). */
+tm_status tm_get_unique_id(uint8_t id[128]);
+
+/* Create a context.  `cache` (device, >= tm_kvcache_bytes, 1024-B aligned)
+ * and `workspace` (device, >= tm_workspace_bytes, 256-B aligned) are owned
+ * by the caller and must outlive the ctx.  nccl_id: NULL when world_size==1.
+ * Validates the config (TM_ERR_SHAPE for H % P != 0, d not in {64,128},
+ * non-positive lengths).  Collective when world_size > 1. */
+tm_status tm_attn_init(const tm_config* cfg, const uint8_t* nccl_id, void* cache,
+                       size_t cache_bytes, void* workspace, size_t workspace_bytes,
+                       tm_ctx** out);
+
+tm_status tm_attn_destroy(tm_ctx* ctx);
+
+/* Start a new stream: forget the chunk order and allow a new reference. */
+tm_status tm_stream_reset(tm_ctx* ctx);
+
+/* a1: store the reference chunk's K/V for (layer, step);
+ * step = -1 stores it for every step.  k, v: device [B][Lr(/P)][H][d].
+ * Once chunk 1 has been attended at a (layer, step), rewriting its reference
+ * returns TM_ERR_REF_IMMUTABLE until tm_stream_reset. */
+tm_status tm_kvcache_put_reference(tm_ctx* ctx, int32_t layer, int32_t step, const void* k,
+                                   const void* v, void* stream);
+
+/* a2-a6: attention of chunk `chunk` (>= 1) at (layer, step).
+ * q, k, v: device [B][Lc(/P)][H][d], the chunk's post-projection queries,
+ * keys and values; o: device output, same shape.  The chunk's K/V are
+ * appended to cache slot chunk&1 (they become c_{t-1} for chunk+1); keys
+ * and values attended are {c_0 (cache), c_{t-1} (cache, chunk >= 2), c_t}
+ * (P:151).  Order per (layer, step): chunk == last + 1, or chunk == last
+ * (a redo of the same chunk, which re-reads the same c_{t-1});
+ * otherwise TM_ERR_STREAM_ORDER; chunk 1 without a reference ->
+ * TM_ERR_STREAM_ORDER (cache miss).  k/v may alias the slot returned
+ * by tm_kvcache_slot_ptr (zero-copy append). */
+tm_status tm_chunk_attention(tm_ctx* ctx, int32_t layer, int32_t step, int64_t chunk,
+                             const void* q, const void* k, const void* v, void* o,
+                             void* stream);
+
+/* Device pointers of the cache slot that chunk `chunk` at (layer, step) is
+ * stored in ([B][Lc][H/P][d] each).  A caller may write the chunk's K/V
+ * there before tm_chunk_attention to skip the append copy. */
+tm_status tm_kvcache_slot_ptr(tm_ctx* ctx, int32_t layer, int32_t step, int64_t chunk,
+                              void** k, void** v);
+
+/* Device pointers of the reference region of (layer, step) ([B][Lr][H/P][d]). */
+tm_status tm_kvcache_ref_ptr(tm_ctx* ctx, int32_t layer, int32_t step, void** k, void** v);
+
+/* a7: x[i] <- x[i] + dt * v[i] for i < n, in place, one fp32
+ * FMA per element (single rounding).  x: device fp32 [n]; v: device, dtype
+ * v_dtype (TM_BF16 or TM_FP32) [n].  ctx may be NULL.  x and v must be
+ * 16-byte aligned.  n == 0 is a no-op. */
+tm_status tm_flow_euler_step(tm_ctx* ctx, float* x, const void* v, int32_t v_dtype, int64_t n,
+                             float dt, void* stream);
+
+/* Introspection for tests / bench: number of device kernels the last
+ * tm_chunk_attention launched on this ctx, and the attention kernel
+ * variant name ("sm100_tcgen05" or "fp32_simt"). */
+int32_t tm_last_launch_count(const tm_ctx* ctx);
+const char* tm_kernel_variant(const tm_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TM_H_ */

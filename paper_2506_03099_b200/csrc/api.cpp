@@ -1,0 +1,458 @@
+// api.cpp -- the C ABI of include/tm.h: config validation, the constant-
+// memory KV cache (rows a1, a3), ordering state, the mask -> segment
+// schedule (row a4), the Ulysses exchange (rows a2, a6) and dispatch to the
+// sm_100a kernels (rows a5, a7).
+//
+// PAPER.md: P:137-151 (Sec 4.2 sparse causal attention, Eq 7), P:187 (KV
+// cache of c_0 and c_{t-1} per timestep per block), P:171 (sequence
+// parallelism), P:55-66 (flow matching, Eqs 1-2).  SPEC.md errors:
+// S:39 (dimension / degenerate mask), S:287 (reference rewrite)
+// (cache miss / order).
+#include "../../include/tm.h"
+
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "comm.h"
+#include "internal.h"
+
+using namespace tmk;
+
+namespace {
+
+thread_local std::string g_err;
+
+tm_status fail(tm_status s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return s;
+}
+
+constexpr size_t kAlign = 1024;
+size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+tm_status validate(const tm_config* c) {
+    if (!c) return fail(TM_ERR_INVALID_ARG, "null config");
+    if (c->dtype != TM_BF16 && c->dtype != TM_FP32)
+        return fail(TM_ERR_INVALID_ARG, "dtype %d not in {TM_BF16, TM_FP32}", c->dtype);
+    if (c->heads <= 0 || c->ref_tokens <= 0 || c->chunk_tokens <= 0 || c->num_layers <= 0 ||
+        c->num_steps <= 0 || c->batch <= 0)
+        return fail(TM_ERR_SHAPE, "non-positive dimension (H=%d Lr=%d Lc=%d layers=%d steps=%d B=%d)",
+                    c->heads, c->ref_tokens, c->chunk_tokens, c->num_layers, c->num_steps,
+                    c->batch);
+    if (c->head_dim != 64 && c->head_dim != 128)
+        return fail(TM_ERR_SHAPE, "head_dim %d not in {64, 128}", c->head_dim);
+    if (c->world_size <= 0 || c->rank < 0 || c->rank >= c->world_size)
+        return fail(TM_ERR_INVALID_ARG, "rank %d / world_size %d", c->rank, c->world_size);
+    if (c->heads % c->world_size)
+        return fail(TM_ERR_SHAPE, "heads %d not divisible by world_size %d (Ulysses head sharding)",
+                    c->heads, c->world_size);
+    if (!(c->softmax_scale >= 0.f) || !std::isfinite(c->softmax_scale))
+        return fail(TM_ERR_INVALID_ARG, "softmax_scale must be finite and >= 0");
+    return TM_OK;
+}
+
+struct Layout {
+    int esize, Hl, P;
+    int64_t Lr, Lc, Lr_s, Lc_s;     // full and per-rank shard token counts
+    size_t ref_bytes, slot_bytes, region_bytes, cache_bytes;
+    size_t flag_bytes, xfer_bytes, head_bytes, ws_bytes;
+};
+
+Layout layout_of(const tm_config* c) {
+    Layout L{};
+    L.esize = c->dtype == TM_BF16 ? 2 : 4;
+    L.P = c->world_size;
+    L.Hl = c->heads / c->world_size;
+    L.Lr = c->ref_tokens;
+    L.Lc = c->chunk_tokens;
+    L.Lr_s = ceil_div(L.Lr, L.P);
+    L.Lc_s = ceil_div(L.Lc, L.P);
+    const size_t row = size_t(L.Hl) * c->head_dim * L.esize;     // one token, local heads
+    L.ref_bytes = align_up(size_t(c->batch) * L.Lr * row);
+    L.slot_bytes = align_up(size_t(c->batch) * L.Lc * row);
+    L.region_bytes = 2 * L.ref_bytes + 4 * L.slot_bytes;          // Kref Vref K0 V0 K1 V1
+    L.cache_bytes = L.region_bytes * size_t(c->num_layers) * size_t(c->num_steps);
+    L.flag_bytes = kAlign;
+    if (L.P > 1) {
+        const size_t full_row = size_t(c->heads) * c->head_dim * L.esize;
+        const size_t qkv = 3 * align_up(size_t(c->batch) * L.Lc_s * full_row);
+        const size_t kv = 2 * align_up(size_t(c->batch) * L.Lr_s * full_row);
+        L.xfer_bytes = qkv > kv ? qkv : kv;
+        L.head_bytes = L.slot_bytes;                               // Q or O, [B][Lc][Hl][d]
+        L.ws_bytes = L.flag_bytes + 2 * L.xfer_bytes + 2 * L.head_bytes;
+    } else {
+        L.ws_bytes = L.flag_bytes;
+    }
+    return L;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+}  // namespace
+
+struct tm_ctx {
+    tm_config cfg;
+    Layout lay;
+    uint8_t* cache;
+    uint8_t* ws;
+    float scale;
+    std::vector<int64_t> last;        // [layer][step]: last chunk attended (0 = none)
+    std::vector<uint8_t> ref_ok;      // [layer][step]: reference written
+    void* comm = nullptr;
+    int launches = 0;
+    bool debug = false;
+
+    size_t idx(int layer, int step) const { return size_t(layer) * cfg.num_steps + step; }
+    uint8_t* region(int layer, int step) const { return cache + idx(layer, step) * lay.region_bytes; }
+    uint8_t* kref(int l, int s) const { return region(l, s); }
+    uint8_t* vref(int l, int s) const { return region(l, s) + lay.ref_bytes; }
+    uint8_t* kslot(int l, int s, int64_t t) const {
+        return region(l, s) + 2 * lay.ref_bytes + (t & 1) * 2 * lay.slot_bytes;
+    }
+    uint8_t* vslot(int l, int s, int64_t t) const { return kslot(l, s, t) + lay.slot_bytes; }
+    int* flag() const { return reinterpret_cast<int*>(ws); }
+    uint8_t* send() const { return ws + lay.flag_bytes; }
+    uint8_t* recv() const { return send() + lay.xfer_bytes; }
+    uint8_t* qh() const { return recv() + lay.xfer_bytes; }
+    uint8_t* oh() const { return qh() + lay.head_bytes; }
+};
+
+namespace {
+
+tm_status cuda_check(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return TM_OK;
+    return fail(TM_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+tm_status debug_check(tm_ctx* c, const void* x, int64_t n, int is_bf16, cudaStream_t s,
+                      const char* what) {
+    if (!c->debug) return TM_OK;
+    tm_status st = cuda_check(cudaMemsetAsync(c->flag(), 0, sizeof(int), s), "debug memset");
+    if (st) return st;
+    st = cuda_check(launch_nonfinite(x, is_bf16, n, c->flag(), s, &c->launches), "nonfinite check");
+    if (st) return st;
+    int h = 0;
+    st = cuda_check(cudaMemcpyAsync(&h, c->flag(), sizeof(int), cudaMemcpyDeviceToHost, s),
+                    "debug readback");
+    if (st) return st;
+    st = cuda_check(cudaStreamSynchronize(s), "debug sync");
+    if (st) return st;
+    if (h) return fail(TM_ERR_NONFINITE, "%s produced NaN/Inf (TM_DEBUG)", what);
+    return TM_OK;
+}
+
+tm_status check_layer_step(const tm_ctx* c, int32_t layer, int32_t step, bool allow_all) {
+    if (layer < 0 || layer >= c->cfg.num_layers)
+        return fail(TM_ERR_INVALID_ARG, "layer %d outside [0, %d)", layer, c->cfg.num_layers);
+    if (step == -1 && allow_all) return TM_OK;
+    if (step < 0 || step >= c->cfg.num_steps)
+        return fail(TM_ERR_INVALID_ARG, "step %d outside [0, %d)", step, c->cfg.num_steps);
+    return TM_OK;
+}
+
+// Ulysses seq -> head exchange of `ntensors` tensors of [B][Ls][H][d] each;
+// received blocks are unpacked to dst[i] ([B][L][Hl][d]).  P:171.
+tm_status ulysses_in(tm_ctx* c, int ntensors, const void* const* src, void* const* dst, int64_t Ls,
+                     int64_t L, cudaStream_t s) {
+    const Layout& Ly = c->lay;
+    const int d = c->cfg.head_dim, B = c->cfg.batch, H = c->cfg.heads;
+    const size_t blk = align_up(size_t(B) * Ls * H * d * Ly.esize);
+    for (int i = 0; i < ntensors; ++i) {
+        tm_status st = cuda_check(launch_pack_seq_to_peers(src[i], c->send() + i * blk, B, Ls, H,
+                                                           Ly.P, d, Ly.esize, s, &c->launches),
+                                  "pack seq->peers");
+        if (st) return st;
+    }
+    for (int i = 0; i < ntensors; ++i) {
+        const char* e = comm_alltoall(c->comm, c->send() + i * blk, c->recv() + i * blk,
+                                      size_t(B) * Ls * Ly.Hl * d * Ly.esize, Ly.P, s);
+        if (e) return fail(TM_ERR_NCCL, "all-to-all (seq->head): %s", e);
+    }
+    for (int i = 0; i < ntensors; ++i) {
+        tm_status st = cuda_check(launch_unpack_peers_to_heads(c->recv() + i * blk, dst[i], B, Ls,
+                                                               L, Ly.Hl, Ly.P, d, Ly.esize, s,
+                                                               &c->launches),
+                                  "unpack peers->heads");
+        if (st) return st;
+    }
+    return TM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t tm_version(void) { return 100; }
+
+const char* tm_last_error(void) { return g_err.c_str(); }
+
+size_t tm_kvcache_bytes(const tm_config* cfg) {
+    if (validate(cfg) != TM_OK) return 0;
+    return layout_of(cfg).cache_bytes;
+}
+
+size_t tm_workspace_bytes(const tm_config* cfg) {
+    if (validate(cfg) != TM_OK) return 0;
+    return layout_of(cfg).ws_bytes;
+}
+
+tm_status tm_get_unique_id(uint8_t id[128]) {
+    if (!id) return fail(TM_ERR_INVALID_ARG, "null id");
+    const char* e = comm_unique_id(id);
+    return e ? fail(TM_ERR_NCCL, "%s", e) : TM_OK;
+}
+
+tm_status tm_attn_init(const tm_config* cfg, const uint8_t* nccl_id, void* cache,
+                       size_t cache_bytes, void* workspace, size_t workspace_bytes, tm_ctx** out) {
+    tm_status st = validate(cfg);
+    if (st) return st;
+    if (!out) return fail(TM_ERR_INVALID_ARG, "null out");
+    *out = nullptr;
+    const Layout L = layout_of(cfg);
+    if (!cache || cache_bytes < L.cache_bytes)
+        return fail(TM_ERR_INVALID_ARG, "cache buffer %zu bytes < required %zu", cache_bytes,
+                    L.cache_bytes);
+    if (reinterpret_cast<uintptr_t>(cache) % kAlign)
+        return fail(TM_ERR_INVALID_ARG, "cache must be %zu-byte aligned", kAlign);
+    if (!workspace || workspace_bytes < L.ws_bytes)
+        return fail(TM_ERR_INVALID_ARG, "workspace %zu bytes < required %zu", workspace_bytes,
+                    L.ws_bytes);
+    if (reinterpret_cast<uintptr_t>(workspace) % 256)
+        return fail(TM_ERR_INVALID_ARG, "workspace must be 256-byte aligned");
+    if (cfg->world_size > 1 && !nccl_id)
+        return fail(TM_ERR_INVALID_ARG, "world_size > 1 needs an NCCL unique id");
+    int cur = -1;
+    if (cudaGetDevice(&cur) != cudaSuccess) return fail(TM_ERR_CUDA, "no CUDA device");
+    if (cur != cfg->device && cudaSetDevice(cfg->device) != cudaSuccess)
+        return fail(TM_ERR_CUDA, "cannot select device %d", cfg->device);
+    int major = 0, minor = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, cfg->device);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, cfg->device);
+    if (major != 10 || minor != 0)
+        return fail(TM_ERR_UNSUPPORTED, "device %d is sm_%d%d; libtm is built for sm_100a only",
+                    cfg->device, major, minor);
+    tm_ctx* c = new tm_ctx();
+    c->cfg = *cfg;
+    c->lay = L;
+    c->cache = static_cast<uint8_t*>(cache);
+    c->ws = static_cast<uint8_t*>(workspace);
+    c->scale = cfg->softmax_scale > 0.f ? cfg->softmax_scale : 1.0f / std::sqrt(float(cfg->head_dim));
+    c->last.assign(size_t(cfg->num_layers) * cfg->num_steps, 0);
+    c->ref_ok.assign(size_t(cfg->num_layers) * cfg->num_steps, 0);
+    const char* dbg = getenv("TM_DEBUG");
+    c->debug = dbg && *dbg && strcmp(dbg, "0") != 0;
+    if (cfg->world_size > 1) {
+        const char* e = comm_init(&c->comm, cfg->world_size, cfg->rank, nccl_id);
+        if (e) {
+            delete c;
+            return fail(TM_ERR_NCCL, "ncclCommInitRank: %s", e);
+        }
+    }
+    *out = c;
+    return TM_OK;
+}
+
+tm_status tm_attn_destroy(tm_ctx* ctx) {
+    if (!ctx) return fail(TM_ERR_INVALID_ARG, "null ctx");
+    if (ctx->comm) comm_destroy(ctx->comm);
+    delete ctx;
+    return TM_OK;
+}
+
+tm_status tm_stream_reset(tm_ctx* ctx) {
+    if (!ctx) return fail(TM_ERR_INVALID_ARG, "null ctx");
+    std::fill(ctx->last.begin(), ctx->last.end(), 0);
+    std::fill(ctx->ref_ok.begin(), ctx->ref_ok.end(), 0);
+    return TM_OK;
+}
+
+tm_status tm_kvcache_ref_ptr(tm_ctx* ctx, int32_t layer, int32_t step, void** k, void** v) {
+    if (!ctx || !k || !v) return fail(TM_ERR_INVALID_ARG, "null argument");
+    tm_status st = check_layer_step(ctx, layer, step, false);
+    if (st) return st;
+    *k = ctx->kref(layer, step);
+    *v = ctx->vref(layer, step);
+    return TM_OK;
+}
+
+tm_status tm_kvcache_slot_ptr(tm_ctx* ctx, int32_t layer, int32_t step, int64_t chunk, void** k,
+                              void** v) {
+    if (!ctx || !k || !v) return fail(TM_ERR_INVALID_ARG, "null argument");
+    tm_status st = check_layer_step(ctx, layer, step, false);
+    if (st) return st;
+    if (chunk < 1) return fail(TM_ERR_INVALID_ARG, "chunk %lld < 1", (long long)chunk);
+    *k = ctx->kslot(layer, step, chunk);
+    *v = ctx->vslot(layer, step, chunk);
+    return TM_OK;
+}
+
+tm_status tm_kvcache_put_reference(tm_ctx* ctx, int32_t layer, int32_t step, const void* k,
+                                   const void* v, void* stream) {
+    if (!ctx || !k || !v) return fail(TM_ERR_INVALID_ARG, "null argument");
+    tm_status st = check_layer_step(ctx, layer, step, true);
+    if (st) return st;
+    const int s0 = step < 0 ? 0 : step, s1 = step < 0 ? ctx->cfg.num_steps : step + 1;
+    for (int s = s0; s < s1; ++s)
+        if (ctx->last[ctx->idx(layer, s)] >= 1)
+            return fail(TM_ERR_REF_IMMUTABLE,
+                        "reference of (layer %d, step %d) is immutable after chunk 1 until "
+                        "tm_stream_reset (S:287)", layer, s);
+    cudaStream_t cs = static_cast<cudaStream_t>(stream);
+    const Layout& Ly = ctx->lay;
+    ctx->launches = 0;
+    if (Ly.P == 1) {
+        const size_t bytes = size_t(ctx->cfg.batch) * Ly.Lr * Ly.Hl * ctx->cfg.head_dim * Ly.esize;
+        for (int s = s0; s < s1; ++s) {
+            st = cuda_check(cudaMemcpyAsync(ctx->kref(layer, s), k, bytes, cudaMemcpyDeviceToDevice, cs),
+                            "reference K copy");
+            if (!st) st = cuda_check(cudaMemcpyAsync(ctx->vref(layer, s), v, bytes,
+                                                     cudaMemcpyDeviceToDevice, cs),
+                                     "reference V copy");
+            if (st) return st;
+        }
+    } else {
+        const void* src[2] = {k, v};
+        void* dst[2] = {ctx->kref(layer, s0), ctx->vref(layer, s0)};
+        st = ulysses_in(ctx, 2, src, dst, Ly.Lr_s, Ly.Lr, cs);
+        if (st) return st;
+        for (int s = s0 + 1; s < s1; ++s) {
+            st = cuda_check(cudaMemcpyAsync(ctx->kref(layer, s), ctx->kref(layer, s0), 2 * Ly.ref_bytes,
+                                            cudaMemcpyDeviceToDevice, cs),
+                            "reference alias copy");
+            if (st) return st;
+        }
+    }
+    for (int s = s0; s < s1; ++s) ctx->ref_ok[ctx->idx(layer, s)] = 1;
+    return TM_OK;
+}
+
+tm_status tm_chunk_attention(tm_ctx* ctx, int32_t layer, int32_t step, int64_t chunk,
+                             const void* q, const void* k, const void* v, void* o, void* stream) {
+    if (!ctx || !q || !k || !v || !o) return fail(TM_ERR_INVALID_ARG, "null argument");
+    tm_status st = check_layer_step(ctx, layer, step, false);
+    if (st) return st;
+    if (chunk < 1) return fail(TM_ERR_INVALID_ARG, "chunk %lld < 1 (the reference is chunk 0)",
+                               (long long)chunk);
+    if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o))
+        return fail(TM_ERR_INVALID_ARG, "q, k, v, o must be 16-byte aligned");
+    const size_t li = ctx->idx(layer, step);
+    if (!ctx->ref_ok[li])
+        return fail(TM_ERR_STREAM_ORDER, "cache miss: no reference for (layer %d, step %d) (S:296)",
+                    layer, step);
+    const int64_t last = ctx->last[li];
+    if (chunk != last + 1 && chunk != last)
+        return fail(TM_ERR_STREAM_ORDER,
+                    "chunk %lld at (layer %d, step %d) out of order (last %lld; S:296)",
+                    (long long)chunk, layer, step, (long long)last);
+    const tm_config& cf = ctx->cfg;
+    const Layout& Ly = ctx->lay;
+    cudaStream_t cs = static_cast<cudaStream_t>(stream);
+    ctx->launches = 0;
+
+    void* kslot = ctx->kslot(layer, step, chunk);
+    void* vslot = ctx->vslot(layer, step, chunk);
+    const void* qattn = q;
+    void* oattn = o;
+    if (Ly.P == 1) {
+        // a3: append c_t's K/V into slot chunk&1 (skipped when the caller wrote them there).
+        const size_t bytes = size_t(cf.batch) * Ly.Lc * Ly.Hl * cf.head_dim * Ly.esize;
+        if (k != kslot) {
+            st = cuda_check(cudaMemcpyAsync(kslot, k, bytes, cudaMemcpyDeviceToDevice, cs), "K append");
+            if (st) return st;
+        }
+        if (v != vslot) {
+            st = cuda_check(cudaMemcpyAsync(vslot, v, bytes, cudaMemcpyDeviceToDevice, cs), "V append");
+            if (st) return st;
+        }
+    } else {
+        // a2: seq -> head all-to-all; K/V land in the cache slot (a3), Q in workspace.
+        const void* src[3] = {q, k, v};
+        void* dst[3] = {ctx->qh(), kslot, vslot};
+        st = ulysses_in(ctx, 3, src, dst, Ly.Lc_s, Ly.Lc, cs);
+        if (st) return st;
+        qattn = ctx->qh();
+        oattn = ctx->oh();
+    }
+
+    // a4: mask {c_0, c_{t-1}, c_t} -> segment schedule.  c_{t-1} is
+    // the other slot; at chunk 1 it coincides with c_0 and is not repeated
+    // (set semantics).
+    AttnProblem pr;
+    pr.q = qattn;
+    pr.o = oattn;
+    pr.Lq = Ly.Lc;
+    pr.B = cf.batch;
+    pr.H = Ly.Hl;
+    pr.d = cf.head_dim;
+    pr.scale = ctx->scale;
+    pr.seg[pr.nseg++] = Segment{ctx->kref(layer, step), ctx->vref(layer, step), Ly.Lr};
+    if (chunk >= 2)
+        pr.seg[pr.nseg++] = Segment{ctx->kslot(layer, step, chunk - 1),
+                                    ctx->vslot(layer, step, chunk - 1), Ly.Lc};
+    pr.seg[pr.nseg++] = Segment{kslot, vslot, Ly.Lc};
+
+    cudaError_t e = cf.dtype == TM_BF16 ? launch_fmha_sm100(pr, cs, &ctx->launches)
+                                        : launch_fmha_fp32(pr, cs, &ctx->launches);
+    st = cuda_check(e, "attention kernel launch");
+    if (st) return st;
+
+    if (Ly.P > 1) {
+        // a6: head -> seq all-to-all of O.
+        const size_t blk = size_t(cf.batch) * Ly.Lc_s * Ly.Hl * cf.head_dim * Ly.esize;
+        st = cuda_check(launch_pack_heads_to_peers(ctx->oh(), ctx->send(), cf.batch, Ly.Lc_s, Ly.Lc,
+                                                   Ly.Hl, Ly.P, cf.head_dim, Ly.esize, cs,
+                                                   &ctx->launches),
+                        "pack heads->peers");
+        if (st) return st;
+        const char* ce = comm_alltoall(ctx->comm, ctx->send(), ctx->recv(), blk, Ly.P, cs);
+        if (ce) return fail(TM_ERR_NCCL, "all-to-all (head->seq): %s", ce);
+        st = cuda_check(launch_unpack_peers_to_seq(ctx->recv(), o, cf.batch, Ly.Lc_s, cf.heads, Ly.P,
+                                                   cf.head_dim, Ly.esize, cs, &ctx->launches),
+                        "unpack peers->seq");
+        if (st) return st;
+    }
+    ctx->last[li] = chunk;
+    const int64_t n_out = int64_t(cf.batch) * (Ly.P > 1 ? Ly.Lc_s : Ly.Lc) * cf.heads * cf.head_dim;
+    return debug_check(ctx, o, n_out, cf.dtype == TM_BF16, cs, "tm_chunk_attention");
+}
+
+tm_status tm_flow_euler_step(tm_ctx* ctx, float* x, const void* v, int32_t v_dtype, int64_t n,
+                             float dt, void* stream) {
+    if (n < 0) return fail(TM_ERR_SHAPE, "n = %lld < 0", (long long)n);
+    if (n == 0) return TM_OK;
+    if (!x || !v) return fail(TM_ERR_INVALID_ARG, "null argument");
+    if (v_dtype != TM_BF16 && v_dtype != TM_FP32)
+        return fail(TM_ERR_INVALID_ARG, "v_dtype %d not in {TM_BF16, TM_FP32}", v_dtype);
+    if (!aligned16(x) || !aligned16(v)) return fail(TM_ERR_INVALID_ARG, "x and v must be 16-byte aligned");
+    if (!std::isfinite(dt)) return fail(TM_ERR_INVALID_ARG, "dt must be finite");
+    int dummy = 0;
+    int* counter = ctx ? &ctx->launches : &dummy;
+    if (ctx) ctx->launches = 0;
+    cudaStream_t cs = static_cast<cudaStream_t>(stream);
+    tm_status st = cuda_check(launch_euler(x, v, v_dtype == TM_BF16, n, dt, cs, counter),
+                              "euler launch");
+    if (st || !ctx) return st;
+    return debug_check(ctx, x, n, 0, cs, "tm_flow_euler_step");
+}
+
+int32_t tm_last_launch_count(const tm_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+const char* tm_kernel_variant(const tm_ctx* ctx) {
+    if (!ctx) return "";
+    return ctx->cfg.dtype == TM_BF16 ? "sm100_tcgen05" : "fp32_simt";
+}
+
+}  // extern "C"

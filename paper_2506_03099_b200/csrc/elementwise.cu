@@ -1,0 +1,191 @@
+// elementwise.cu -- HBM-bound kernels of the path:
+//   a7  flow-matching Euler step x <- x + dt*v (Eqs 1-2),
+//       one fp32 FMA per element (single rounding), 16-byte vector loads,
+//       grid sized in multiples of the SM count;
+//   a2/a6 Ulysses pack / unpack between sequence shards and head shards
+//       (DeepSpeed-Ulysses), 16-byte vector moves;
+//   debug finiteness check (TM_DEBUG).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "internal.h"
+
+namespace tmk {
+namespace {
+
+int num_sms() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+unsigned grid_for(int64_t work_items, int threads, int per_sm = 8) {
+    const int64_t want = (work_items + threads - 1) / threads;
+    const int64_t cap = int64_t(num_sms()) * per_sm;
+    return unsigned(want < cap ? (want > 0 ? want : 1) : cap);
+}
+
+// ------------------------------------------------------------------ Euler
+// x: fp32 [n] (16-B aligned), v: fp32 or bf16 [n].  Each thread handles 8
+// consecutive elements per iteration (2 x float4 of x, 8 v values).
+template <bool kBf16>
+__global__ void __launch_bounds__(256) euler_kernel(float* __restrict__ x,
+                                                    const void* __restrict__ vv, int64_t n,
+                                                    float dt) {
+    const int64_t n8 = n / 8;
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n8; i += stride) {
+        float4 a = reinterpret_cast<const float4*>(x)[2 * i];
+        float4 c = reinterpret_cast<const float4*>(x)[2 * i + 1];
+        float v[8];
+        if constexpr (kBf16) {
+            const uint4 w = reinterpret_cast<const uint4*>(vv)[i];
+            const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                v[2 * e] = __uint_as_float(ws[e] << 16);
+                v[2 * e + 1] = __uint_as_float(ws[e] & 0xffff0000u);
+            }
+        } else {
+            const float4 b0 = reinterpret_cast<const float4*>(vv)[2 * i];
+            const float4 b1 = reinterpret_cast<const float4*>(vv)[2 * i + 1];
+            v[0] = b0.x; v[1] = b0.y; v[2] = b0.z; v[3] = b0.w;
+            v[4] = b1.x; v[5] = b1.y; v[6] = b1.z; v[7] = b1.w;
+        }
+        a.x = __fmaf_rn(dt, v[0], a.x); a.y = __fmaf_rn(dt, v[1], a.y);
+        a.z = __fmaf_rn(dt, v[2], a.z); a.w = __fmaf_rn(dt, v[3], a.w);
+        c.x = __fmaf_rn(dt, v[4], c.x); c.y = __fmaf_rn(dt, v[5], c.y);
+        c.z = __fmaf_rn(dt, v[6], c.z); c.w = __fmaf_rn(dt, v[7], c.w);
+        reinterpret_cast<float4*>(x)[2 * i] = a;
+        reinterpret_cast<float4*>(x)[2 * i + 1] = c;
+    }
+    // ragged tail (< 8 elements), handled by the first threads of block 0
+    if (blockIdx.x == 0) {
+        const int64_t t = n8 * 8 + threadIdx.x;
+        if (t < n) {
+            float v;
+            if constexpr (kBf16)
+                v = __uint_as_float(uint32_t(static_cast<const uint16_t*>(vv)[t]) << 16);
+            else
+                v = static_cast<const float*>(vv)[t];
+            x[t] = __fmaf_rn(dt, v, x[t]);
+        }
+    }
+}
+
+// ------------------------------------------------------------------ finiteness
+template <bool kBf16>
+__global__ void nonfinite_kernel(const void* __restrict__ x, int64_t n, int* flag) {
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    int bad = 0;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+        float f = kBf16 ? __uint_as_float(uint32_t(static_cast<const uint16_t*>(x)[i]) << 16)
+                        : static_cast<const float*>(x)[i];
+        bad |= !isfinite(f);
+    }
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
+// ------------------------------------------------------------------ Ulysses
+// Rows are d*esize bytes, moved as 16-byte words (d*esize % 16 == 0).
+// mode 0  pack_seq_to_peers:    src [B][Ls][H][d]        -> dst [P][B][Ls][Hl][d]
+// mode 1  unpack_peers_to_heads: src [P][B][Ls][Hl][d]    -> dst [B][L][Hl][d]  (rows < L)
+// mode 2  pack_heads_to_peers:  src [B][L][Hl][d]         -> dst [P][B][Ls][Hl][d] (pad rows 0)
+// mode 3  unpack_peers_to_seq:  src [P][B][Ls][Hl][d]     -> dst [B][Ls][H][d]
+struct Shuffle {
+    const uint4* src;
+    uint4* dst;
+    int B, P, Hl, W;   // W = 16-byte words per row
+    int64_t Ls, L;
+    int mode;
+};
+
+__global__ void __launch_bounds__(256) ulysses_kernel(const Shuffle s) {
+    // Iterate over the [P][B][Ls][Hl][W] peer-block index space.
+    const int64_t total = int64_t(s.P) * s.B * s.Ls * s.Hl * s.W;
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < total; idx += stride) {
+        int64_t r = idx;
+        const int w = int(r % s.W); r /= s.W;
+        const int hl = int(r % s.Hl); r /= s.Hl;
+        const int64_t t = r % s.Ls; r /= s.Ls;
+        const int b = int(r % s.B); r /= s.B;
+        const int p = int(r);
+        const int H = s.Hl * s.P;
+        const int64_t blk = idx;                                            // [P][B][Ls][Hl][W]
+        const int64_t seq = ((int64_t(b) * s.Ls + t) * H + p * s.Hl + hl) * s.W + w;   // [B][Ls][H]
+        const int64_t g = p * s.Ls + t;                                     // global token
+        const int64_t head = ((int64_t(b) * s.L + g) * s.Hl + hl) * s.W + w;  // [B][L][Hl]
+        switch (s.mode) {
+            case 0: s.dst[blk] = s.src[seq]; break;
+            case 1: if (g < s.L) s.dst[head] = s.src[blk]; break;
+            case 2: s.dst[blk] = g < s.L ? s.src[head] : make_uint4(0, 0, 0, 0); break;
+            default: s.dst[seq] = s.src[blk]; break;
+        }
+    }
+}
+
+cudaError_t launch_shuffle(const void* src, void* dst, int B, int64_t Ls, int64_t L, int Hl, int P,
+                           int d, int esize, int mode, cudaStream_t st, int* launches) {
+    if ((d * esize) % 16) return cudaErrorInvalidValue;
+    Shuffle s{static_cast<const uint4*>(src), static_cast<uint4*>(dst), B, P, Hl, d * esize / 16,
+              Ls, L, mode};
+    const int64_t total = int64_t(P) * B * Ls * Hl * s.W;
+    ulysses_kernel<<<grid_for(total, 256), 256, 0, st>>>(s);
+    if (launches) ++*launches;
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_euler(float* x, const void* v, int v_is_bf16, int64_t n, float dt,
+                         cudaStream_t s, int* launches) {
+    if (n <= 0) return cudaSuccess;
+    const unsigned grid = grid_for((n + 7) / 8, 256, 4);
+    if (v_is_bf16)
+        euler_kernel<true><<<grid, 256, 0, s>>>(x, v, n, dt);
+    else
+        euler_kernel<false><<<grid, 256, 0, s>>>(x, v, n, dt);
+    if (launches) ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_nonfinite(const void* x, int is_bf16, int64_t n, int* flag, cudaStream_t s,
+                             int* launches) {
+    if (n <= 0) return cudaSuccess;
+    const unsigned grid = grid_for(n, 256, 4);
+    if (is_bf16)
+        nonfinite_kernel<true><<<grid, 256, 0, s>>>(x, n, flag);
+    else
+        nonfinite_kernel<false><<<grid, 256, 0, s>>>(x, n, flag);
+    if (launches) ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pack_seq_to_peers(const void* src, void* dst, int B, int64_t Ls, int H, int P,
+                                     int d, int esize, cudaStream_t s, int* launches) {
+    return launch_shuffle(src, dst, B, Ls, Ls * P, H / P, P, d, esize, 0, s, launches);
+}
+cudaError_t launch_unpack_peers_to_heads(const void* src, void* dst, int B, int64_t Ls, int64_t L,
+                                         int Hl, int P, int d, int esize, cudaStream_t s,
+                                         int* launches) {
+    return launch_shuffle(src, dst, B, Ls, L, Hl, P, d, esize, 1, s, launches);
+}
+cudaError_t launch_pack_heads_to_peers(const void* src, void* dst, int B, int64_t Ls, int64_t L,
+                                       int Hl, int P, int d, int esize, cudaStream_t s,
+                                       int* launches) {
+    return launch_shuffle(src, dst, B, Ls, L, Hl, P, d, esize, 2, s, launches);
+}
+cudaError_t launch_unpack_peers_to_seq(const void* src, void* dst, int B, int64_t Ls, int H,
+                                       int P, int d, int esize, cudaStream_t s, int* launches) {
+    return launch_shuffle(src, dst, B, Ls, Ls * P, H / P, P, d, esize, 3, s, launches);
+}
+
+}  // namespace tmk

@@ -1,0 +1,52 @@
+// internal.h -- host-side declarations shared by the C-ABI (api.cpp) and the
+// kernel launchers.  Not part of the public ABI (include/tm.h is).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tmk {
+
+constexpr int kMaxSegments = 3;   // {c_0, c_{t-1}, c_t}
+
+// One contiguous K/V segment in token-major layout [B][len][H][d].
+struct Segment {
+    const void* k = nullptr;
+    const void* v = nullptr;
+    int64_t len = 0;               // tokens (0 = absent)
+};
+
+// a4: the segment schedule of one chunk-attention call.
+struct AttnProblem {
+    const void* q = nullptr;       // [B][Lq][H][d]
+    void* o = nullptr;             // [B][Lq][H][d]
+    int64_t Lq = 0;
+    int B = 1, H = 1, d = 128;     // H = heads resident on this rank
+    int nseg = 0;
+    Segment seg[kMaxSegments];
+    float scale = 0.f;             // softmax scale (1/sqrt(d), Eq 7)
+};
+
+// Launchers; return cudaSuccess or the launch error.  `launches` is
+// incremented by the number of kernels enqueued.
+cudaError_t launch_fmha_sm100(const AttnProblem& p, cudaStream_t s, int* launches);
+cudaError_t launch_fmha_fp32(const AttnProblem& p, cudaStream_t s, int* launches);
+cudaError_t launch_euler(float* x, const void* v, int v_is_bf16, int64_t n, float dt,
+                         cudaStream_t s, int* launches);
+// Non-finite check: sets *flag (device int) to 1 if any element is NaN/Inf.
+cudaError_t launch_nonfinite(const void* x, int is_bf16, int64_t n, int* flag, cudaStream_t s,
+                             int* launches);
+
+// Ulysses pack / unpack.  Token-major [B][L][H][d] <-> per-peer
+// blocks; see ulysses.cu for the exact layouts.
+cudaError_t launch_pack_seq_to_peers(const void* src, void* dst, int B, int64_t Ls, int H, int P,
+                                     int d, int esize, cudaStream_t s, int* launches);
+cudaError_t launch_unpack_peers_to_heads(const void* src, void* dst, int B, int64_t Ls,
+                                         int64_t L, int Hl, int P, int d, int esize,
+                                         cudaStream_t s, int* launches);
+cudaError_t launch_pack_heads_to_peers(const void* src, void* dst, int B, int64_t Ls, int64_t L,
+                                       int Hl, int P, int d, int esize, cudaStream_t s,
+                                       int* launches);
+cudaError_t launch_unpack_peers_to_seq(const void* src, void* dst, int B, int64_t Ls, int H,
+                                       int P, int d, int esize, cudaStream_t s, int* launches);
+
+}  // namespace tmk

@@ -1,0 +1,239 @@
+"""Thin ctypes binding of libtm.so (include/tm.h).  Argument marshalling only:
+every step of the hot path runs in the library's CUDA kernels.  PyTorch is
+used by callers for device memory, streams and process groups; this module
+accepts torch tensors (or raw integer device pointers) and passes
+data_ptr()s.  There is no CPU fallback: if libtm.so is missing or cannot be
+loaded, import fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libtm.so")
+
+TM_OK = 0
+STATUS = {0: "TM_OK", 1: "TM_ERR_INVALID_ARG", 2: "TM_ERR_SHAPE", 3: "TM_ERR_DEGENERATE_MASK",
+          4: "TM_ERR_STREAM_ORDER", 5: "TM_ERR_REF_IMMUTABLE", 6: "TM_ERR_NONFINITE",
+          7: "TM_ERR_UNSUPPORTED", 8: "TM_ERR_CUDA", 9: "TM_ERR_NCCL"}
+TM_BF16, TM_FP32 = 0, 1
+
+
+class TMError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class tm_config(ctypes.Structure):
+    _fields_ = [("heads", ctypes.c_int32), ("head_dim", ctypes.c_int32),
+                ("ref_tokens", ctypes.c_int32), ("chunk_tokens", ctypes.c_int32),
+                ("num_layers", ctypes.c_int32), ("num_steps", ctypes.c_int32),
+                ("batch", ctypes.c_int32), ("dtype", ctypes.c_int32),
+                ("softmax_scale", ctypes.c_float), ("world_size", ctypes.c_int32),
+                ("rank", ctypes.c_int32), ("device", ctypes.c_int32)]
+
+
+def make_config(heads, head_dim, ref_tokens, chunk_tokens, num_layers=1, num_steps=1, batch=1,
+                dtype=TM_BF16, softmax_scale=0.0, world_size=1, rank=0, device=0) -> tm_config:
+    return tm_config(heads, head_dim, ref_tokens, chunk_tokens, num_layers, num_steps, batch,
+                     dtype, softmax_scale, world_size, rank, device)
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libtm.so not built at {LIB_PATH}; run `python -m "
+                          f"paper_2506_03099_b200.build` (there is no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_GLOBAL)
+    P, V, S = ctypes.POINTER, ctypes.c_void_p, ctypes.c_size_t
+    i32, i64 = ctypes.c_int32, ctypes.c_int64
+    cfgp = P(tm_config)
+    sig = {
+        "tm_version": ([], i32),
+        "tm_last_error": ([], ctypes.c_char_p),
+        "tm_kvcache_bytes": ([cfgp], S),
+        "tm_workspace_bytes": ([cfgp], S),
+        "tm_get_unique_id": ([ctypes.c_char_p], i32),
+        "tm_attn_init": ([cfgp, ctypes.c_char_p, V, S, V, S, P(V)], i32),
+        "tm_attn_destroy": ([V], i32),
+        "tm_stream_reset": ([V], i32),
+        "tm_kvcache_put_reference": ([V, i32, i32, V, V, V], i32),
+        "tm_chunk_attention": ([V, i32, i32, i64, V, V, V, V, V], i32),
+        "tm_kvcache_slot_ptr": ([V, i32, i32, i64, P(V), P(V)], i32),
+        "tm_kvcache_ref_ptr": ([V, i32, i32, P(V), P(V)], i32),
+        "tm_flow_euler_step": ([V, V, V, i32, i64, ctypes.c_float, V], i32),
+        "tm_last_launch_count": ([V], i32),
+        "tm_kernel_variant": ([V], ctypes.c_char_p),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = res
+    return L
+
+
+lib = _load()
+
+EXPORTED = ("tm_version", "tm_last_error", "tm_kvcache_bytes", "tm_workspace_bytes",
+            "tm_get_unique_id", "tm_attn_init", "tm_attn_destroy", "tm_stream_reset",
+            "tm_kvcache_put_reference", "tm_chunk_attention", "tm_kvcache_slot_ptr",
+            "tm_kvcache_ref_ptr", "tm_flow_euler_step", "tm_last_launch_count",
+            "tm_kernel_variant")
+
+
+def _ptr(x):
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return x
+    return x.data_ptr()
+
+
+def _stream(s):
+    if s is None:
+        return None
+    if isinstance(s, int):
+        return s
+    return s.cuda_stream
+
+
+def _check(status):
+    if status != TM_OK:
+        raise TMError(status, lib.tm_last_error().decode())
+
+
+def tm_version() -> int:
+    return lib.tm_version()
+
+
+def tm_last_error() -> str:
+    return lib.tm_last_error().decode()
+
+
+def tm_kvcache_bytes(cfg: tm_config) -> int:
+    return lib.tm_kvcache_bytes(ctypes.byref(cfg))
+
+
+def tm_workspace_bytes(cfg: tm_config) -> int:
+    return lib.tm_workspace_bytes(ctypes.byref(cfg))
+
+
+def tm_get_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(lib.tm_get_unique_id(buf))
+    return buf.raw
+
+
+def tm_attn_init(cfg: tm_config, nccl_id, cache, cache_bytes, workspace, ws_bytes):
+    out = ctypes.c_void_p()
+    _check(lib.tm_attn_init(ctypes.byref(cfg), nccl_id, _ptr(cache), cache_bytes,
+                            _ptr(workspace), ws_bytes, ctypes.byref(out)))
+    return out.value
+
+
+def tm_attn_destroy(ctx) -> None:
+    _check(lib.tm_attn_destroy(ctx))
+
+
+def tm_stream_reset(ctx) -> None:
+    _check(lib.tm_stream_reset(ctx))
+
+
+def tm_kvcache_put_reference(ctx, layer, step, k, v, stream=None) -> None:
+    _check(lib.tm_kvcache_put_reference(ctx, layer, step, _ptr(k), _ptr(v), _stream(stream)))
+
+
+def tm_chunk_attention(ctx, layer, step, chunk, q, k, v, o, stream=None) -> None:
+    _check(lib.tm_chunk_attention(ctx, layer, step, chunk, _ptr(q), _ptr(k), _ptr(v), _ptr(o),
+                                  _stream(stream)))
+
+
+def tm_kvcache_slot_ptr(ctx, layer, step, chunk):
+    k, v = ctypes.c_void_p(), ctypes.c_void_p()
+    _check(lib.tm_kvcache_slot_ptr(ctx, layer, step, chunk, ctypes.byref(k), ctypes.byref(v)))
+    return k.value, v.value
+
+
+def tm_kvcache_ref_ptr(ctx, layer, step):
+    k, v = ctypes.c_void_p(), ctypes.c_void_p()
+    _check(lib.tm_kvcache_ref_ptr(ctx, layer, step, ctypes.byref(k), ctypes.byref(v)))
+    return k.value, v.value
+
+
+def tm_flow_euler_step(ctx, x, v, v_dtype, n, dt, stream=None) -> None:
+    _check(lib.tm_flow_euler_step(ctx, _ptr(x), _ptr(v), v_dtype, n, dt, _stream(stream)))
+
+
+def tm_last_launch_count(ctx) -> int:
+    return lib.tm_last_launch_count(ctx)
+
+
+def tm_kernel_variant(ctx) -> str:
+    return lib.tm_kernel_variant(ctx).decode()
+
+
+class ChunkAttention:
+    """Owns a tm_ctx plus torch-allocated cache and workspace (plumbing only).
+
+    Tensors passed to the methods are torch CUDA tensors in the layouts of
+    include/tm.h: q/k/v/o [B][Lc(/P)][H][d], reference k/v [B][Lr(/P)][H][d].
+    """
+
+    def __init__(self, heads, head_dim, ref_tokens, chunk_tokens, num_layers=1, num_steps=1,
+                 batch=1, dtype=TM_BF16, softmax_scale=0.0, world_size=1, rank=0, device=0,
+                 nccl_id=None):
+        import torch
+        self.cfg = make_config(heads, head_dim, ref_tokens, chunk_tokens, num_layers, num_steps,
+                               batch, dtype, softmax_scale, world_size, rank, device)
+        self.cache_bytes = tm_kvcache_bytes(self.cfg)
+        self.ws_bytes = tm_workspace_bytes(self.cfg)
+        if self.cache_bytes == 0 or self.ws_bytes == 0:
+            raise TMError(2, f"invalid config: {tm_last_error()}")
+        dev = torch.device("cuda", device)
+        # torch's caching allocator returns >= 512-B aligned blocks; over-allocate
+        # by 1 KiB and offset to honour the cache's 1024-B alignment.
+        self._cache = torch.empty(self.cache_bytes + 1024, dtype=torch.uint8, device=dev)
+        self._ws = torch.zeros(self.ws_bytes + 1024, dtype=torch.uint8, device=dev)
+        self.cache_ptr = (self._cache.data_ptr() + 1023) // 1024 * 1024
+        self.ws_ptr = (self._ws.data_ptr() + 1023) // 1024 * 1024
+        self.ctx = tm_attn_init(self.cfg, nccl_id, self.cache_ptr, self.cache_bytes,
+                                self.ws_ptr, self.ws_bytes)
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            tm_attn_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def reset(self):
+        tm_stream_reset(self.ctx)
+
+    def put_reference(self, layer, step, k, v, stream=None):
+        tm_kvcache_put_reference(self.ctx, layer, step, k, v, stream)
+
+    def attend(self, layer, step, chunk, q, k, v, o, stream=None):
+        tm_chunk_attention(self.ctx, layer, step, chunk, q, k, v, o, stream)
+        return o
+
+    def slot_ptr(self, layer, step, chunk):
+        return tm_kvcache_slot_ptr(self.ctx, layer, step, chunk)
+
+    def ref_ptr(self, layer, step):
+        return tm_kvcache_ref_ptr(self.ctx, layer, step)
+
+    def euler(self, x, v, v_dtype, dt, stream=None):
+        tm_flow_euler_step(self.ctx, x, v, v_dtype, x.numel(), dt, stream)
+
+    @property
+    def launches(self):
+        return tm_last_launch_count(self.ctx)
+
+    @property
+    def variant(self):
+        return tm_kernel_variant(self.ctx)

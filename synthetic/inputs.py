@@ -11,7 +11,7 @@ Workload recipe (SURVEY.md §8(d) value distributions)
   D2 reference-dominant: a shared unit direction u is added (x3) to q and to
      K_ref, so most attention mass sits on the cached reference segment
   D3 segment-tagged V: V_ref += 1, V_prev -= 1    (exposes a dropped segment)
-  D4 q = 0                                        (all logits equal -> closed form)
+  D4 q = 0 with D3's segment tags on V             (all logits equal -> closed form)
   D6 large magnitude: q, k scaled by 30           (max-subtraction guard)
 Shapes come from BASELINE.json configs (SURVEY.md §8 notation): WAN-2.1 512^2
 H=40, d=128, Lr=1024, Lc=3072; 720^2 Lr=2025, Lc=6075; tiny H=2, d=64, Lr=16,
@@ -97,13 +97,13 @@ def chunk_qkv(rng: np.random.Generator, L: int, H: int, d: int, dtype: str,
         q += 3.0 * shared_dir[None, :, :]
         if role == "ref":
             k += 3.0 * shared_dir[None, :, :]
-    elif dist == "D3":
+    elif dist in ("D3", "D4"):
         if role == "ref":
             v += 1.0
         elif role == "prev":
             v -= 1.0
-    elif dist == "D4":
-        q[...] = 0.0
+        if dist == "D4":
+            q[...] = 0.0
     elif dist == "D6":
         q *= 30.0
         k *= 30.0

@@ -1,0 +1,99 @@
+"""CPU-side checks of the C-ABI library: it loads, exports every symbol that
+include/tm.h declares, and its host logic (config validation, the
+closed-form cache size) works without a GPU."""
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_2506_03099_b200 import tm
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "tm.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    names = re.findall(r"\b(tm_[a-z_0-9]+)\s*\(", src)
+    return sorted(set(names))
+
+
+def test_library_exports_every_declared_symbol():
+    names = header_functions()
+    assert "tm_chunk_attention" in names and "tm_flow_euler_step" in names
+    lib = ctypes.CDLL(tm.LIB_PATH)
+    for n in names:
+        assert hasattr(lib, n), f"libtm.so does not export {n}"
+    assert set(names) == set(tm.EXPORTED)
+
+
+def test_version():
+    assert tm.tm_version() == 100
+
+
+def wan512(**kw):
+    base = dict(heads=40, head_dim=128, ref_tokens=1024, chunk_tokens=3072, num_layers=40,
+                num_steps=2)
+    base.update(kw)
+    return tm.make_config(**base)
+
+
+def test_cache_bytes_closed_form():
+    """Constant memory: ref + 2 slots of K and V per
+    (layer, step); 10.94 GiB / P at 512^2."""
+    c = wan512()
+    per_tok = 40 * 128 * 2
+    expect = 40 * 2 * (2 * 1024 * per_tok + 4 * 3072 * per_tok)
+    assert tm.tm_kvcache_bytes(c) == expect
+    assert abs(expect / 2**30 - 10.9375) < 1e-9
+    for P in (2, 4, 8):
+        assert tm.tm_kvcache_bytes(wan512(world_size=P)) == expect // P
+
+
+def test_cache_bytes_720_and_alignment():
+    c = tm.make_config(40, 128, 2025, 6075, 40, 2)
+    per_tok = 40 * 128 * 2
+    al = lambda x: (x + 1023) // 1024 * 1024
+    assert tm.tm_kvcache_bytes(c) == 80 * (2 * al(2025 * per_tok) + 4 * al(6075 * per_tok))
+
+
+@pytest.mark.parametrize("bad", [
+    dict(head_dim=96), dict(head_dim=0), dict(heads=0), dict(ref_tokens=0), dict(chunk_tokens=-1),
+    dict(world_size=3), dict(world_size=2, rank=2), dict(dtype=5), dict(num_steps=0),
+    dict(batch=0), dict(softmax_scale=-1.0)])
+def test_invalid_configs_are_rejected(bad):
+    c = wan512(**bad)
+    assert tm.tm_kvcache_bytes(c) == 0
+    assert tm.tm_workspace_bytes(c) == 0
+    with pytest.raises(tm.TMError) as e:
+        tm.tm_attn_init(c, None, 1024, 1 << 40, 1024, 1 << 20)
+    assert e.value.status in (1, 2)
+
+
+def test_workspace_sizes():
+    assert tm.tm_workspace_bytes(wan512()) == 1024
+    ws8 = tm.tm_workspace_bytes(wan512(world_size=8))
+    shard = 384 * 40 * 128 * 2          # [Lc/8][H][d] bf16
+    assert ws8 >= 1024 + 2 * 3 * shard + 2 * 3072 * 5 * 128 * 2
+
+
+def test_null_and_error_paths_without_gpu():
+    with pytest.raises(tm.TMError):
+        tm.tm_attn_init(wan512(), None, 0, 0, 0, 0)
+    # Euler argument validation happens before any launch
+    with pytest.raises(tm.TMError):
+        tm.tm_flow_euler_step(None, 0, 0, tm.TM_FP32, 10, 0.5)
+    with pytest.raises(tm.TMError):
+        tm.tm_flow_euler_step(None, 16, 16, 7, 10, 0.5)
+    tm.tm_flow_euler_step(None, 0, 0, tm.TM_FP32, 0, 0.5)   # n == 0 is a no-op
+    assert tm.tm_last_launch_count(None) == -1
+
+
+def test_init_without_device_reports_cuda_error():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(tm.TMError) as e:
+        tm.tm_attn_init(wan512(), None, 1024, 1 << 40, 1024, 1 << 20)
+    assert e.value.status == 8

@@ -1,0 +1,307 @@
+"""GPU parity: the CUDA path (through the C-ABI) vs the fp64 oracle on the
+same seeded inputs.  Tolerances (BJ.north_star): bf16 max|err| <= 2e-2 *
+max|O| (internal alarm 8e-3), fp32 validation mode <= 1e-4, Euler fp32
+<= 1e-6 * max|x|."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from gpu_util import (BF16_ALARM, BF16_TOL, FP32_TOL, dev_copy, from_dev, rel_err, sample_rows,
+                      to_dev)
+from paper_2506_03099_b200 import tm
+from synthetic import inputs as syn
+
+pytestmark = pytest.mark.gpu
+
+DT = {"bf16": tm.TM_BF16, "fp32": tm.TM_FP32}
+
+
+def run_stream(H, d, Lr, Lc, dtype, dist="D0", chunks=2, layers=1, steps=1, rows=None,
+               seed=syn.SEED_BASE, batch_check=True):
+    """Stream `chunks` chunks through every (layer, step) and compare each
+    call with the oracle's own streaming replay.  Returns the worst error."""
+    si = syn.StreamInputs(H, d, Lr, Lc, dtype, dist, seed)
+    ca = tm.ChunkAttention(H, d, Lr, Lc, layers, steps, dtype=DT[dtype])
+    so = oracle.StreamOracle()
+    for layer in range(layers):
+        for step in range(steps):
+            _, k, v = si.chunk(layer, step, 0)
+            ca.put_reference(layer, step, to_dev(k), to_dev(v))
+            so.put_reference(layer, step, k.f64, v.f64)
+    worst = 0.0
+    for t in range(1, chunks + 1):
+        for step in range(steps):
+            for layer in range(layers):
+                q, k, v = si.chunk(layer, step, t)
+                qd, kd, vd = to_dev(q), to_dev(k), to_dev(v)
+                o = torch.empty_like(qd)
+                ca.attend(layer, step, t, qd, kd, vd, o)
+                ref = so.attend(layer, step, t, q.f64, k.f64, v.f64, rows=rows)
+                got = from_dev(o)
+                if rows is not None:
+                    got = got[rows]
+                worst = max(worst, rel_err(got, ref))
+    ca.close()
+    return worst
+
+
+# ------------------------------------------------------------------ tiny (BJ.configs[0])
+
+def test_tiny_config_fp32():
+    """BJ.configs[0]: 2 heads, d=64, ref 16 tokens, 2 chunks x 32, fp32, 1 step."""
+    err = run_stream(2, 64, 16, 32, "fp32", chunks=2)
+    assert err <= FP32_TOL, err
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_tiny_config_bf16(d):
+    err = run_stream(2, d, 16, 32, "bf16", chunks=3)
+    assert err <= BF16_ALARM, err
+
+
+@pytest.mark.parametrize("dtype", ["fp32", "bf16"])
+@pytest.mark.parametrize("Lr,Lc", [(1, 1), (1, 130), (130, 1), (127, 129), (256, 128), (5, 300)])
+def test_ragged_segments(dtype, Lr, Lc):
+    """D5: segments of 1..300 tokens: partial KV tiles (masked keys must not
+    leak: SURVEY Sec 4.4 shows 5 unmasked zero keys cost 4.6e-4, caught by
+    the fp32 bar) and partial Q tiles (pad rows must not be stored)."""
+    err = run_stream(3, 128, Lr, Lc, dtype, chunks=3)
+    assert err <= (FP32_TOL if dtype == "fp32" else BF16_ALARM), err
+
+
+@pytest.mark.parametrize("dist", ["D1", "D2", "D3", "D6"])
+def test_distributions_bf16(dist):
+    err = run_stream(4, 128, 256, 640, "bf16", dist=dist, chunks=3)
+    assert err <= BF16_ALARM, (dist, err)
+
+
+@pytest.mark.parametrize("dist", ["D1", "D2", "D6"])
+def test_distributions_fp32(dist):
+    err = run_stream(2, 128, 200, 330, "fp32", dist=dist, chunks=3)
+    assert err <= FP32_TOL, (dist, err)
+
+
+def test_layers_and_steps_keep_separate_caches():
+    """K/V cached per timestep per block -- 3 layers x 2 steps, 4 chunks."""
+    err = run_stream(2, 128, 64, 192, "bf16", chunks=4, layers=3, steps=2)
+    assert err <= BF16_ALARM, err
+
+
+# ------------------------------------------------------------------ WAN-2.1 shapes
+
+def test_wan512_single_layer_bf16_sampled():
+    """BJ.configs[1]: 40 heads, d=128, Lr=1024 (one reference frame),
+    Lc=3072 (3 latent frames): chunk 1 (Lk=4096) and chunk 2 (Lk=7168)."""
+    rows = sample_rows(3072, k=40)
+    err = run_stream(40, 128, 1024, 3072, "bf16", chunks=2, rows=rows)
+    assert err <= BF16_ALARM, err
+
+
+def test_wan720_bf16_sampled():
+    """BJ.configs[4]: 720^2, 2025 tokens/frame: Lr=2025, Lc=6075 (ragged tiles)."""
+    rows = sample_rows(6075, k=24)
+    err = run_stream(40, 128, 2025, 6075, "bf16", chunks=2, rows=rows)
+    assert err <= BF16_ALARM, err
+
+
+def test_wan512_fp32_validation_sampled():
+    rows = sample_rows(3072, k=12)
+    err = run_stream(40, 128, 1024, 3072, "fp32", chunks=2, rows=rows)
+    assert err <= FP32_TOL, err
+
+
+def test_wan512_uniform_closed_form_all_rows():
+    """S:42 closed form at full size, every row: q = 0 -> O = mean of the
+    allowed V rows; segment-tagged V (D3) exposes a dropped/duplicated
+    segment.  Expected value from numpy means of the bf16 inputs."""
+    H, d, Lr, Lc = 40, 128, 1024, 3072
+    si = syn.StreamInputs(H, d, Lr, Lc, "bf16", "D4", syn.seed_for(1, 4))
+    ca = tm.ChunkAttention(H, d, Lr, Lc, 1, 1)
+    _, kr, vr = si.chunk(0, 0, 0)
+    ca.put_reference(0, 0, to_dev(kr), to_dev(vr))
+    vals = [vr.f64]
+    for t in (1, 2, 3):
+        q, k, v = si.chunk(0, 0, t)
+        o = torch.empty_like(to_dev(q))
+        ca.attend(0, 0, t, to_dev(q), to_dev(k), to_dev(v), o)
+        allowed = [vals[0]] + ([vals[-1]] if t >= 2 else []) + [v.f64]
+        mean = np.concatenate(allowed).mean(axis=0)            # [H][d]
+        got = from_dev(o)
+        err = np.abs(got - mean[None]).max() / np.abs(mean).max()
+        assert err <= BF16_TOL, (t, err)
+        vals.append(v.f64)
+    ca.close()
+
+
+# ------------------------------------------------------------------ invariants
+
+def test_deterministic_bitwise():
+    """Q15 / S:68: fixed tile order, no atomics -> bitwise identical reruns."""
+    H, d, Lr, Lc = 8, 128, 512, 1536
+    si = syn.StreamInputs(H, d, Lr, Lc, "bf16", "D0", 5)
+    outs = []
+    for _ in range(2):
+        ca = tm.ChunkAttention(H, d, Lr, Lc, 1, 1)
+        _, kr, vr = si.chunk(0, 0, 0)
+        ca.put_reference(0, 0, to_dev(kr), to_dev(vr))
+        res = []
+        for t in (1, 2, 3):
+            q, k, v = si.chunk(0, 0, t)
+            o = torch.empty_like(to_dev(q))
+            ca.attend(0, 0, t, to_dev(q), to_dev(k), to_dev(v), o)
+            res.append(o.view(torch.int16).cpu().numpy())
+        outs.append(res)
+        ca.close()
+    for a, b in zip(*outs):
+        assert (a == b).all()
+
+
+def test_reference_immutable_and_constant_footprint():
+    """reference bitwise unchanged after many chunks; the cache
+    footprint is a closed form independent of stream length; chunk 200
+    still matches the oracle."""
+    H, d, Lr, Lc = 2, 128, 128, 256
+    torch.manual_seed(syn.seed_for(9, 0))
+    ca = tm.ChunkAttention(H, d, Lr, Lc, 1, 1)
+    before = ca.cache_bytes
+    kr = torch.randn(Lr, H, d, device="cuda").bfloat16()
+    vr = torch.randn(Lr, H, d, device="cuda").bfloat16()
+    ca.put_reference(0, 0, kr, vr)
+    kp, vp = ca.ref_ptr(0, 0)
+    snap = kr.clone()
+    so = oracle.StreamOracle()
+    so.put_reference(0, 0, from_dev(kr), from_dev(vr))
+    for t in range(1, 201):
+        q, k, v = (torch.randn(Lc, H, d, device="cuda").bfloat16() for _ in range(3))
+        o = torch.empty_like(q)
+        ca.attend(0, 0, t, q, k, v, o)
+        ref = so.attend(0, 0, t, from_dev(q), from_dev(k), from_dev(v),
+                        rows=[0, 77, 255] if t < 200 else None)
+        got = from_dev(o)
+        got = got if t == 200 else got[[0, 77, 255]]
+        assert rel_err(got, ref) <= BF16_ALARM
+    torch.cuda.synchronize()
+    buf = torch.empty_like(kr)
+    dev_copy(buf.data_ptr(), kp, kr.numel() * 2)
+    assert torch.equal(buf.view(torch.int16), snap.view(torch.int16))
+    assert tm.tm_kvcache_bytes(ca.cfg) == before
+    ca.close()
+
+
+def test_stream_order_errors_on_device():
+    H, d = 2, 64
+    ca = tm.ChunkAttention(H, d, 16, 32, 2, 2)
+    q = torch.zeros(32, H, d, device="cuda", dtype=torch.bfloat16)
+    o = torch.empty_like(q)
+    r = torch.zeros(16, H, d, device="cuda", dtype=torch.bfloat16)
+    with pytest.raises(tm.TMError) as e:
+        ca.attend(0, 0, 1, q, q, q, o)                      # cache miss
+    assert e.value.status == 4
+    ca.put_reference(0, -1, r, r)                           # all steps
+    with pytest.raises(tm.TMError) as e:
+        ca.attend(0, 1, 2, q, q, q, o)                      # skipped chunk 1
+    assert e.value.status == 4
+    ca.attend(0, 1, 1, q, q, q, o)
+    ca.attend(0, 1, 1, q, q, q, o)                          # redo allowed
+    with pytest.raises(tm.TMError) as e:
+        ca.put_reference(0, 1, r, r)
+    assert e.value.status == 5
+    ca.put_reference(0, 0, r, r)                            # step 0 not started yet: allowed
+    with pytest.raises(tm.TMError) as e:
+        ca.attend(5, 0, 1, q, q, q, o)
+    assert e.value.status == 1
+    with pytest.raises(tm.TMError):
+        ca.attend(0, 0, 0, q, q, q, o)                      # chunk 0 is the reference
+    ca.reset()
+    ca.put_reference(0, 1, r, r)                            # new stream
+    ca.close()
+
+
+def test_zero_copy_append_via_slot_ptr():
+    """Writing K/V straight into tm_kvcache_slot_ptr skips the append copy
+    and gives the same result."""
+    H, d, Lr, Lc = 4, 128, 128, 384
+    si = syn.StreamInputs(H, d, Lr, Lc, "bf16", "D0", 17)
+    res = []
+    for zero_copy in (False, True):
+        ca = tm.ChunkAttention(H, d, Lr, Lc, 1, 1)
+        _, kr, vr = si.chunk(0, 0, 0)
+        ca.put_reference(0, 0, to_dev(kr), to_dev(vr))
+        outs = []
+        for t in (1, 2, 3):
+            q, k, v = si.chunk(0, 0, t)
+            kd, vd = to_dev(k), to_dev(v)
+            if zero_copy:
+                kp, vp = ca.slot_ptr(0, 0, t)
+                dev_copy(kp, kd.data_ptr(), kd.numel() * 2)
+                dev_copy(vp, vd.data_ptr(), vd.numel() * 2)
+                kd_arg, vd_arg = kp, vp
+            else:
+                kd_arg, vd_arg = kd, vd
+            o = torch.empty_like(kd)
+            ca.attend(0, 0, t, to_dev(q), kd_arg, vd_arg, o)
+            outs.append(o.view(torch.int16).cpu().numpy())
+        res.append(outs)
+        ca.close()
+    for a, b in zip(*res):
+        assert (a == b).all()
+
+
+def test_launch_count_and_variant():
+    ca = tm.ChunkAttention(2, 128, 128, 128, 1, 1)
+    assert ca.variant == "sm100_tcgen05"
+    x = torch.zeros(128, 2, 128, device="cuda", dtype=torch.bfloat16)
+    ca.put_reference(0, 0, x, x)
+    o = torch.empty_like(x)
+    ca.attend(0, 0, 1, x, x, x, o)
+    assert ca.launches == 1
+    ca.close()
+    cf = tm.ChunkAttention(2, 64, 16, 32, 1, 1, dtype=tm.TM_FP32)
+    assert cf.variant == "fp32_simt"
+    cf.close()
+
+
+# ------------------------------------------------------------------ Euler (a7)
+
+@pytest.mark.parametrize("v_dtype", ["fp32", "bf16"])
+@pytest.mark.parametrize("n", [1, 7, 8, 1000, 196_608, 388_800 + 3])
+def test_euler_vs_oracle(v_dtype, n):
+    """x <- x + dt*v: fp32 single-FMA vs the fp64 oracle,
+    <= 1e-6 * max|x|."""
+    x, v = syn.euler_inputs(n, syn.seed_for(7, 0), v_dtype)
+    xd, vd = to_dev(x), to_dev(v)
+    for dt in (1.0, 0.5, -0.125):
+        ref = oracle.euler(from_dev(xd), v.f64, dt)
+        tm.tm_flow_euler_step(None, xd, vd, DT[v_dtype], n, dt)
+        torch.cuda.synchronize()
+        got = from_dev(xd)
+        assert np.abs(got - ref).max() <= 1e-6 * np.abs(ref).max()
+
+
+def test_euler_constant_velocity_closed_form():
+    """constant velocity c, N Euler steps of 1/N -> x0 + c."""
+    n = 4096
+    for N in (1, 2, 12, 24):
+        x = torch.full((n,), 0.25, device="cuda")
+        c = torch.full((n,), 3.0, device="cuda")
+        for _ in range(N):
+            tm.tm_flow_euler_step(None, x, c, tm.TM_FP32, n, 1.0 / N)
+        torch.cuda.synchronize()
+        assert torch.allclose(x, torch.full_like(x, 3.25), rtol=0, atol=1e-5 * N)
+
+
+def test_euler_rectified_flow_identity():
+    """Eqs 1-2: from x_t = t x1 + (1-t) x0 one step of dt along v = x1 - x0
+    lands on x_{t+dt} (to fp32 rounding)."""
+    n = 10_000
+    rng = np.random.default_rng(3)
+    x0, x1 = rng.standard_normal(n), rng.standard_normal(n)
+    for t, dt in [(0.0, 1.0), (0.0, 0.5), (0.5, 0.5)]:
+        xt = oracle.interpolate(x0, x1, t).astype(np.float32)
+        v = oracle.velocity_target(x0, x1).astype(np.float32)
+        xd, vd = torch.from_numpy(xt).cuda(), torch.from_numpy(v).cuda()
+        tm.tm_flow_euler_step(None, xd, vd, tm.TM_FP32, n, dt)
+        torch.cuda.synchronize()
+        target = oracle.interpolate(x0, x1, t + dt)
+        assert np.abs(xd.double().cpu().numpy() - target).max() < 1e-5
