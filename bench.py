@@ -1,0 +1,382 @@
+#!/usr/bin/env python
+"""Benchmark of the sparse-causal chunk-attention hot path (BASELINE.json metric:
+"chunk-attention TFLOP/s & ms/chunk (frac of bf16 peak) at 1/2/4/8 B200").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl tm|reference]
+                    [--config wan512|wan720]
+
+Workload (BASELINE.json configs[1]; configs[2] for N > 1): one WAN-2.1-14B-
+shaped attention layer, H=40, d=128, 512x512 video -> 1024 tokens per latent
+frame, reference c_0 = 1 latent frame (Lr=1024), chunk = 3 latent frames
+(Lc=3072), chunk index t >= 2 so the attend set is {c_0, c_{t-1}, c_t}
+(Lk = 7168; Eq 7).  FLOP per call = 4*Lc*Lk*d*H = 450.97 GFLOP
+(algorithmic: allowed keys only, QK^T + PV).
+
+One STEP = one pass of the hot path over one chunk at one (layer, step):
+  a2/a3 (Ulysses exchange for N>1 / K,V append into cache slot t&1)
+  a4    mask -> segment schedule
+  a5    tcgen05 attention over {c_0, c_{t-1}, c_t}
+  a6    (N>1) head -> seq exchange of O
+  a7    flow-matching Euler update of the chunk latent (16 x 3 x 64 x 64)
+The reference K/V (a1) is written once per stream per (layer, step) in setup,
+as the paper caches it.  Steps rotate over 8 layers' caches and 4
+input sets (~210 MB touched per step, > 126 MB L2), so every step reads its
+operands from HBM ("inputs larger than L2").
+
+N > 1: heads are sharded across ranks (H/N per rank), each rank passes its
+sequence shard [Lc/N][H][d]; the library runs the Ulysses all-to-all (NCCL)
+in and out.  Total work is fixed -> "scaling": "strong".
+
+--impl reference: the fp64 CPU oracle (oracle/) timed on the host cores on a
+bounded row sample of the same workload (this tier has no reference code).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "chunk-attention TFLOP/s & ms/chunk (frac of bf16 peak) at 1/2/4/8 B200"
+CONFIGS = {
+    "wan512": dict(H=40, d=128, Lr=1024, Lc=3072, latent=16 * 3 * 64 * 64,
+                   workload="WAN-2.1-14B-shaped single layer, 512x512 (1024 tok/frame), "
+                            "chunk t>=2 = 3 latent frames + cached reference frame + previous chunk"),
+    "wan720": dict(H=40, d=128, Lr=2025, Lc=6075, latent=16 * 3 * 90 * 90,
+                   workload="WAN-2.1-14B-shaped single layer, 720x720 (2025 tok/frame), "
+                            "chunk t>=2 = 3 latent frames + cached reference frame + previous chunk"),
+}
+FALLBACK_PEAK_TFLOPS = 1590.0     # /opt/skills/guides/B200_PROFILING.md fallback
+
+
+def flop_per_call(c, t=2):
+    Lk = c["Lr"] + (2 if t >= 2 else 1) * c["Lc"]
+    return 4.0 * c["Lc"] * Lk * c["d"] * c["H"]
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            j = json.load(f)
+        return float(j["bf16_tflops"]), float(j.get("bf16_tflops_sustained", 0)), "measured"
+    except Exception:
+        return FALLBACK_PEAK_TFLOPS, None, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index):
+        self.dev = device_index
+        self.proc = None
+        self.tmp = None
+
+    def start(self):
+        try:
+            self.tmp = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.dev}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=self.tmp, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.tmp.flush()
+        self.tmp.seek(0)
+        rows = [r.split(",") for r in self.tmp.read().strip().splitlines() if r.strip()]
+        os.unlink(self.tmp.name)
+        sm, smax, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[1]))
+                smax = max(smax, float(r[2]))
+                for nm, val in zip(names, r[5:9]):
+                    if "Active" in val and "Not" not in val:
+                        reasons.add(nm)
+            except Exception:
+                continue
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- reference arm
+
+def run_oracle_sample(c, rows, seed):
+    """Oracle (fp64 C, OpenMP) on `rows` query rows x all heads of one t>=2
+    call; returns (seconds, flop, threads)."""
+    import numpy as np
+    import oracle
+    from synthetic import inputs as syn
+    si = syn.StreamInputs(c["H"], c["d"], c["Lr"], c["Lc"], "bf16", "D0", seed)
+    _, kr, vr = si.chunk(0, 0, 0)
+    _, kp, vp = si.chunk(0, 0, 1)
+    q, kc, vc = si.chunk(0, 0, 2)
+    r = np.linspace(0, c["Lc"] - 1, rows).astype(np.int64)
+    t0 = time.perf_counter()
+    oracle.stream_attention(q.f64, kr.f64, vr.f64, kp.f64, vp.f64, kc.f64, vc.f64, rows=r)
+    dt = time.perf_counter() - t0
+    Lk = c["Lr"] + 2 * c["Lc"]
+    return dt, 4.0 * rows * Lk * c["d"] * c["H"], oracle.num_threads()
+
+
+def reference_arm(args, c):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    rows = args.oracle_rows
+    times, flops = [], 0.0
+    threads = 0
+    for s in range(args.warmup):
+        run_oracle_sample(c, max(8, rows // 8), 11 + s)
+    for s in range(args.steps):
+        dt, fl, threads = run_oracle_sample(c, rows, 100 + s)
+        times.append(dt)
+        flops = fl
+    total = sum(times)
+    value = flops * args.steps / total / 1e12
+    sample = (f"{rows} query rows x {c['H']} heads of one t>=2 call (Lk={c['Lr'] + 2 * c['Lc']}), "
+              f"per step; fp64 two-pass softmax over the literal concatenation")
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s",
+           "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": c["workload"], "heads": c["H"], "head_dim": c["d"],
+                      "ref_tokens": c["Lr"], "chunk_tokens": c["Lc"], "chunk_index": 2},
+           "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": threads, "kind": "oracle",
+                            "sample": sample},
+           "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+
+
+# ----------------------------------------------------------------------------- tm arm
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=40)
+    ap.add_argument("--warmup", type=int, default=8)
+    ap.add_argument("--impl", default="tm", choices=["tm", "reference"])
+    ap.add_argument("--config", default="wan512", choices=sorted(CONFIGS))
+    ap.add_argument("--layers", type=int, default=8, help="layer caches rotated over")
+    ap.add_argument("--oracle-rows", type=int, default=256)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    c = CONFIGS[args.config]
+    if args.impl == "reference":
+        reference_arm(args, c)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2506_03099_b200 import tm
+
+    H, d, Lr, Lc = c["H"], c["d"], c["Lr"], c["Lc"]
+    P = world
+    Lc_s, Lr_s = -(-Lc // P), -(-Lr // P)
+    NL = args.layers
+    nccl_id = None
+    if P > 1:
+        obj = [tm.tm_get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    ca = tm.ChunkAttention(H, d, Lr, Lc, num_layers=NL, num_steps=1, world_size=P, rank=rank,
+                           device=local, nccl_id=nccl_id)
+    stream = torch.cuda.current_stream()
+    g = torch.Generator(device="cuda").manual_seed(2506030990 + 1000 + rank)
+    bf = torch.bfloat16
+    NB = 4
+    sets = [[torch.randn(Lc_s, H, d, device="cuda", dtype=bf, generator=g) for _ in range(3)]
+            for _ in range(NB)]
+    outs = [torch.empty(Lc_s, H, d, device="cuda", dtype=bf) for _ in range(NB)]
+    xlat = torch.randn(c["latent"], device="cuda", generator=g)
+    vlat = torch.randn(c["latent"], device="cuda", generator=g).to(bf)
+    kref = torch.randn(Lr_s, H, d, device="cuda", dtype=bf, generator=g)
+    vref = torch.randn(Lr_s, H, d, device="cuda", dtype=bf, generator=g)
+    for layer in range(NL):                                    # a1, once per stream
+        ca.put_reference(layer, 0, kref, vref, stream)
+    chunk = [0] * NL
+    launches = [0]
+
+    def step(i, zero_copy=False):
+        layer = i % NL
+        chunk[layer] += 1
+        q, k, v = sets[i % NB]
+        o = outs[i % NB]
+        if zero_copy:
+            k, v = ca.slot_ptr(layer, 0, chunk[layer])
+        ca.attend(layer, 0, chunk[layer], q, k, v, o, stream)
+        n = ca.launches
+        ca.euler(xlat, vlat, tm.TM_BF16, 0.5, stream)
+        launches[0] += n + ca.launches
+
+    for i in range(NL):                                        # chunk 1 of every layer
+        step(i)
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if P > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if P == 1:
+            return x
+        t = torch.tensor([x], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---------------------------------------------------------------- main timed region
+    clocks = ClockSampler(local)
+    clocks.start()
+    launches[0] = 0
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(args.steps):
+        step(i)
+    e1.record(stream)
+    barrier()
+    ms_total = max_over_ranks(e0.elapsed_time(e1))
+    clk = clocks.stop()
+    gpu_launches = launches[0]
+
+    # ---------------------------------------------------------------- attention kernel alone
+    # K/V pre-placed in the cache slot (zero-copy append) so each call is one
+    # attention-kernel launch; per-call CUDA events on the launching stream.
+    kev = []
+    barrier()
+    for i in range(args.steps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        layer = i % NL
+        chunk[layer] += 1
+        q = sets[i % NB][0]
+        kp, vp = ca.slot_ptr(layer, 0, chunk[layer])
+        a.record(stream)
+        ca.attend(layer, 0, chunk[layer], q, kp, vp, outs[i % NB], stream)
+        b.record(stream)
+        kev.append((a, b))
+    barrier()
+    k_ms = max_over_ranks(statistics.mean(a.elapsed_time(b) for a, b in kev))
+
+    # ---------------------------------------------------------------- end to end, host buffers
+    e2e = None
+    if not args.no_e2e:
+        hq = [t.cpu().pin_memory() for t in sets[0]]
+        ho = torch.empty(Lc_s, H, d, dtype=bf).pin_memory()
+        hx = xlat.cpu().pin_memory()
+        hv = vlat.cpu().pin_memory()
+        dq = [torch.empty_like(t) for t in sets[0]]
+        dx, dv = torch.empty_like(xlat), torch.empty_like(vlat)
+        h2d = sum(t.numel() * t.element_size() for t in hq) + hx.numel() * 4 + hv.numel() * 2
+        d2h = ho.numel() * 2 + hx.numel() * 4
+        ke = max(3, min(args.steps, 10))
+        barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for i in range(ke):
+            layer = i % NL
+            chunk[layer] += 1
+            for dst, src in zip(dq, hq):
+                dst.copy_(src, non_blocking=True)
+            dx.copy_(hx, non_blocking=True)
+            dv.copy_(hv, non_blocking=True)
+            ca.attend(layer, 0, chunk[layer], dq[0], dq[1], dq[2], outs[0], stream)
+            ca.euler(dx, dv, tm.TM_BF16, 0.5, stream)
+            ho.copy_(outs[0], non_blocking=True)
+            hx.copy_(dx, non_blocking=True)
+        b.record(stream)
+        barrier()
+        e_ms = max_over_ranks(a.elapsed_time(b)) / ke
+        e2e = {"value": flop_per_call(c) / (e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+               "ms_per_step": e_ms, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h)}
+
+    fl = flop_per_call(c)
+    ms_step = ms_total / args.steps
+    value = fl * args.steps / (ms_total * 1e-3) / 1e12
+    peak, peak_sus, peak_src = measured_peaks()
+    achieved = fl / (k_ms * 1e-3) / 1e12
+    prof = os.path.join(ROOT, "profiles", "ncu_fmha_traffic.json")
+    traffic = None
+    try:
+        with open(prof) as f:
+            pj = json.load(f)
+        if pj.get("config") == args.config and pj.get("n_gpus") == P:
+            traffic = pj.get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    cpu = None
+    if rank == 0 and P == 1 and not args.no_cpu_baseline:
+        dt, sfl, th = run_oracle_sample(c, args.oracle_rows, 7)
+        cpu = {"value": sfl / dt / 1e12, "unit": "TFLOP/s", "cores": th, "kind": "oracle",
+               "sample": f"{args.oracle_rows} query rows x {H} heads of one t>=2 call "
+                         f"(Lk={Lr + 2 * Lc}); {dt:.1f} s"}
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": P,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": c["workload"], "heads": H, "head_dim": d, "ref_tokens": Lr,
+                       "chunk_tokens": Lc, "chunk_index": ">=2", "keys_attended": Lr + 2 * Lc,
+                       "gflop_per_chunk_attention": fl / 1e9, "euler_elements": c["latent"],
+                       "parallelism": f"ulysses-heads{P}" if P > 1 else "single-gpu",
+                       "l2": "inputs larger than L2 (8 layer caches x 4 input sets rotated)"},
+            "ms_per_chunk_attention": k_ms,
+            "frac_of_bf16_peak": achieved / peak,
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak,
+                         "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "tm_fmha_sm100 (tcgen05)", "peak_source": f"{peak_src} bf16 burst",
+                         "flop_per_launch": fl},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": gpu_launches,
+            "clocks": clk,
+        }
+        print(json.dumps(out))
+    ca.close()
+    if P > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -7,6 +7,9 @@
 // memory; lane j computes the logit of key j, and the online softmax's row
 // max / row sum are warp-shuffle reductions; for P.V each lane owns d/32
 // output dims and key j's probability is broadcast with __shfl_sync.
+// The logit q.k is a compensated (Ogita-Rump-Oishi "Dot2") fp32 dot product:
+// with |logits| ~ 1e3 (distribution D6) a plain fp32 FMA chain loses ~6e-4
+// of the softmax weights' relative accuracy, which would miss the 1e-4 bar.
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -91,13 +94,29 @@ __global__ void __launch_bounds__(kWarps * 32) fmha_fp32_kernel(const Fp32Params
 #pragma unroll
             for (int r = 0; r < kRowsPerWarp; ++r) {
                 const int rr = warp * kRowsPerWarp + r;
-                float dot = 0.f;
+                // Dot2: s + c carries the dot product to ~twice fp32 precision.
+                float sum = 0.f, comp = 0.f;
 #pragma unroll 16
-                for (int c = 0; c < D; ++c) dot = fmaf(sq[rr][c], sk[lane][c], dot);
-                const float sc = key_ok ? dot * p.scale : -INFINITY;
-                const float m_new = fmaxf(m[r], warp_max(sc));
+                for (int c = 0; c < D; ++c) {
+                    const float a = sq[rr][c], bk = sk[lane][c];
+                    // _rn intrinsics: never contracted into FMAs, so the
+                    // error-free transformations stay exact.
+                    const float pr = __fmul_rn(a, bk);
+                    const float pe = fmaf(a, bk, -pr);                  // TwoProduct error
+                    const float t = __fadd_rn(sum, pr);                 // TwoSum
+                    const float z = __fsub_rn(t, sum);
+                    comp = __fadd_rn(comp, __fadd_rn(__fadd_rn(__fsub_rn(sum, __fsub_rn(t, z)),
+                                                               __fsub_rn(pr, z)), pe));
+                    sum = t;
+                }
+                // logit = hi + lo (unevaluated pair); the running max uses hi
+                // and exp() sees (hi - m) + lo, so |logit| ~ 1e3 keeps ~1e-7
+                // relative accuracy in the weights.
+                const float hi = key_ok ? __fmul_rn(sum, p.scale) : -INFINITY;
+                const float lo = key_ok ? fmaf(sum, p.scale, -hi) + comp * p.scale : 0.f;
+                const float m_new = fmaxf(m[r], warp_max(hi));
                 const float alpha = expf(m[r] - m_new);     // m = -inf at start -> 0
-                const float pj = expf(sc - m_new);
+                const float pj = expf(__fadd_rn(__fsub_rn(hi, m_new), lo));
                 l[r] = l[r] * alpha + warp_sum(pj);
                 m[r] = m_new;
 #pragma unroll
