@@ -1,0 +1,121 @@
+#!/usr/bin/env python
+"""Summarise an `ncu --set full` report (.ncu-rep) and/or an ncu launch list
+(--metrics gpu__time_duration.sum --csv) into profiles/.
+
+    python tools/ncu_summary.py --rep gpurun_out/prof.ncu-rep --launches gpurun_out/launches.csv \
+        --tag r1_v1 [--config wan512 --n-gpus 1 --flop 450.97e9 --algo-bytes 209.7e6]
+"""
+import argparse
+import csv
+import io
+import json
+import os
+import subprocess
+from collections import defaultdict
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+KEYS = [
+    "gpu__time_duration.sum",
+    "sm__cycles_elapsed.avg.per_second",
+    "dram__bytes_read.sum",
+    "dram__bytes_write.sum",
+    "lts__t_sector_hit_rate.pct",
+    "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+    "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+    "smsp__issue_active.avg.pct_of_peak_sustained_active",
+    "launch__registers_per_thread",
+    "launch__grid_size",
+    "launch__block_size",
+    "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_wait_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_math_pipe_throttle_per_issue_active.ratio",
+    "local_load_bytes", "local_store",
+]
+
+
+def to_bytes(v, unit):
+    v = float(v)
+    return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
+
+
+def summarise_rep(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr, units = rows[0], rows[1]
+    kernels = []
+    for vals in rows[2:]:
+        d = {}
+        for h, u, v in zip(hdr, units, vals):
+            if h in ("Kernel Name",) or any(h == k or h.startswith(k) for k in KEYS):
+                d[h] = (v, u)
+        kernels.append(d)
+    return kernels
+
+
+def summarise_launches(path):
+    rows = list(csv.reader(open(path)))
+    hdr, data = None, []
+    for r in rows:
+        if r and r[0] == "ID":
+            hdr = r
+            continue
+        if hdr and len(r) == len(hdr):
+            data.append(dict(zip(hdr, r)))
+    agg = defaultdict(lambda: [0, 0.0])
+    for d in data:
+        if d["Metric Name"] == "gpu__time_duration.sum":
+            scale = {"ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3}.get(d["Metric Unit"], 1e-3)
+            k = d["Kernel Name"]
+            agg[k][0] += 1
+            agg[k][1] += float(d["Metric Value"]) * scale
+    tot = sum(v[1] for v in agg.values())
+    return [{"kernel": k, "launches": v[0], "total_us": v[1], "mean_us": v[1] / v[0],
+             "share": v[1] / tot} for k, v in sorted(agg.items(), key=lambda x: -x[1][1])]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--rep")
+    ap.add_argument("--launches")
+    ap.add_argument("--tag", required=True)
+    ap.add_argument("--kernel", default="fmha_sm100")
+    ap.add_argument("--config", default="wan512")
+    ap.add_argument("--n-gpus", type=int, default=1)
+    ap.add_argument("--flop", type=float, default=450.97156608e9)
+    ap.add_argument("--algo-bytes", type=float, default=209.7e6)
+    a = ap.parse_args()
+    prof = os.path.join(ROOT, "profiles")
+    os.makedirs(prof, exist_ok=True)
+    summary = {"tag": a.tag}
+    if a.launches:
+        summary["launches"] = summarise_launches(a.launches)
+    if a.rep:
+        ks = summarise_rep(a.rep)
+        summary["ncu_full"] = ks
+        for k in ks:
+            if a.kernel in k.get("Kernel Name", ("",))[0]:
+                rd = to_bytes(*k["dram__bytes_read.sum"])
+                wr = to_bytes(*k["dram__bytes_write.sum"])
+                t_us = float(k["gpu__time_duration.sum"][0]) * (1e-3 if k["gpu__time_duration.sum"][1] == "nsecond" else 1.0)
+                traffic = {"config": a.config, "n_gpus": a.n_gpus, "tag": a.tag,
+                           "dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
+                           "algorithmic_bytes": a.algo_bytes,
+                           "ncu_duration_us": t_us,
+                           "note": "one `ncu --set full --clock-control none` capture of one launch"}
+                with open(os.path.join(prof, "ncu_fmha_traffic.json"), "w") as f:
+                    json.dump(traffic, f, indent=1)
+                summary["traffic"] = traffic
+                break
+    with open(os.path.join(prof, f"{a.tag}_ncu_summary.json"), "w") as f:
+        json.dump(summary, f, indent=1)
+    print(json.dumps({k: v for k, v in summary.items() if k != "ncu_full"}, indent=1)[:3000])
+
+
+if __name__ == "__main__":
+    main()
