@@ -68,7 +68,7 @@ struct Layout {
     int esize, Hl, P;
     int64_t Lr, Lc, Lr_s, Lc_s;     // full and per-rank shard token counts
     size_t ref_bytes, slot_bytes, region_bytes, cache_bytes;
-    size_t flag_bytes, xfer_bytes, head_bytes, ws_bytes;
+    size_t flag_bytes, scratch_bytes, xfer_bytes, head_bytes, ws_bytes;
 };
 
 Layout layout_of(const tm_config* c) {
@@ -86,15 +86,16 @@ Layout layout_of(const tm_config* c) {
     L.region_bytes = 2 * L.ref_bytes + 4 * L.slot_bytes;          // Kref Vref K0 V0 K1 V1
     L.cache_bytes = L.region_bytes * size_t(c->num_layers) * size_t(c->num_steps);
     L.flag_bytes = kAlign;
+    L.scratch_bytes = c->dtype == TM_BF16 ? align_up(fmha_sm100_scratch_bytes(c->head_dim)) : 0;
     if (L.P > 1) {
         const size_t full_row = size_t(c->heads) * c->head_dim * L.esize;
         const size_t qkv = 3 * align_up(size_t(c->batch) * L.Lc_s * full_row);
         const size_t kv = 2 * align_up(size_t(c->batch) * L.Lr_s * full_row);
         L.xfer_bytes = qkv > kv ? qkv : kv;
         L.head_bytes = L.slot_bytes;                               // Q or O, [B][Lc][Hl][d]
-        L.ws_bytes = L.flag_bytes + 2 * L.xfer_bytes + 2 * L.head_bytes;
+        L.ws_bytes = L.flag_bytes + L.scratch_bytes + 2 * L.xfer_bytes + 2 * L.head_bytes;
     } else {
-        L.ws_bytes = L.flag_bytes;
+        L.ws_bytes = L.flag_bytes + L.scratch_bytes;
     }
     return L;
 }
@@ -124,7 +125,8 @@ struct tm_ctx {
     }
     uint8_t* vslot(int l, int s, int64_t t) const { return kslot(l, s, t) + lay.slot_bytes; }
     int* flag() const { return reinterpret_cast<int*>(ws); }
-    uint8_t* send() const { return ws + lay.flag_bytes; }
+    uint8_t* scratch() const { return ws + lay.flag_bytes; }
+    uint8_t* send() const { return scratch() + lay.scratch_bytes; }
     uint8_t* recv() const { return send() + lay.xfer_bytes; }
     uint8_t* qh() const { return recv() + lay.xfer_bytes; }
     uint8_t* oh() const { return qh() + lay.head_bytes; }
@@ -252,6 +254,11 @@ tm_status tm_attn_init(const tm_config* cfg, const uint8_t* nccl_id, void* cache
     c->scale = cfg->softmax_scale > 0.f ? cfg->softmax_scale : 1.0f / std::sqrt(float(cfg->head_dim));
     c->last.assign(size_t(cfg->num_layers) * cfg->num_steps, 0);
     c->ref_ok.assign(size_t(cfg->num_layers) * cfg->num_steps, 0);
+    // The split-KV scratch (merge counters) must start zeroed; kernels leave it zeroed.
+    if (cudaMemset(c->ws, 0, L.ws_bytes) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) {
+        delete c;
+        return fail(TM_ERR_CUDA, "workspace initialisation failed");
+    }
     const char* dbg = getenv("TM_DEBUG");
     c->debug = dbg && *dbg && strcmp(dbg, "0") != 0;
     if (cfg->world_size > 1) {
@@ -404,7 +411,7 @@ tm_status tm_chunk_attention(tm_ctx* ctx, int32_t layer, int32_t step, int64_t c
                                     ctx->vslot(layer, step, chunk - 1), Ly.Lc};
     pr.seg[pr.nseg++] = Segment{kslot, vslot, Ly.Lc};
 
-    cudaError_t e = cf.dtype == TM_BF16 ? launch_fmha_sm100(pr, cs, &ctx->launches)
+    cudaError_t e = cf.dtype == TM_BF16 ? launch_fmha_sm100(pr, ctx->scratch(), cs, &ctx->launches)
                                         : launch_fmha_fp32(pr, cs, &ctx->launches);
     st = cuda_check(e, "attention kernel launch");
     if (st) return st;

@@ -8,9 +8,16 @@
 // c_t); every other chunk is never touched.  Ragged segment tails are
 // masked to -inf by key index.
 //
-// Blackwell design (one CTA = one head x two 128-row Q tiles):
-//   warp 8      TMA producer: Q0,Q1 once, then K_j / V_j tiles through a
-//               4-slot shared-memory ring (cp.async.bulk.tensor, 128B swizzle)
+// Blackwell design.  Work unit = (batch, head, pair of 128-row Q tiles).
+// PERSISTENT grid of min(#SMs, 160) CTAs, one per SM: CTA c runs units c,
+// c+C, ... (whole); the T = U mod C tail units are split along the KV axis
+// into S = C/T pieces so the last wave fills the machine (split-KV tail);
+// the last piece of a unit to finish merges the pieces' (O, m, l) in fixed
+// piece order (deterministic, no floating-point atomics).
+// Warp roles (384 threads; setmaxnreg gives the softmax warpgroups 232 regs):
+//   warp 8      TMA producer: Q_i per unit (reloaded per tile as soon as its
+//               last S MMA completes), K_j / V_j through a 4-slot smem ring
+//               (cp.async.bulk.tensor, 128B swizzle).
 //   warp 9      tcgen05 MMA issuer (one thread) + TMEM owner:
 //                 S_i = Q_i K_j^T  (SS, M=128 N=128 K=d, fp32 in TMEM)
 //                 O_i += P_i V_j   (TS: P_i bf16 read from TMEM, V MN-major)
@@ -18,11 +25,14 @@
 //               works on one tile while the other tile's softmax runs.
 //   warps 0-7   softmax, one warpgroup per Q tile, one thread per query row
 //               (tcgen05.ld 32x32b puts a whole S row in one thread's
-//               registers, so row max/sum need no shuffles); exp2 with the
-//               scale*log2(e) folded into one FFMA; conditional O rescale
-//               (only when the running max grows by > 8 in log2 units --
-//               exact after the final 1/l); P rounded to bf16 (RNE) and
-//               stored back into TMEM over S_i; epilogue O/l -> bf16.
+//               registers): 3-input-max tree, exp2 with scale*log2(e) folded
+//               into one packed FFMA2, 62.5% of the exponentials on the MUFU
+//               pipe and 37.5% as a degree-3 polynomial on the FMA pipe (the
+//               MUFU rate equals the tensor rate at d=128), packed FADD2 row
+//               sums, conditional O rescale (only when the running max grows
+//               by > 8 in log2 units -- exact after the final 1/l), P rounded
+//               to bf16 (RNE) and stored back into TMEM over S_i; epilogue
+//               O/l -> bf16 (or the unnormalised partial for split pieces).
 // TMEM: S0 [0,128) S1 [128,256) O0 [256,256+d) O1 [256+d, 256+2d).
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -31,6 +41,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstring>
 #include <mutex>
 
 #include "internal.h"
@@ -42,7 +53,9 @@ namespace {
 constexpr int kBM = 128;          // query rows per Q tile
 constexpr int kBN = 128;          // keys per KV tile
 constexpr int kStages = 4;        // K/V smem ring slots
-constexpr int kThreads = 320;     // 8 softmax warps + TMA warp + MMA warp
+constexpr int kThreads = 384;     // 2 softmax warpgroups + {TMA, MMA, 2 spare} warpgroup
+constexpr int kRegsSoftmax = 224; // setmaxnreg budgets: 256 x 224 + 128 x 64 <= 64K
+constexpr int kRegsOther = 64;
 constexpr int kHalfBytes = 128 * 128;   // one 64-column (128 B) half of a 128-row tile
 
 struct __align__(64) FmhaParams {
@@ -52,11 +65,48 @@ struct __align__(64) FmhaParams {
     int seg_tile_start[kMaxSegments + 1];
     int seg_len[kMaxSegments];
     int nseg;
-    int n_tiles;
+    int n_tiles;                      // KV tiles of a whole unit
     int Lq, H, B;
     float scale_log2;                 // softmax scale * log2(e)
     uint16_t* o;                      // bf16 bits [B][Lq][H][d]
+    // persistent schedule
+    int n_qpairs;                     // Q-tile pairs per (b, h)
+    int whole_items;                  // R * C: items that are whole units
+    int tail_pieces;                  // T * S
+    int splits;                       // S
+    float* part;                      // split partials: per piece [d/4][256] float4 + m[256] + l[256]
+    int* counters;                    // per tail unit, zero between launches
 };
+
+struct Item {
+    int b, h, qp, lo, hi, piece, tail_unit, split;
+};
+
+__device__ __forceinline__ bool get_item(const FmhaParams& p, int w, Item& it) {
+    int unit;
+    if (w < p.whole_items) {
+        unit = w;
+        it.lo = 0;
+        it.hi = p.n_tiles;
+        it.piece = 0;
+        it.tail_unit = 0;
+        it.split = 0;
+    } else {
+        const int pw = w - p.whole_items;
+        if (pw >= p.tail_pieces) return false;
+        it.tail_unit = pw / p.splits;
+        it.split = pw % p.splits;
+        unit = p.whole_items + it.tail_unit;
+        it.lo = int((long long)it.split * p.n_tiles / p.splits);
+        it.hi = int((long long)(it.split + 1) * p.n_tiles / p.splits);
+        it.piece = p.splits > 1;
+    }
+    it.qp = unit % p.n_qpairs;
+    const int bh = unit / p.n_qpairs;
+    it.h = bh % p.H;
+    it.b = bh / p.H;
+    return true;
+}
 
 __device__ __forceinline__ void tile_info(const FmhaParams& p, int j, int& seg, int& row,
                                           int& valid) {
@@ -66,6 +116,58 @@ __device__ __forceinline__ void tile_info(const FmhaParams& p, int j, int& seg, 
         if (s < p.nseg && j >= p.seg_tile_start[s]) seg = s;
     row = (j - p.seg_tile_start[seg]) * kBN;
     valid = min(kBN, p.seg_len[seg] - row);
+}
+
+__device__ __forceinline__ float max3(float a, float b, float c) {
+    float d;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+    return d;
+}
+__device__ __forceinline__ uint64_t f2u(float2 a) { return *reinterpret_cast<uint64_t*>(&a); }
+__device__ __forceinline__ float2 u2f(uint64_t a) { return *reinterpret_cast<float2*>(&a); }
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+    uint64_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(f2u(a)), "l"(f2u(b)), "l"(f2u(c)));
+    return u2f(d);
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+    uint64_t d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2u(a)), "l"(f2u(b)));
+    return u2f(d);
+}
+
+// 2^x for a pair, on the FMA pipe: x = n + f, n = rint(x), f in [-0.5, 0.5];
+// 2^f by a degree-3 minimax polynomial (max rel. error 8.0e-5, far below
+// the bf16 rounding of P); 2^n inserted into the exponent field.  x is
+// clamped at -125 (result stays a normal float; 2^-125 is ~0 for softmax).
+__device__ __forceinline__ float2 exp2_poly2(float2 x) {
+    constexpr float kMagic = 12582912.f;    // 1.5 * 2^23: round-to-nearest trick
+    x.x = fmaxf(x.x, -125.f);
+    x.y = fmaxf(x.y, -125.f);
+    const float2 j = fadd2(x, make_float2(kMagic, kMagic));
+    const float2 n = fadd2(j, make_float2(-kMagic, -kMagic));
+    const float2 f = ffma2(n, make_float2(-1.f, -1.f), x);
+    float2 p = ffma2(make_float2(0.055171094834804535f, 0.055171094834804535f), f,
+                     make_float2(0.24260999262332916f, 0.24260999262332916f));
+    p = ffma2(p, f, make_float2(0.6932609677314758f, 0.6932609677314758f));
+    p = ffma2(p, f, make_float2(0.9999281167984009f, 0.9999281167984009f));
+    p.x = __uint_as_float(__float_as_uint(p.x) + (__float_as_uint(j.x) << 23));
+    p.y = __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(j.y) << 23));
+    return p;
+}
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+        "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+        "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+        "r"(r[15])
+        : "memory");
+}
+
+__device__ __forceinline__ void softmax_bar() {   // the 256 softmax threads only
+    asm volatile("bar.sync 1, 256;" ::: "memory");
 }
 
 template <int D>
@@ -79,30 +181,32 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
     uint8_t* sQ = smem;                                  // 2 tiles
     uint8_t* sKV = smem + 2 * kTileBytes;                // kStages slots
     uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + kStages * kTileBytes);
-    uint64_t* q_full = bars;
-    uint64_t* kv_full = bars + 1;
-    uint64_t* kv_empty = kv_full + kStages;
-    uint64_t* s_full = kv_empty + kStages;
-    uint64_t* p_full = s_full + 2;
-    uint64_t* o_final = p_full + 2;
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(o_final + 2);
+    uint64_t* q_full = bars;                 // [2]
+    uint64_t* q_empty = q_full + 2;          // [2]
+    uint64_t* kv_full = q_empty + 2;         // [kStages]
+    uint64_t* kv_empty = kv_full + kStages;  // [kStages]
+    uint64_t* s_full = kv_empty + kStages;   // [2]
+    uint64_t* p_full = s_full + 2;           // [2]
+    uint64_t* o_final = p_full + 2;          // [2]
+    uint64_t* o_empty = o_final + 2;         // [2]
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(o_empty + 2);
+    int* merge_flag = reinterpret_cast<int*>(tmem_holder + 1);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const int h = blockIdx.y, b = blockIdx.z;
-    const int q0 = blockIdx.x * 2 * kBM;
-    const int n = p.n_tiles;
 
     if (threadIdx.x == 0) {
-        mbar_init(q_full, 1);
-        for (int s = 0; s < kStages; ++s) {
-            mbar_init(&kv_full[s], 1);
-            mbar_init(&kv_empty[s], 1);
-        }
         for (int i = 0; i < 2; ++i) {
+            mbar_init(&q_full[i], 1);
+            mbar_init(&q_empty[i], 1);
             mbar_init(&s_full[i], 1);
             mbar_init(&p_full[i], 128);
             mbar_init(&o_final[i], 1);
+            mbar_init(&o_empty[i], 128);
+        }
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&kv_full[s], 1);
+            mbar_init(&kv_empty[s], 1);
         }
         fence_mbar_init();
     }
@@ -119,165 +223,287 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
     tc_fence_after();
     const uint32_t tmem = *tmem_holder;
 
-    if (warp == 8) {
+    if (warp >= 8) {
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsOther));
+      if (warp == 8) {
         // ------------------------------------------------ TMA producer
         if (lane == 0) {
-            mbar_arrive_expect_tx(q_full, 2 * kTileBytes);
-            for (int i = 0; i < 2; ++i)
-                for (int hf = 0; hf < D / 64; ++hf)
-                    tma_load_4d(sQ + i * kTileBytes + hf * kHalfBytes, &p.tq, q_full, hf * 64, h,
-                                q0 + i * kBM, b);
-            for (int it = 0; it < 2 * n; ++it) {
-                const int s = it % kStages;
-                mbar_wait(&kv_empty[s], ((it / kStages) & 1) ^ 1);
-                int seg, row, valid;
-                tile_info(p, it >> 1, seg, row, valid);
-                const CUtensorMap* m = (it & 1) ? &p.tv[seg] : &p.tk[seg];
-                mbar_arrive_expect_tx(&kv_full[s], kTileBytes);
-                for (int hf = 0; hf < D / 64; ++hf)
-                    tma_load_4d(sKV + s * kTileBytes + hf * kHalfBytes, m, &kv_full[s], hf * 64,
-                                h, row, b);
+            uint32_t kv_it = 0, n_item = 0;
+            Item it;
+            for (int w = blockIdx.x; get_item(p, w, it); w += gridDim.x, ++n_item) {
+                for (int i = 0; i < 2; ++i) {
+                    mbar_wait(&q_empty[i], (n_item & 1) ^ 1);
+                    mbar_arrive_expect_tx(&q_full[i], kTileBytes);
+                    for (int hf = 0; hf < D / 64; ++hf)
+                        tma_load_4d(sQ + i * kTileBytes + hf * kHalfBytes, &p.tq, &q_full[i],
+                                    hf * 64, it.h, it.qp * 2 * kBM + i * kBM, it.b);
+                }
+                for (int j = it.lo; j < it.hi; ++j) {
+                    int seg, row, valid;
+                    tile_info(p, j, seg, row, valid);
+                    for (int kv = 0; kv < 2; ++kv, ++kv_it) {
+                        const int s = kv_it % kStages;
+                        mbar_wait(&kv_empty[s], ((kv_it / kStages) & 1) ^ 1);
+                        const CUtensorMap* m = kv ? &p.tv[seg] : &p.tk[seg];
+                        mbar_arrive_expect_tx(&kv_full[s], kTileBytes);
+                        for (int hf = 0; hf < D / 64; ++hf)
+                            tma_load_4d(sKV + s * kTileBytes + hf * kHalfBytes, m, &kv_full[s],
+                                        hf * 64, it.h, row, it.b);
+                    }
+                }
             }
         }
-    } else if (warp == 9) {
+      } else if (warp == 9) {
         // ------------------------------------------------ MMA issuer
         if (lane == 0) {
-            const uint32_t sQa = smem_u32(sQ), sKVa = smem_u32(sKV);
+            const uint64_t dq = make_sdesc_sw128(smem_u32(sQ), 16, 1024);
+            const uint64_t dk = make_sdesc_sw128(smem_u32(sKV), 16, 1024);
+            const uint64_t dv = make_sdesc_sw128(smem_u32(sKV), kHalfBytes, 1024);
+            constexpr uint32_t kTile16 = kTileBytes >> 4;      // descriptor address units
             auto issue_s = [&](int i, int slot) {
-#pragma unroll
+                const uint64_t a0 = dq + i * kTile16, b0 = dk + slot * kTile16;
+#pragma unroll 1
                 for (int kk = 0; kk < D / 16; ++kk) {
-                    const uint32_t off = (kk >> 2) * kHalfBytes + (kk & 3) * 32;
-                    mma_ss(tmem + i * 128, make_sdesc_sw128(sQa + i * kTileBytes + off, 16, 1024),
-                           make_sdesc_sw128(sKVa + slot * kTileBytes + off, 16, 1024), kIdescS,
-                           kk > 0);
+                    const uint32_t off = (kk >> 2) * (kHalfBytes >> 4) + (kk & 3) * 2;
+                    mma_ss(tmem + i * 128, a0 + off, b0 + off, kIdescS, kk > 0);
                 }
             };
             auto issue_pv = [&](int i, int slot, bool acc) {
-#pragma unroll
+                const uint64_t b0 = dv + slot * kTile16;
+#pragma unroll 1
                 for (int kk = 0; kk < kBN / 16; ++kk)
-                    mma_ts(tmem + 256 + i * D, tmem + i * 128 + kk * 8,
-                           make_sdesc_sw128(sKVa + slot * kTileBytes + kk * 2048, kHalfBytes, 1024),
-                           kIdescO, (acc || kk > 0) ? 1u : 0u);
+                    mma_ts(tmem + 256 + i * D, tmem + i * 128 + kk * 8, b0 + kk * 128, kIdescO,
+                           (acc || kk > 0) ? 1u : 0u);
             };
-            mbar_wait(q_full, 0);
-            tc_fence_after();
-            for (int j = 0; j < n; ++j) {
-                const int ik = 2 * j, sk = ik % kStages;
-                mbar_wait(&kv_full[sk], (ik / kStages) & 1);
-                tc_fence_after();
-                int sv = 0;
-                if (j > 0) {
-                    const int iv = 2 * (j - 1) + 1;
-                    sv = iv % kStages;
-                    mbar_wait(&kv_full[sv], (iv / kStages) & 1);
+            uint32_t kv_it = 0, g = 0, n_item = 0;
+            Item it;
+            for (int w = blockIdx.x; get_item(p, w, it); w += gridDim.x, ++n_item) {
+                const int nkv = it.hi - it.lo;
+                for (int j = 0; j < nkv; ++j) {
+                    const uint32_t ik = kv_it + 2 * j, sk = ik % kStages;
+                    mbar_wait(&kv_full[sk], (ik / kStages) & 1);
                     tc_fence_after();
-                }
-                for (int i = 0; i < 2; ++i) {
+                    uint32_t sv = 0;
                     if (j > 0) {
-                        mbar_wait(&p_full[i], (j - 1) & 1);
+                        const uint32_t iv = kv_it + 2 * (j - 1) + 1;
+                        sv = iv % kStages;
+                        mbar_wait(&kv_full[sv], (iv / kStages) & 1);
                         tc_fence_after();
-                        issue_pv(i, sv, j - 1 > 0);
                     }
-                    issue_s(i, sk);
-                    mma_commit(&s_full[i]);
+                    for (int i = 0; i < 2; ++i) {
+                        if (j > 0) {
+                            mbar_wait(&p_full[i], (g + j - 1) & 1);
+                            if (j == 1 && n_item > 0) mbar_wait(&o_empty[i], (n_item - 1) & 1);
+                            tc_fence_after();
+                            issue_pv(i, sv, j - 1 > 0);
+                        }
+                        if (j == 0) {
+                            mbar_wait(&q_full[i], n_item & 1);
+                            tc_fence_after();
+                        }
+                        issue_s(i, sk);
+                        mma_commit(&s_full[i]);
+                        if (j == nkv - 1) mma_commit(&q_empty[i]);
+                    }
+                    mma_commit(&kv_empty[sk]);
+                    if (j > 0) mma_commit(&kv_empty[sv]);
                 }
-                mma_commit(&kv_empty[sk]);
-                if (j > 0) mma_commit(&kv_empty[sv]);
-            }
-            const int iv = 2 * (n - 1) + 1, sv = iv % kStages;
-            mbar_wait(&kv_full[sv], (iv / kStages) & 1);
-            tc_fence_after();
-            for (int i = 0; i < 2; ++i) {
-                mbar_wait(&p_full[i], (n - 1) & 1);
+                const uint32_t iv = kv_it + 2 * (nkv - 1) + 1, sv = iv % kStages;
+                mbar_wait(&kv_full[sv], (iv / kStages) & 1);
                 tc_fence_after();
-                issue_pv(i, sv, n - 1 > 0);
-                mma_commit(&o_final[i]);
+                for (int i = 0; i < 2; ++i) {
+                    mbar_wait(&p_full[i], (g + nkv - 1) & 1);
+                    if (nkv == 1 && n_item > 0) mbar_wait(&o_empty[i], (n_item - 1) & 1);
+                    tc_fence_after();
+                    issue_pv(i, sv, nkv - 1 > 0);
+                    mma_commit(&o_final[i]);
+                }
+                mma_commit(&kv_empty[sv]);
+                kv_it += 2 * nkv;
+                g += nkv;
             }
-            mma_commit(&kv_empty[sv]);
         }
+      }
     } else {
-        // ------------------------------------------------ softmax (warps 0-7)
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsSoftmax));
+        // ------------------------------------------------ softmax + epilogue (warps 0-7)
         const int i = warp >> 2, wq = warp & 3;
+        const int row_in_pair = i * kBM + wq * 32 + lane;       // 0..255
         const uint32_t lane_off = uint32_t(wq * 32) << 16;
         const uint32_t tSi = tmem + lane_off + i * 128;
         const uint32_t tOi = tmem + lane_off + 256 + i * D;
         const float sl2 = p.scale_log2;
-        float m_run = -INFINITY, l = 0.f;
-        uint32_t r[kBN];
-        uint32_t pk[kBN / 2];
-        for (int j = 0; j < n; ++j) {
-            int seg, row, valid;
-            tile_info(p, j, seg, row, valid);
-            mbar_wait(&s_full[i], j & 1);
+        uint32_t g = 0, n_item = 0;
+        Item it;
+        for (int w = blockIdx.x; get_item(p, w, it); w += gridDim.x, ++n_item) {
+            float m_run = -INFINITY, l = 0.f;
+            for (int j = it.lo; j < it.hi; ++j, ++g) {
+                int seg, row, valid;
+                tile_info(p, j, seg, row, valid);
+                uint32_t r[kBN];
+                mbar_wait(&s_full[i], g & 1);
+                tc_fence_after();
+#pragma unroll
+                for (int c = 0; c < kBN; c += 32) tmem_ld32(tSi + c, r + c);
+                tmem_wait_ld();
+                if (valid < kBN) {
+#pragma unroll
+                    for (int c = 0; c < kBN; ++c)
+                        if (c >= valid) r[c] = 0xff800000u;   // -inf: key beyond the segment
+                }
+                // row max: 3-input max tree (depth 5)
+                float t1[43];
+#pragma unroll
+                for (int k = 0; k < 42; ++k)
+                    t1[k] = max3(__uint_as_float(r[3 * k]), __uint_as_float(r[3 * k + 1]),
+                                 __uint_as_float(r[3 * k + 2]));
+                t1[42] = fmaxf(__uint_as_float(r[126]), __uint_as_float(r[127]));
+                float t2[15];
+#pragma unroll
+                for (int k = 0; k < 14; ++k) t2[k] = max3(t1[3 * k], t1[3 * k + 1], t1[3 * k + 2]);
+                t2[14] = t1[42];
+                float t3[5];
+#pragma unroll
+                for (int k = 0; k < 5; ++k) t3[k] = max3(t2[3 * k], t2[3 * k + 1], t2[3 * k + 2]);
+                const float mx = max3(max3(t3[0], t3[1], t3[2]), t3[3], t3[4]);
+
+                const float m_new = fmaxf(m_run, mx * sl2);
+                const bool need = m_new > m_run + 8.0f;
+                float alpha = 1.f;
+                if (need) {
+                    alpha = ex2(m_run - m_new);
+                    m_run = m_new;
+                }
+                l *= alpha;
+                if (j > it.lo && __any_sync(0xffffffffu, need)) {
+                    // O_i was last written by PV_i_{j-1}, complete before s_full fired.
+#pragma unroll
+                    for (int c = 0; c < D; c += 32) {
+                        uint32_t o[32];
+                        tmem_ld32(tOi + c, o);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int e = 0; e < 32; ++e)
+                            o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+                        tmem_st32(tOi + c, o);
+                    }
+                }
+                const float nm = (m_run == -INFINITY) ? 0.f : -m_run;
+                const float2 sc2 = make_float2(sl2, sl2), nm2 = make_float2(nm, nm);
+                float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                                 make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    uint32_t pk[16];
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) {
+                        const float2 x = ffma2(make_float2(__uint_as_float(r[32 * c + 2 * e]),
+                                                           __uint_as_float(r[32 * c + 2 * e + 1])),
+                                               sc2, nm2);
+                        float2 pe;
+                        if (e < 10) {                       // cols 0..19 of each 32: MUFU
+                            pe.x = ex2(x.x);
+                            pe.y = ex2(x.y);
+                        } else {                            // cols 20..31: FMA-pipe polynomial
+                            pe = exp2_poly2(x);
+                        }
+                        acc[e & 3] = fadd2(acc[e & 3], pe);
+                        pk[e] = pack_bf16x2(pe.x, pe.y);
+                    }
+                    tmem_st16(tSi + c * 16, pk);
+                }
+                const float2 s01 = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
+                l += s01.x + s01.y;
+                tmem_wait_st();
+                tc_fence_before();
+                mbar_arrive(&p_full[i]);
+            }
+            // ------------------------------------------------ epilogue
+            mbar_wait(&o_final[i], n_item & 1);
             tc_fence_after();
+            const int q = it.qp * 2 * kBM + row_in_pair;
+            if (!it.piece) {
+                const float inv_l = 1.f / l;
+                uint16_t* dst = p.o + ((int64_t(it.b) * p.Lq + q) * p.H + it.h) * D;
 #pragma unroll
-            for (int c = 0; c < kBN; c += 32) tmem_ld32(tSi + c, r + c);
-            tmem_wait_ld();
-            if (valid < kBN) {
+                for (int c = 0; c < D; c += 32) {
+                    uint32_t o[32];
+                    tmem_ld32(tOi + c, o);
+                    tmem_wait_ld();
+                    uint32_t wv[16];
 #pragma unroll
-                for (int c = 0; c < kBN; ++c)
-                    if (c >= valid) r[c] = 0xff800000u;   // -inf: key beyond the segment
-            }
-            float mx = -INFINITY;
+                    for (int e = 0; e < 16; ++e)
+                        wv[e] = pack_bf16x2(__uint_as_float(o[2 * e]) * inv_l,
+                                            __uint_as_float(o[2 * e + 1]) * inv_l);
+                    if (q < p.Lq) {
+                        uint4* d4 = reinterpret_cast<uint4*>(dst + c);
 #pragma unroll
-            for (int c = 0; c < kBN; ++c) mx = fmaxf(mx, __uint_as_float(r[c]));
-            const float m_new = fmaxf(m_run, mx * sl2);
-            const bool need = m_new > m_run + 8.0f;
-            float alpha = 1.f;
-            if (need) {
-                alpha = ex2(m_run - m_new);
-                m_run = m_new;
-            }
-            l *= alpha;
-            if (j > 0 && __any_sync(0xffffffffu, need)) {
-                // O_i was last written by PV_i_{j-1}, complete before s_full fired.
+                        for (int e = 0; e < 4; ++e)
+                            d4[e] = make_uint4(wv[4 * e], wv[4 * e + 1], wv[4 * e + 2], wv[4 * e + 3]);
+                    }
+                }
+                tc_fence_before();
+                mbar_arrive(&o_empty[i]);
+            } else {
+                // split piece: unnormalised O, running max m (log2 units) and l
+                constexpr int kPieceFloats = 256 * D + 512;
+                float* base = p.part + size_t(it.tail_unit * p.splits + it.split) * kPieceFloats;
+                float4* po = reinterpret_cast<float4*>(base);
 #pragma unroll
                 for (int c = 0; c < D; c += 32) {
                     uint32_t o[32];
                     tmem_ld32(tOi + c, o);
                     tmem_wait_ld();
 #pragma unroll
-                    for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-                    tmem_st32(tOi + c, o);
+                    for (int e = 0; e < 8; ++e)
+                        po[((c >> 2) + e) * 256 + row_in_pair] =
+                            make_float4(__uint_as_float(o[4 * e]), __uint_as_float(o[4 * e + 1]),
+                                        __uint_as_float(o[4 * e + 2]), __uint_as_float(o[4 * e + 3]));
                 }
-            }
-            const float nm = (m_run == -INFINITY) ? 0.f : -m_run;
-            float sum = 0.f;
-#pragma unroll
-            for (int c = 0; c < kBN / 2; ++c) {
-                const float p0 = ex2(fmaf(__uint_as_float(r[2 * c]), sl2, nm));
-                const float p1 = ex2(fmaf(__uint_as_float(r[2 * c + 1]), sl2, nm));
-                sum += p0 + p1;
-                pk[c] = pack_bf16x2(p0, p1);
-            }
-            l += sum;
-            tmem_st32(tSi, pk);
-            tmem_st32(tSi + 32, pk + 32);
-            tmem_wait_st();
-            tc_fence_before();
-            mbar_arrive(&p_full[i]);
-        }
-        // ------------------------------------------------ epilogue O / l
-        mbar_wait(&o_final[i], 0);
-        tc_fence_after();
-        const float inv_l = 1.f / l;
-        const int q = q0 + i * kBM + wq * 32 + lane;
-        uint16_t* dst = p.o + ((int64_t(b) * p.Lq + q) * p.H + h) * D;
-#pragma unroll
-        for (int c = 0; c < D; c += 32) {
-            uint32_t o[32];
-            tmem_ld32(tOi + c, o);
-            tmem_wait_ld();
-            uint32_t w[16];
-#pragma unroll
-            for (int e = 0; e < 16; ++e)
-                w[e] = pack_bf16x2(__uint_as_float(o[2 * e]) * inv_l,
-                                   __uint_as_float(o[2 * e + 1]) * inv_l);
-            if (q < p.Lq) {
-                uint4* d4 = reinterpret_cast<uint4*>(dst + c);
-#pragma unroll
-                for (int e = 0; e < 4; ++e)
-                    d4[e] = make_uint4(w[4 * e], w[4 * e + 1], w[4 * e + 2], w[4 * e + 3]);
+                tc_fence_before();
+                mbar_arrive(&o_empty[i]);
+                base[256 * D + row_in_pair] = m_run;
+                base[256 * D + 256 + row_in_pair] = l;
+                __threadfence();
+                softmax_bar();
+                if (threadIdx.x == 0)
+                    *merge_flag = atomicAdd(&p.counters[it.tail_unit], 1) == p.splits - 1;
+                softmax_bar();
+                const int do_merge = *merge_flag;
+                softmax_bar();          // everyone has read the flag before it is reused
+                if (do_merge) {
+                    // last piece to finish: merge all S pieces in piece order.
+                    __threadfence();
+                    const float* b0 = p.part + size_t(it.tail_unit * p.splits) * kPieceFloats;
+                    float mstar = -INFINITY;
+                    for (int s = 0; s < p.splits; ++s)
+                        mstar = fmaxf(mstar, __ldcg(b0 + size_t(s) * kPieceFloats + 256 * D + row_in_pair));
+                    float wsum = 0.f;
+                    for (int s = 0; s < p.splits; ++s) {
+                        const float* bs = b0 + size_t(s) * kPieceFloats;
+                        wsum += ex2(__ldcg(bs + 256 * D + row_in_pair) - mstar) *
+                                __ldcg(bs + 256 * D + 256 + row_in_pair);
+                    }
+                    const float inv = 1.f / wsum;
+                    uint16_t* dst = p.o + ((int64_t(it.b) * p.Lq + q) * p.H + it.h) * D;
+#pragma unroll 1
+                    for (int c4 = 0; c4 < D / 4; c4 += 2) {
+                        float4 a = make_float4(0.f, 0.f, 0.f, 0.f), bq = a;
+                        for (int s = 0; s < p.splits; ++s) {
+                            const float* bs = b0 + size_t(s) * kPieceFloats;
+                            const float ws = ex2(__ldcg(bs + 256 * D + row_in_pair) - mstar);
+                            const float4 x = __ldcg(reinterpret_cast<const float4*>(bs) + c4 * 256 + row_in_pair);
+                            const float4 y = __ldcg(reinterpret_cast<const float4*>(bs) + (c4 + 1) * 256 + row_in_pair);
+                            a.x += ws * x.x; a.y += ws * x.y; a.z += ws * x.z; a.w += ws * x.w;
+                            bq.x += ws * y.x; bq.y += ws * y.y; bq.z += ws * y.z; bq.w += ws * y.w;
+                        }
+                        if (q < p.Lq)
+                            *reinterpret_cast<uint4*>(dst + 4 * c4) =
+                                make_uint4(pack_bf16x2(a.x * inv, a.y * inv), pack_bf16x2(a.z * inv, a.w * inv),
+                                           pack_bf16x2(bq.x * inv, bq.y * inv), pack_bf16x2(bq.z * inv, bq.w * inv));
+                    }
+                    if (threadIdx.x == 0) p.counters[it.tail_unit] = 0;   // ready for the next launch
+                }
             }
         }
     }
@@ -322,9 +548,39 @@ constexpr int smem_bytes() {
     return 1024 + (2 + kStages) * kBN * D * 2 + 256;
 }
 
+int sm_count() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+template <int D>
+cudaError_t launch_t(const FmhaParams& p, int grid, cudaStream_t stream) {
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(fmha_sm100_kernel<D>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             smem_bytes<D>());
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    fmha_sm100_kernel<D><<<grid, kThreads, smem_bytes<D>(), stream>>>(p);
+    return cudaGetLastError();
+}
+
 }  // namespace
 
-cudaError_t launch_fmha_sm100(const AttnProblem& pr, cudaStream_t stream, int* launches) {
+size_t fmha_sm100_scratch_bytes(int d) {
+    return size_t(kMaxPersistentCtas) * (256 * size_t(d) + 512) * 4 + kMaxPersistentCtas * 4;
+}
+
+cudaError_t launch_fmha_sm100(const AttnProblem& pr, void* scratch, cudaStream_t stream,
+                              int* launches) {
     if (pr.d != 64 && pr.d != 128) return cudaErrorInvalidValue;
     FmhaParams p;
     memset(&p, 0, sizeof(p));
@@ -347,29 +603,29 @@ cudaError_t launch_fmha_sm100(const AttnProblem& pr, cudaStream_t stream, int* l
     p.scale_log2 = pr.scale * 1.4426950408889634f;
     p.o = static_cast<uint16_t*>(pr.o);
     const int qtiles = int((pr.Lq + kBM - 1) / kBM);
-    dim3 grid((qtiles + 1) / 2, pr.H, pr.B);
-    cudaError_t e;
-    if (pr.d == 128) {
-        static bool attr = false;
-        if (!attr) {
-            e = cudaFuncSetAttribute(fmha_sm100_kernel<128>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<128>());
-            if (e != cudaSuccess) return e;
-            attr = true;
-        }
-        fmha_sm100_kernel<128><<<grid, kThreads, smem_bytes<128>(), stream>>>(p);
-    } else {
-        static bool attr = false;
-        if (!attr) {
-            e = cudaFuncSetAttribute(fmha_sm100_kernel<64>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<64>());
-            if (e != cudaSuccess) return e;
-            attr = true;
-        }
-        fmha_sm100_kernel<64><<<grid, kThreads, smem_bytes<64>(), stream>>>(p);
+    p.n_qpairs = (qtiles + 1) / 2;
+    // Persistent schedule: R whole rounds over C CTAs, then the T tail units
+    // split S ways along the KV axis (S*T <= C).
+    const int C = sm_count() < kMaxPersistentCtas ? sm_count() : kMaxPersistentCtas;
+    const int U = pr.B * pr.H * p.n_qpairs;
+    const int R = U / C;
+    const int T = U - R * C;
+    int S = 1;
+    if (T > 0) {
+        S = C / T;
+        if (S > tiles) S = tiles;
+        if (S < 1) S = 1;
     }
-    if (launches) ++*launches;
-    return cudaGetLastError();
+    p.whole_items = R * C;
+    p.tail_pieces = T * S;
+    p.splits = S;
+    p.part = static_cast<float*>(scratch);
+    p.counters = reinterpret_cast<int*>(static_cast<uint8_t*>(scratch) +
+                                        size_t(kMaxPersistentCtas) * (256 * size_t(pr.d) + 512) * 4);
+    const int grid = R > 0 ? C : T * S;
+    cudaError_t e = pr.d == 128 ? launch_t<128>(p, grid, stream) : launch_t<64>(p, grid, stream);
+    if (e == cudaSuccess && launches) ++*launches;
+    return e;
 }
 
 }  // namespace tmk

@@ -7,6 +7,7 @@
 namespace tmk {
 
 constexpr int kMaxSegments = 3;   // {c_0, c_{t-1}, c_t}
+constexpr int kMaxPersistentCtas = 160;   // persistent grid cap (B200: 148 SMs)
 
 // One contiguous K/V segment in token-major layout [B][len][H][d].
 struct Segment {
@@ -28,7 +29,10 @@ struct AttnProblem {
 
 // Launchers; return cudaSuccess or the launch error.  `launches` is
 // incremented by the number of kernels enqueued.
-cudaError_t launch_fmha_sm100(const AttnProblem& p, cudaStream_t s, int* launches);
+// `scratch` (fmha_sm100_scratch_bytes(d) bytes, zero-initialised once) holds
+// the split-KV partials and merge counters; counters return to zero.
+size_t fmha_sm100_scratch_bytes(int d);
+cudaError_t launch_fmha_sm100(const AttnProblem& p, void* scratch, cudaStream_t s, int* launches);
 cudaError_t launch_fmha_fp32(const AttnProblem& p, cudaStream_t s, int* launches);
 cudaError_t launch_euler(float* x, const void* v, int v_is_bf16, int64_t n, float dt,
                          cudaStream_t s, int* launches);

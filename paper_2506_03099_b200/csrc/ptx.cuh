@@ -39,18 +39,14 @@ __device__ __forceinline__ uint32_t mbar_try_wait(uint32_t bar, uint32_t parity)
     return ok;
 }
 // Wait for the phase with the given parity to complete.  A watchdog traps
-// (kernel error instead of a hung GPU) if nothing happens for ~2^33 cycles.
+// (a kernel error instead of a hung GPU) if the phase does not complete
+// within ~2^33 cycles; no printf, so the inlined loop needs no stack.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     const uint32_t a = smem_u32(bar);
     if (mbar_try_wait(a, parity)) return;
     const long long t0 = clock64();
-    while (!mbar_try_wait(a, parity)) {
-        if (clock64() - t0 > (1ll << 33)) {
-            printf("tm: mbarrier watchdog block (%d,%d,%d) thread %d parity %u\n", blockIdx.x,
-                   blockIdx.y, blockIdx.z, threadIdx.x, parity);
-            __trap();
-        }
-    }
+    while (!mbar_try_wait(a, parity))
+        if (clock64() - t0 > (1ll << 33)) __trap();
 }
 
 // ---------------------------------------------------------------- TMA

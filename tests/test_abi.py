@@ -72,7 +72,10 @@ def test_invalid_configs_are_rejected(bad):
 
 
 def test_workspace_sizes():
-    assert tm.tm_workspace_bytes(wan512()) == 1024
+    # bf16: debug flag + split-KV scratch for <= 160 persistent CTAs (partials + counters)
+    scratch = 160 * (256 * 128 + 512) * 4 + 160 * 4
+    assert tm.tm_workspace_bytes(wan512()) == 1024 + (scratch + 1023) // 1024 * 1024
+    assert tm.tm_workspace_bytes(wan512(dtype=tm.TM_FP32)) == 1024
     ws8 = tm.tm_workspace_bytes(wan512(world_size=8))
     shard = 384 * 40 * 128 * 2          # [Lc/8][H][d] bf16
     assert ws8 >= 1024 + 2 * 3 * shard + 2 * 3072 * 5 * 128 * 2
