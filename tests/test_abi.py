@@ -98,5 +98,5 @@ def test_init_without_device_reports_cuda_error():
     if torch.cuda.is_available():
         pytest.skip("GPU present")
     with pytest.raises(tm.TMError) as e:
-        tm.tm_attn_init(wan512(), None, 1024, 1 << 40, 1024, 1 << 20)
+        tm.tm_attn_init(wan512(), None, 1024, 1 << 40, 1024, 1 << 30)
     assert e.value.status == 8
