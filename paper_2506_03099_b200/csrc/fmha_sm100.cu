@@ -54,8 +54,11 @@ constexpr int kBM = 128;          // query rows per Q tile
 constexpr int kBN = 128;          // keys per KV tile
 constexpr int kStages = 4;        // K/V smem ring slots
 constexpr int kThreads = 384;     // 2 softmax warpgroups + {TMA, MMA, 2 spare} warpgroup
-constexpr int kRegsSoftmax = 224; // setmaxnreg budgets: 256 x 224 + 128 x 64 <= 64K
+constexpr int kRegsSoftmax = 216; // setmaxnreg budgets (see the static_assert)
 constexpr int kRegsOther = 64;
+// The CTA launches with 168 regs/thread (64K / 384 rounded down to 8); setmaxnreg
+// only redistributes that pool, so the budgets must fit in 384 x 168.
+static_assert(256 * kRegsSoftmax + 128 * kRegsOther <= kThreads * 168, "register pool");
 constexpr int kHalfBytes = 128 * 128;   // one 64-column (128 B) half of a 128-row tile
 
 struct __align__(64) FmhaParams {
