@@ -115,6 +115,8 @@ struct tm_ctx {
     void* comm = nullptr;
     int launches = 0;
     bool debug = false;
+    unsigned long long* trace = nullptr;   // TM_TRACE=<file>: kernel timeline of CTA 0
+    std::string trace_path;
 
     size_t idx(int layer, int step) const { return size_t(layer) * cfg.num_steps + step; }
     uint8_t* region(int layer, int step) const { return cache + idx(layer, step) * lay.region_bytes; }
@@ -261,6 +263,9 @@ tm_status tm_attn_init(const tm_config* cfg, const uint8_t* nccl_id, void* cache
     }
     const char* dbg = getenv("TM_DEBUG");
     c->debug = dbg && *dbg && strcmp(dbg, "0") != 0;
+    if (const char* tp = getenv("TM_TRACE")) {
+        if (*tp && cudaMalloc(&c->trace, 4 * 4096 * 8) == cudaSuccess) c->trace_path = tp;
+    }
     if (cfg->world_size > 1) {
         const char* e = comm_init(&c->comm, cfg->world_size, cfg->rank, nccl_id);
         if (e) {
@@ -275,6 +280,7 @@ tm_status tm_attn_init(const tm_config* cfg, const uint8_t* nccl_id, void* cache
 tm_status tm_attn_destroy(tm_ctx* ctx) {
     if (!ctx) return fail(TM_ERR_INVALID_ARG, "null ctx");
     if (ctx->comm) comm_destroy(ctx->comm);
+    if (ctx->trace) cudaFree(ctx->trace);
     delete ctx;
     return TM_OK;
 }
@@ -411,10 +417,20 @@ tm_status tm_chunk_attention(tm_ctx* ctx, int32_t layer, int32_t step, int64_t c
                                     ctx->vslot(layer, step, chunk - 1), Ly.Lc};
     pr.seg[pr.nseg++] = Segment{kslot, vslot, Ly.Lc};
 
-    cudaError_t e = cf.dtype == TM_BF16 ? launch_fmha_sm100(pr, ctx->scratch(), cs, &ctx->launches)
+    if (ctx->trace) cudaMemsetAsync(ctx->trace, 0, 4 * 4096 * 8, cs);
+    cudaError_t e = cf.dtype == TM_BF16 ? launch_fmha_sm100(pr, ctx->scratch(), cs, &ctx->launches, ctx->trace)
                                         : launch_fmha_fp32(pr, cs, &ctx->launches);
     st = cuda_check(e, "attention kernel launch");
     if (st) return st;
+    if (ctx->trace) {   // debug only: dump CTA 0's timeline (synchronises)
+        std::vector<unsigned long long> h(4 * 4096);
+        cudaMemcpyAsync(h.data(), ctx->trace, h.size() * 8, cudaMemcpyDeviceToHost, cs);
+        cudaStreamSynchronize(cs);
+        if (FILE* f = fopen(ctx->trace_path.c_str(), "ab")) {
+            fwrite(h.data(), 8, h.size(), f);
+            fclose(f);
+        }
+    }
 
     if (Ly.P > 1) {
         // a6: head -> seq all-to-all of O.

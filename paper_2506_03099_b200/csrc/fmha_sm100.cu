@@ -79,7 +79,16 @@ struct __align__(64) FmhaParams {
     int splits;                       // S
     float* part;                      // split partials: per piece [d/4][256] float4 + m[256] + l[256]
     int* counters;                    // per tail unit, zero between launches
+    unsigned long long* trace;        // debug timeline (TM_TRACE=1), CTA 0 only; may be null
 };
+
+// Debug timeline: role r in [0,4) owns trace[r*kTraceCap ..]; entry =
+// clock64() << 8 | event code.  Only CTA 0 records; off when p.trace == 0.
+constexpr int kTraceCap = 4096;
+__device__ __forceinline__ void trace_ev(const FmhaParams& p, int role, int& n, int code) {
+    if (p.trace != nullptr && blockIdx.x == 0 && n < kTraceCap)
+        p.trace[role * kTraceCap + n++] = (static_cast<unsigned long long>(clock64()) << 8) | code;
+}
 
 struct Item {
     int b, h, qp, lo, hi, piece, tail_unit, split;
@@ -231,6 +240,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
       if (warp == 8) {
         // ------------------------------------------------ TMA producer
         if (lane == 0) {
+            int tn = 0;
             uint32_t kv_it = 0, n_item = 0;
             Item it;
             for (int w = blockIdx.x; get_item(p, w, it); w += gridDim.x, ++n_item) {
@@ -247,6 +257,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                     for (int kv = 0; kv < 2; ++kv, ++kv_it) {
                         const int s = kv_it % kStages;
                         mbar_wait(&kv_empty[s], ((kv_it / kStages) & 1) ^ 1);
+                        trace_ev(p, 0, tn, 1 + kv);
                         const CUtensorMap* m = kv ? &p.tv[seg] : &p.tk[seg];
                         mbar_arrive_expect_tx(&kv_full[s], kTileBytes);
                         for (int hf = 0; hf < D / 64; ++hf)
@@ -279,12 +290,14 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                            (acc || kk > 0) ? 1u : 0u);
             };
             uint32_t kv_it = 0, g = 0, n_item = 0;
+            int tn = 0;
             Item it;
             for (int w = blockIdx.x; get_item(p, w, it); w += gridDim.x, ++n_item) {
                 const int nkv = it.hi - it.lo;
                 for (int j = 0; j < nkv; ++j) {
                     const uint32_t ik = kv_it + 2 * j, sk = ik % kStages;
                     mbar_wait(&kv_full[sk], (ik / kStages) & 1);
+                    trace_ev(p, 1, tn, 10);
                     tc_fence_after();
                     uint32_t sv = 0;
                     if (j > 0) {
@@ -297,6 +310,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                         if (j > 0) {
                             mbar_wait(&p_full[i], (g + j - 1) & 1);
                             if (j == 1 && n_item > 0) mbar_wait(&o_empty[i], (n_item - 1) & 1);
+                            trace_ev(p, 1, tn, 11 + i);
                             tc_fence_after();
                             issue_pv(i, sv, j - 1 > 0);
                         }
@@ -306,6 +320,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                         }
                         issue_s(i, sk);
                         mma_commit(&s_full[i]);
+                        trace_ev(p, 1, tn, 13 + i);
                         if (j == nkv - 1) mma_commit(&q_empty[i]);
                     }
                     mma_commit(&kv_empty[sk]);
@@ -337,6 +352,8 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
         const uint32_t tOi = tmem + lane_off + 256 + i * D;
         const float sl2 = p.scale_log2;
         uint32_t g = 0, n_item = 0;
+        int tn = 0;
+        const bool tr = (wq == 0 && lane == 0);
         Item it;
         for (int w = blockIdx.x; get_item(p, w, it); w += gridDim.x, ++n_item) {
             float m_run = -INFINITY, l = 0.f;
@@ -345,10 +362,12 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                 tile_info(p, j, seg, row, valid);
                 uint32_t r[kBN];
                 mbar_wait(&s_full[i], g & 1);
+                if (tr) trace_ev(p, 2 + i, tn, 20);
                 tc_fence_after();
 #pragma unroll
                 for (int c = 0; c < kBN; c += 32) tmem_ld32(tSi + c, r + c);
                 tmem_wait_ld();
+                if (tr) trace_ev(p, 2 + i, tn, 21);
                 if (valid < kBN) {
 #pragma unroll
                     for (int c = 0; c < kBN; ++c)
@@ -370,6 +389,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                 for (int k = 0; k < 5; ++k) t3[k] = max3(t2[3 * k], t2[3 * k + 1], t2[3 * k + 2]);
                 const float mx = max3(max3(t3[0], t3[1], t3[2]), t3[3], t3[4]);
 
+                if (tr) trace_ev(p, 2 + i, tn, 22);
                 const float m_new = fmaxf(m_run, mx * sl2);
                 const bool need = m_new > m_run + 8.0f;
                 float alpha = 1.f;
@@ -417,9 +437,11 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                 }
                 const float2 s01 = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
                 l += s01.x + s01.y;
+                if (tr) trace_ev(p, 2 + i, tn, 23);
                 tmem_wait_st();
                 tc_fence_before();
                 mbar_arrive(&p_full[i]);
+                if (tr) trace_ev(p, 2 + i, tn, 24);
             }
             // ------------------------------------------------ epilogue
             mbar_wait(&o_final[i], n_item & 1);
@@ -583,7 +605,7 @@ size_t fmha_sm100_scratch_bytes(int d) {
 }
 
 cudaError_t launch_fmha_sm100(const AttnProblem& pr, void* scratch, cudaStream_t stream,
-                              int* launches) {
+                              int* launches, unsigned long long* trace) {
     if (pr.d != 64 && pr.d != 128) return cudaErrorInvalidValue;
     FmhaParams p;
     memset(&p, 0, sizeof(p));
@@ -622,6 +644,7 @@ cudaError_t launch_fmha_sm100(const AttnProblem& pr, void* scratch, cudaStream_t
     p.whole_items = R * C;
     p.tail_pieces = T * S;
     p.splits = S;
+    p.trace = trace;
     p.part = static_cast<float*>(scratch);
     p.counters = reinterpret_cast<int*>(static_cast<uint8_t*>(scratch) +
                                         size_t(kMaxPersistentCtas) * (256 * size_t(pr.d) + 512) * 4);

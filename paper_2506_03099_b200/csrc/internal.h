@@ -32,7 +32,9 @@ struct AttnProblem {
 // `scratch` (fmha_sm100_scratch_bytes(d) bytes, zero-initialised once) holds
 // the split-KV partials and merge counters; counters return to zero.
 size_t fmha_sm100_scratch_bytes(int d);
-cudaError_t launch_fmha_sm100(const AttnProblem& p, void* scratch, cudaStream_t s, int* launches);
+// `trace` (debug, may be null): 4 x 4096 uint64 clock64 timeline of CTA 0.
+cudaError_t launch_fmha_sm100(const AttnProblem& p, void* scratch, cudaStream_t s, int* launches,
+                              unsigned long long* trace = nullptr);
 cudaError_t launch_fmha_fp32(const AttnProblem& p, cudaStream_t s, int* launches);
 cudaError_t launch_euler(float* x, const void* v, int v_is_bf16, int64_t n, float dt,
                          cudaStream_t s, int* launches);
