@@ -54,8 +54,8 @@ constexpr int kBM = 128;          // query rows per Q tile
 constexpr int kBN = 128;          // keys per KV tile
 constexpr int kStages = 4;        // K/V smem ring slots
 constexpr int kThreads = 384;     // 2 softmax warpgroups + {TMA, MMA, 2 spare} warpgroup
-constexpr int kRegsSoftmax = 216; // setmaxnreg budgets (see the static_assert)
-constexpr int kRegsOther = 64;
+constexpr int kRegsSoftmax = 208; // setmaxnreg budgets (see the static_assert)
+constexpr int kRegsOther = 88;
 // The CTA launches with 168 regs/thread (64K / 384 rounded down to 8); setmaxnreg
 // only redistributes that pool, so the budgets must fit in 384 x 168.
 static_assert(256 * kRegsSoftmax + 128 * kRegsOther <= kThreads * 168, "register pool");
@@ -269,24 +269,25 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
         }
       } else if (warp == 9) {
         // ------------------------------------------------ MMA issuer
-        if (lane == 0) {
+        {   // the whole warp runs the loop (uniform operands live in uniform
+            // registers); one elected lane issues each tcgen05 instruction.
             const uint64_t dq = make_sdesc_sw128(smem_u32(sQ), 16, 1024);
             const uint64_t dk = make_sdesc_sw128(smem_u32(sKV), 16, 1024);
             const uint64_t dv = make_sdesc_sw128(smem_u32(sKV), kHalfBytes, 1024);
             constexpr uint32_t kTile16 = kTileBytes >> 4;      // descriptor address units
             auto issue_s = [&](int i, int slot) {
                 const uint64_t a0 = dq + i * kTile16, b0 = dk + slot * kTile16;
-#pragma unroll 1
+#pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk) {
                     const uint32_t off = (kk >> 2) * (kHalfBytes >> 4) + (kk & 3) * 2;
-                    mma_ss(tmem + i * 128, a0 + off, b0 + off, kIdescS, kk > 0);
+                    mma_ss_w(tmem + i * 128, a0 + off, b0 + off, kIdescS, kk > 0);
                 }
             };
             auto issue_pv = [&](int i, int slot, bool acc) {
                 const uint64_t b0 = dv + slot * kTile16;
-#pragma unroll 1
+#pragma unroll
                 for (int kk = 0; kk < kBN / 16; ++kk)
-                    mma_ts(tmem + 256 + i * D, tmem + i * 128 + kk * 8, b0 + kk * 128, kIdescO,
+                    mma_ts_w(tmem + 256 + i * D, tmem + i * 128 + kk * 8, b0 + kk * 128, kIdescO,
                            (acc || kk > 0) ? 1u : 0u);
             };
             uint32_t kv_it = 0, g = 0, n_item = 0;
@@ -297,7 +298,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                 for (int j = 0; j < nkv; ++j) {
                     const uint32_t ik = kv_it + 2 * j, sk = ik % kStages;
                     mbar_wait(&kv_full[sk], (ik / kStages) & 1);
-                    trace_ev(p, 1, tn, 10);
+                    if (lane == 0) trace_ev(p, 1, tn, 10);
                     tc_fence_after();
                     uint32_t sv = 0;
                     if (j > 0) {
@@ -310,7 +311,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                         if (j > 0) {
                             mbar_wait(&p_full[i], (g + j - 1) & 1);
                             if (j == 1 && n_item > 0) mbar_wait(&o_empty[i], (n_item - 1) & 1);
-                            trace_ev(p, 1, tn, 11 + i);
+                            if (lane == 0) trace_ev(p, 1, tn, 11 + i);
                             tc_fence_after();
                             issue_pv(i, sv, j - 1 > 0);
                         }
@@ -319,12 +320,12 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                             tc_fence_after();
                         }
                         issue_s(i, sk);
-                        mma_commit(&s_full[i]);
-                        trace_ev(p, 1, tn, 13 + i);
-                        if (j == nkv - 1) mma_commit(&q_empty[i]);
+                        mma_commit_w(&s_full[i]);
+                        if (lane == 0) trace_ev(p, 1, tn, 13 + i);
+                        if (j == nkv - 1) mma_commit_w(&q_empty[i]);
                     }
-                    mma_commit(&kv_empty[sk]);
-                    if (j > 0) mma_commit(&kv_empty[sv]);
+                    mma_commit_w(&kv_empty[sk]);
+                    if (j > 0) mma_commit_w(&kv_empty[sv]);
                 }
                 const uint32_t iv = kv_it + 2 * (nkv - 1) + 1, sv = iv % kStages;
                 mbar_wait(&kv_full[sv], (iv / kStages) & 1);
@@ -334,9 +335,9 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                     if (nkv == 1 && n_item > 0) mbar_wait(&o_empty[i], (n_item - 1) & 1);
                     tc_fence_after();
                     issue_pv(i, sv, nkv - 1 > 0);
-                    mma_commit(&o_final[i]);
+                    mma_commit_w(&o_final[i]);
                 }
-                mma_commit(&kv_empty[sv]);
+                mma_commit_w(&kv_empty[sv]);
                 kv_it += 2 * nkv;
                 g += nkv;
             }
