@@ -42,7 +42,8 @@ def _nccl_default() -> str:
 
 
 def _flags():
-    return ARCH + ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC",
+    extra = ["-DTM_TRACE_ENABLED"] if os.environ.get("TM_TRACE_BUILD") == "1" else []
+    return extra + ARCH + ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC",
                    "-Xptxas", "-v", f"-I{os.path.join(ROOT, 'include')}",
                    f'-DTM_NCCL_DEFAULT="{_nccl_default()}"']
 
@@ -58,6 +59,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
     hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "tm.h"),
                                                      os.path.abspath(__file__)]
+    stamp = os.path.join(BUILD, "flags.txt")
+    flags_now = " ".join(_flags())
+    if not os.path.exists(stamp) or open(stamp).read() != flags_now:
+        force = True
+        with open(stamp, "w") as f:
+            f.write(flags_now)
     objs, jobs = [], []
     for s in SOURCES:
         src = os.path.join(CSRC, s)

@@ -85,9 +85,15 @@ struct __align__(64) FmhaParams {
 // Debug timeline: role r in [0,4) owns trace[r*kTraceCap ..]; entry =
 // clock64() << 8 | event code.  Only CTA 0 records; off when p.trace == 0.
 constexpr int kTraceCap = 4096;
+// Compiled in only with -DTM_TRACE_ENABLED (TM_TRACE_BUILD=1 python -m
+// paper_2506_03099_b200.build); the production build has no trace code.
 __device__ __forceinline__ void trace_ev(const FmhaParams& p, int role, int& n, int code) {
+#ifdef TM_TRACE_ENABLED
     if (p.trace != nullptr && blockIdx.x == 0 && n < kTraceCap)
         p.trace[role * kTraceCap + n++] = (static_cast<unsigned long long>(clock64()) << 8) | code;
+#else
+    (void)p; (void)role; (void)n; (void)code;
+#endif
 }
 
 struct Item {
@@ -374,32 +380,67 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                     for (int c = 0; c < kBN; ++c)
                         if (c >= valid) r[c] = 0xff800000u;   // -inf: key beyond the segment
                 }
-                // row max: 3-input max tree (depth 5)
-                float t1[43];
+                // exps of the row against the running max m_run: P -> TMEM (bf16
+                // over S_i), returns the row sum of this tile.  7 of every 16
+                // pairs use the FMA-pipe polynomial, interleaved with MUFU.
+                auto exps = [&](float mrun) -> float {
+                    const float nm = (mrun == -INFINITY) ? 0.f : -mrun;
+                    const float2 sc2 = make_float2(sl2, sl2), nm2 = make_float2(nm, nm);
+                    float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                                     make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
-                for (int k = 0; k < 42; ++k)
-                    t1[k] = max3(__uint_as_float(r[3 * k]), __uint_as_float(r[3 * k + 1]),
-                                 __uint_as_float(r[3 * k + 2]));
-                t1[42] = fmaxf(__uint_as_float(r[126]), __uint_as_float(r[127]));
-                float t2[15];
+                    for (int c = 0; c < 4; ++c) {
+                        uint32_t pk[16];
 #pragma unroll
-                for (int k = 0; k < 14; ++k) t2[k] = max3(t1[3 * k], t1[3 * k + 1], t1[3 * k + 2]);
-                t2[14] = t1[42];
-                float t3[5];
+                        for (int e = 0; e < 16; ++e) {
+                            const float2 x = ffma2(make_float2(__uint_as_float(r[32 * c + 2 * e]),
+                                                               __uint_as_float(r[32 * c + 2 * e + 1])),
+                                                   sc2, nm2);
+                            float2 pe;
+                            constexpr uint32_t kPolyMask = 0xA54Au;   // e in {1,3,6,8,10,13,15}
+                            if ((kPolyMask >> e) & 1) {
+                                pe = exp2_poly2(x);
+                            } else {
+                                pe.x = ex2(x.x);
+                                pe.y = ex2(x.y);
+                            }
+                            acc[e & 3] = fadd2(acc[e & 3], pe);
+                            pk[e] = pack_bf16x2(pe.x, pe.y);
+                        }
+                        tmem_st16(tSi + c * 16, pk);
+                    }
+                    const float2 s01 = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
+                    return s01.x + s01.y;
+                };
+                auto row_max = [&]() -> float {   // 3-input max tree (depth 5)
+                    float t1[43];
 #pragma unroll
-                for (int k = 0; k < 5; ++k) t3[k] = max3(t2[3 * k], t2[3 * k + 1], t2[3 * k + 2]);
-                const float mx = max3(max3(t3[0], t3[1], t3[2]), t3[3], t3[4]);
-
+                    for (int k = 0; k < 42; ++k)
+                        t1[k] = max3(__uint_as_float(r[3 * k]), __uint_as_float(r[3 * k + 1]),
+                                     __uint_as_float(r[3 * k + 2]));
+                    t1[42] = fmaxf(__uint_as_float(r[126]), __uint_as_float(r[127]));
+                    float t2[15];
+#pragma unroll
+                    for (int k = 0; k < 14; ++k) t2[k] = max3(t1[3 * k], t1[3 * k + 1], t1[3 * k + 2]);
+                    t2[14] = t1[42];
+                    float t3[5];
+#pragma unroll
+                    for (int k = 0; k < 5; ++k) t3[k] = max3(t2[3 * k], t2[3 * k + 1], t2[3 * k + 2]);
+                    return max3(max3(t3[0], t3[1], t3[2]), t3[3], t3[4]);
+                };
+                // Lazy running max: the first tile of an item sets m_run to its
+                // exact row max; later tiles reuse m_run and only fall back
+                // (exact max, O rescale, recompute) when some weight would
+                // exceed ~2^24 -- the result is exact either way after O / l.
+                if (j == it.lo) m_run = row_max() * sl2;
                 if (tr) trace_ev(p, 2 + i, tn, 22);
-                const float m_new = fmaxf(m_run, mx * sl2);
-                const bool need = m_new > m_run + 8.0f;
-                float alpha = 1.f;
-                if (need) {
-                    alpha = ex2(m_run - m_new);
+                float tsum = exps(m_run);
+                const bool bad = !(tsum <= 16777216.f);      // also catches inf / nan
+                if (__any_sync(0xffffffffu, bad)) {
+                    const float m_new = fmaxf(m_run, row_max() * sl2);
+                    const float alpha = ex2(m_run - m_new);
                     m_run = m_new;
-                }
-                l *= alpha;
-                if (j > it.lo && __any_sync(0xffffffffu, need)) {
+                    l *= alpha;
                     // O_i was last written by PV_i_{j-1}, complete before s_full fired.
 #pragma unroll
                     for (int c = 0; c < D; c += 32) {
@@ -411,33 +452,9 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                             o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
                         tmem_st32(tOi + c, o);
                     }
+                    tsum = exps(m_run);
                 }
-                const float nm = (m_run == -INFINITY) ? 0.f : -m_run;
-                const float2 sc2 = make_float2(sl2, sl2), nm2 = make_float2(nm, nm);
-                float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f),
-                                 make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-#pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    uint32_t pk[16];
-#pragma unroll
-                    for (int e = 0; e < 16; ++e) {
-                        const float2 x = ffma2(make_float2(__uint_as_float(r[32 * c + 2 * e]),
-                                                           __uint_as_float(r[32 * c + 2 * e + 1])),
-                                               sc2, nm2);
-                        float2 pe;
-                        if (e < 10) {                       // cols 0..19 of each 32: MUFU
-                            pe.x = ex2(x.x);
-                            pe.y = ex2(x.y);
-                        } else {                            // cols 20..31: FMA-pipe polynomial
-                            pe = exp2_poly2(x);
-                        }
-                        acc[e & 3] = fadd2(acc[e & 3], pe);
-                        pk[e] = pack_bf16x2(pe.x, pe.y);
-                    }
-                    tmem_st16(tSi + c * 16, pk);
-                }
-                const float2 s01 = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
-                l += s01.x + s01.y;
+                l += tsum;
                 if (tr) trace_ev(p, 2 + i, tn, 23);
                 tmem_wait_st();
                 tc_fence_before();

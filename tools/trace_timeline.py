@@ -19,6 +19,10 @@ if os.path.exists(PATH):
     os.unlink(PATH)
 os.environ["TM_TRACE"] = PATH
 
+import subprocess  # noqa: E402
+os.environ["TM_TRACE_BUILD"] = "1"
+subprocess.check_call([sys.executable, "-m", "paper_2506_03099_b200.build"], cwd=ROOT,
+                      stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
 import torch  # noqa: E402
 
 from paper_2506_03099_b200 import tm  # noqa: E402
