@@ -41,6 +41,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -188,7 +189,7 @@ __device__ __forceinline__ void softmax_bar() {   // the 256 softmax threads onl
     asm volatile("bar.sync 1, 256;" ::: "memory");
 }
 
-template <int D>
+template <int D, uint32_t kPolyMask>
 __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_constant__ FmhaParams p) {
     constexpr int kTileBytes = kBN * D * 2;
     constexpr uint32_t kIdescS = make_idesc_bf16(kBM, kBN, 0, 0);   // Q, K both K-major
@@ -397,7 +398,6 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                                                                __uint_as_float(r[32 * c + 2 * e + 1])),
                                                    sc2, nm2);
                             float2 pe;
-                            constexpr uint32_t kPolyMask = 0xA54Au;   // e in {1,3,6,8,10,13,15}
                             if ((kPolyMask >> e) & 1) {
                                 pe = exp2_poly2(x);
                             } else {
@@ -602,18 +602,37 @@ int sm_count() {
     return n;
 }
 
-template <int D>
+template <int D, uint32_t kPolyMask>
 cudaError_t launch_t(const FmhaParams& p, int grid, cudaStream_t stream) {
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(fmha_sm100_kernel<D>,
+        cudaError_t e = cudaFuncSetAttribute(fmha_sm100_kernel<D, kPolyMask>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              smem_bytes<D>());
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    fmha_sm100_kernel<D><<<grid, kThreads, smem_bytes<D>(), stream>>>(p);
+    fmha_sm100_kernel<D, kPolyMask><<<grid, kThreads, smem_bytes<D>(), stream>>>(p);
     return cudaGetLastError();
+}
+
+// Which of every 16 exp2 pairs run as the FMA-pipe polynomial (bit e set) --
+// the MUFU/FMA balance.  Default 7/16; TM_POLY (tuning/debug) selects others.
+constexpr uint32_t kPolyDefault = 0xA54Au;   // e in {1,3,6,8,10,13,15}
+template <int D>
+cudaError_t launch_d(const FmhaParams& p, int grid, cudaStream_t stream) {
+    static int sel = [] {
+        const char* e = getenv("TM_POLY");
+        return e ? atoi(e) : 7;
+    }();
+    switch (sel) {
+        case 0: return launch_t<D, 0x0000u>(p, grid, stream);
+        case 4: return launch_t<D, 0x4444u>(p, grid, stream);   // {2,6,10,14}
+        case 5: return launch_t<D, 0x2492u>(p, grid, stream);   // {1,4,7,10,13}
+        case 6: return launch_t<D, 0x4A4Au>(p, grid, stream);   // {1,3,6,9,11,14}
+        case 8: return launch_t<D, 0xAAAAu>(p, grid, stream);
+        default: return launch_t<D, kPolyDefault>(p, grid, stream);
+    }
 }
 
 }  // namespace
@@ -667,7 +686,7 @@ cudaError_t launch_fmha_sm100(const AttnProblem& pr, void* scratch, cudaStream_t
     p.counters = reinterpret_cast<int*>(static_cast<uint8_t*>(scratch) +
                                         size_t(kMaxPersistentCtas) * (256 * size_t(pr.d) + 512) * 4);
     const int grid = R > 0 ? C : T * S;
-    cudaError_t e = pr.d == 128 ? launch_t<128>(p, grid, stream) : launch_t<64>(p, grid, stream);
+    cudaError_t e = pr.d == 128 ? launch_d<128>(p, grid, stream) : launch_d<64>(p, grid, stream);
     if (e == cudaSuccess && launches) ++*launches;
     return e;
 }
