@@ -26,8 +26,8 @@
 //   warps 0-7   softmax, one warpgroup per Q tile, one thread per query row
 //               (tcgen05.ld 32x32b puts a whole S row in one thread's
 //               registers): 3-input-max tree, exp2 with scale*log2(e) folded
-//               into one packed FFMA2, 62.5% of the exponentials on the MUFU
-//               pipe and 37.5% as a degree-3 polynomial on the FMA pipe (the
+//               into one packed FFMA2, 75% of the exponentials on the MUFU
+//               pipe and 25% as a degree-3 polynomial on the FMA pipe (the
 //               MUFU rate equals the tensor rate at d=128), packed FADD2 row
 //               sums, conditional O rescale (only when the running max grows
 //               by > 8 in log2 units -- exact after the final 1/l), P rounded
@@ -170,9 +170,13 @@ __device__ __forceinline__ float2 exp2_poly2(float2 x) {
                      make_float2(0.24260999262332916f, 0.24260999262332916f));
     p = ffma2(p, f, make_float2(0.6932609677314758f, 0.6932609677314758f));
     p = ffma2(p, f, make_float2(0.9999281167984009f, 0.9999281167984009f));
-    p.x = __uint_as_float(__float_as_uint(p.x) + (__float_as_uint(j.x) << 23));
-    p.y = __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(j.y) << 23));
-    return p;
+    // exponent insertion on the ALU pipe (SHL + IADD), not IMAD on the busy FMA pipe
+    uint32_t ex, ey;
+    asm("{\n\t.reg .b32 t;\n\tshl.b32 t, %1, 23;\n\tadd.u32 %0, %2, t;\n\t}"
+        : "=r"(ex) : "r"(__float_as_uint(j.x)), "r"(__float_as_uint(p.x)));
+    asm("{\n\t.reg .b32 t;\n\tshl.b32 t, %1, 23;\n\tadd.u32 %0, %2, t;\n\t}"
+        : "=r"(ey) : "r"(__float_as_uint(j.y)), "r"(__float_as_uint(p.y)));
+    return make_float2(__uint_as_float(ex), __uint_as_float(ey));
 }
 
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
@@ -617,17 +621,17 @@ cudaError_t launch_t(const FmhaParams& p, int grid, cudaStream_t stream) {
 }
 
 // Which of every 16 exp2 pairs run as the FMA-pipe polynomial (bit e set) --
-// the MUFU/FMA balance.  Default 7/16; TM_POLY (tuning/debug) selects others.
-constexpr uint32_t kPolyDefault = 0xA54Au;   // e in {1,3,6,8,10,13,15}
+// the MUFU/FMA balance.  Default 4/16 (fastest in the TM_POLY sweep).
+constexpr uint32_t kPolyDefault = 0x4444u;   // e in {2,6,10,14} (sweep: fastest)
 template <int D>
 cudaError_t launch_d(const FmhaParams& p, int grid, cudaStream_t stream) {
     static int sel = [] {
         const char* e = getenv("TM_POLY");
-        return e ? atoi(e) : 7;
+        return e ? atoi(e) : 4;
     }();
     switch (sel) {
         case 0: return launch_t<D, 0x0000u>(p, grid, stream);
-        case 4: return launch_t<D, 0x4444u>(p, grid, stream);   // {2,6,10,14}
+        case 7: return launch_t<D, 0xA54Au>(p, grid, stream);   // {1,3,6,8,10,13,15}
         case 5: return launch_t<D, 0x2492u>(p, grid, stream);   // {1,4,7,10,13}
         case 6: return launch_t<D, 0x4A4Au>(p, grid, stream);   // {1,3,6,9,11,14}
         case 8: return launch_t<D, 0xAAAAu>(p, grid, stream);
