@@ -14,7 +14,7 @@
 // into S = C/T pieces so the last wave fills the machine (split-KV tail);
 // the last piece of a unit to finish merges the pieces' (O, m, l) in fixed
 // piece order (deterministic, no floating-point atomics).
-// Warp roles (576 threads, 112 registers each):
+// Warp roles (640 threads; setmaxnreg: softmax 104 regs, TMA/MMA 64):
 //   warp 16     TMA producer: Q_i per unit (reloaded per tile as soon as its
 //               last S MMA completes), K_j / V_j through a 4-slot smem ring
 //               (cp.async.bulk.tensor, 128B swizzle).
@@ -57,8 +57,12 @@ constexpr int kBM = 128;          // query rows per Q tile
 constexpr int kBN = 128;          // keys per KV tile
 constexpr int kStages = 4;        // K/V smem ring slots
 constexpr int kSoftmaxThreads = 512;  // 4 warpgroups: 2 Q tiles x 2 column halves
-constexpr int kThreads = 576;     // + TMA warp + MMA warp: 18 warps -> 112 regs/thread
+constexpr int kThreads = 640;     // + {TMA, MMA, 2 spare} warpgroup
 constexpr int kTmaWarp = 16, kMmaWarp = 17;
+// Registers are granted per 4-warp group: 640 threads launch with 96 each;
+// setmaxnreg moves them to the softmax warpgroups (4 x 128 x 104 + 128 x 64).
+constexpr int kRegsSoftmax = 104, kRegsOther = 64;
+static_assert(kSoftmaxThreads * kRegsSoftmax + 128 * kRegsOther <= kThreads * 96, "register pool");
 constexpr int kHalfBytes = 128 * 128;   // one 64-column (128 B) half of a 128-row tile
 // TMEM columns: one S buffer shared by both Q tiles, P0/P1 (bf16 pairs), O0/O1.
 constexpr uint32_t kColS = 0, kColP = 128, kColO = 256;
@@ -218,7 +222,7 @@ __device__ __forceinline__ bool bar_red_or(uint32_t id, uint32_t n, bool pred) {
 }
 
 template <int D, uint32_t kPolyMask>
-__global__ void __maxnreg__(112)
+__global__ void __launch_bounds__(kThreads, 1)
 fmha_sm100_kernel(const __grid_constant__ FmhaParams p) {
     constexpr int kTileBytes = kBN * D * 2;
     constexpr uint32_t kIdescS = make_idesc_bf16(kBM, kBN, 0, 0);   // Q, K both K-major
@@ -278,6 +282,7 @@ fmha_sm100_kernel(const __grid_constant__ FmhaParams p) {
     const uint32_t tmem = *tmem_holder;
 
     if (warp >= kSoftmaxThreads / 32) {
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsOther));
       if (warp == kTmaWarp) {
         // ------------------------------------------------ TMA producer
         if (lane == 0) {
@@ -318,7 +323,7 @@ fmha_sm100_kernel(const __grid_constant__ FmhaParams p) {
             constexpr uint32_t kTile16 = kTileBytes >> 4;      // descriptor address units
             auto issue_s = [&](int i, int slot) {      // S = Q_i K^T into the S buffer
                 const uint64_t a0 = dq + i * kTile16, b0 = dk + slot * kTile16;
-#pragma unroll
+#pragma unroll 1
                 for (int kk = 0; kk < D / 16; ++kk) {
                     const uint32_t off = (kk >> 2) * (kHalfBytes >> 4) + (kk & 3) * 2;
                     mma_ss_w(tmem + kColS, a0 + off, b0 + off, kIdescS, kk > 0);
@@ -326,7 +331,7 @@ fmha_sm100_kernel(const __grid_constant__ FmhaParams p) {
             };
             auto issue_pv = [&](int i, int slot, bool acc) {   // O_i += P_i V
                 const uint64_t b0 = dv + slot * kTile16;
-#pragma unroll
+#pragma unroll 1
                 for (int kk = 0; kk < kBN / 16; ++kk)
                     mma_ts_w(tmem + kColO + i * D, tmem + kColP + i * 64 + kk * 8, b0 + kk * 128,
                              kIdescO, (acc || kk > 0) ? 1u : 0u);
@@ -384,6 +389,7 @@ fmha_sm100_kernel(const __grid_constant__ FmhaParams p) {
         }
       }
     } else {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsSoftmax));
         // ------------------------------------------------ softmax + epilogue (warps 0-15)
         // Warp w: Q tile i = w/8, column half hh = (w/4)%2, TMEM lane quarter wq = w%4.
         // Threads (hh=0, hh=1) of the same row hold S columns [0,64) / [64,128),
