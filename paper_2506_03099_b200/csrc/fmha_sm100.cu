@@ -14,20 +14,20 @@
 // into S = C/T pieces so the last wave fills the machine (split-KV tail);
 // the last piece of a unit to finish merges the pieces' (O, m, l) in fixed
 // piece order (deterministic, no floating-point atomics).
-// Warp roles (640 threads; setmaxnreg: softmax 104 regs, TMA/MMA 64):
-//   warp 16     TMA producer: Q_i per unit (reloaded per tile as soon as its
+// Warp roles (384 threads; setmaxnreg gives the softmax warpgroups 232 regs):
+//   warp 8      TMA producer: Q_i per unit (reloaded per tile as soon as its
 //               last S MMA completes), K_j / V_j through a 4-slot smem ring
 //               (cp.async.bulk.tensor, 128B swizzle).
-//   warp 17     tcgen05 MMA issuer (one thread) + TMEM owner:
+//   warp 9      tcgen05 MMA issuer (one thread) + TMEM owner:
 //                 S_i = Q_i K_j^T  (SS, M=128 N=128 K=d, fp32 in TMEM)
 //                 O_i += P_i V_j   (TS: P_i bf16 read from TMEM, V MN-major)
 //               issue order S0_j, PV0_{j-1}, S1_j, PV1_{j-1} into ONE shared S
 //               buffer and separate P_i columns, so S_i(j) is computed while
 //               softmax_i is still on tile j-1 (the softmax never waits for
 //               its own PV + S round trip).
-//   warps 0-15  softmax, two warpgroups per Q tile, two threads per query row
-//               (tcgen05.ld 32x32b puts 64 of its 128 S columns in each
-//               thread's registers): 3-input-max tree, exp2 with scale*log2(e) folded
+//   warps 0-7   softmax, one warpgroup per Q tile, one thread per query row
+//               (tcgen05.ld 32x32b puts a whole S row in one thread's
+//               registers): 3-input-max tree, exp2 with scale*log2(e) folded
 //               into one packed FFMA2, 75% of the exponentials on the MUFU
 //               pipe and 25% as a degree-3 polynomial on the FMA pipe (the
 //               MUFU rate equals the tensor rate at d=128), packed FADD2 row
@@ -56,13 +56,12 @@ namespace {
 constexpr int kBM = 128;          // query rows per Q tile
 constexpr int kBN = 128;          // keys per KV tile
 constexpr int kStages = 4;        // K/V smem ring slots
-constexpr int kSoftmaxThreads = 512;  // 4 warpgroups: 2 Q tiles x 2 column halves
-constexpr int kThreads = 640;     // + {TMA, MMA, 2 spare} warpgroup
-constexpr int kTmaWarp = 16, kMmaWarp = 17;
-// Registers are granted per 4-warp group: 640 threads launch with 96 each;
-// setmaxnreg moves them to the softmax warpgroups (4 x 128 x 104 + 128 x 64).
-constexpr int kRegsSoftmax = 104, kRegsOther = 64;
-static_assert(kSoftmaxThreads * kRegsSoftmax + 128 * kRegsOther <= kThreads * 96, "register pool");
+constexpr int kThreads = 384;     // 2 softmax warpgroups + {TMA, MMA, 2 spare} warpgroup
+constexpr int kRegsSoftmax = 208; // setmaxnreg budgets (see the static_assert)
+constexpr int kRegsOther = 88;
+// The CTA launches with 168 regs/thread (64K / 384 rounded down to 8); setmaxnreg
+// only redistributes that pool, so the budgets must fit in 384 x 168.
+static_assert(256 * kRegsSoftmax + 128 * kRegsOther <= kThreads * 168, "register pool");
 constexpr int kHalfBytes = 128 * 128;   // one 64-column (128 B) half of a 128-row tile
 // TMEM columns: one S buffer shared by both Q tiles, P0/P1 (bf16 pairs), O0/O1.
 constexpr uint32_t kColS = 0, kColP = 128, kColO = 256;
@@ -194,36 +193,12 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
         : "memory");
 }
 
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* r) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
-        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
-          "=r"(r[14]), "=r"(r[15])
-        : "r"(taddr));
-}
-__device__ __forceinline__ void softmax_bar() {   // the 512 softmax threads only
-    asm volatile("bar.sync 1, 512;" ::: "memory");
-}
-__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t n) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-// Named barrier with an OR reduction of a predicate over the participants.
-__device__ __forceinline__ bool bar_red_or(uint32_t id, uint32_t n, bool pred) {
-    uint32_t out;
-    asm volatile(
-        "{\n\t.reg .pred pi, po;\n\tsetp.ne.u32 pi, %1, 0;\n\t"
-        "bar.red.or.pred po, %2, %3, pi;\n\tselp.u32 %0, 1, 0, po;\n\t}"
-        : "=r"(out)
-        : "r"(uint32_t(pred)), "r"(id), "r"(n)
-        : "memory");
-    return out != 0;
+__device__ __forceinline__ void softmax_bar() {   // the 256 softmax threads only
+    asm volatile("bar.sync 1, 256;" ::: "memory");
 }
 
 template <int D, uint32_t kPolyMask>
-__global__ void __launch_bounds__(kThreads, 1)
-fmha_sm100_kernel(const __grid_constant__ FmhaParams p) {
+__global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_constant__ FmhaParams p) {
     constexpr int kTileBytes = kBN * D * 2;
     constexpr uint32_t kIdescS = make_idesc_bf16(kBM, kBN, 0, 0);   // Q, K both K-major
     constexpr uint32_t kIdescO = make_idesc_bf16(kBM, D, 0, 1);     // P (TMEM), V MN-major
@@ -245,8 +220,6 @@ fmha_sm100_kernel(const __grid_constant__ FmhaParams p) {
     uint64_t* s_free = o_done + 2;           // [1]  S buffer loaded into registers
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(s_free + 1);
     int* merge_flag = reinterpret_cast<int*>(tmem_holder + 1);
-    // half-row exchange: max [2 tiles][2 halves][128 rows], then l, same shape
-    float* xchg = reinterpret_cast<float*>(bars + 64);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -256,34 +229,34 @@ fmha_sm100_kernel(const __grid_constant__ FmhaParams p) {
             mbar_init(&q_full[i], 1);
             mbar_init(&q_empty[i], 1);
             mbar_init(&s_full[i], 1);
-            mbar_init(&p_full[i], 256);     // both column halves of a tile
+            mbar_init(&p_full[i], 128);
             mbar_init(&o_final[i], 1);
-            mbar_init(&o_empty[i], 256);
+            mbar_init(&o_empty[i], 128);
             mbar_init(&o_done[i], 1);
         }
-        mbar_init(s_free, 256);
+        mbar_init(s_free, 128);
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&kv_full[s], 1);
             mbar_init(&kv_empty[s], 1);
         }
         fence_mbar_init();
     }
-    if (warp == kTmaWarp && lane == 0) {
+    if (warp == 8 && lane == 0) {
         tma_prefetch(&p.tq);
         for (int s = 0; s < p.nseg; ++s) {
             tma_prefetch(&p.tk[s]);
             tma_prefetch(&p.tv[s]);
         }
     }
-    if (warp == kMmaWarp) tmem_alloc(tmem_holder, 512);
+    if (warp == 9) tmem_alloc(tmem_holder, 512);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_holder;
 
-    if (warp >= kSoftmaxThreads / 32) {
+    if (warp >= 8) {
       asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsOther));
-      if (warp == kTmaWarp) {
+      if (warp == 8) {
         // ------------------------------------------------ TMA producer
         if (lane == 0) {
             int tn = 0;
@@ -313,7 +286,7 @@ fmha_sm100_kernel(const __grid_constant__ FmhaParams p) {
                 }
             }
         }
-      } else if (warp == kMmaWarp) {
+      } else if (warp == 9) {
         // ------------------------------------------------ MMA issuer
         {   // the whole warp runs the loop (uniform operands live in uniform
             // registers); one elected lane issues each tcgen05 instruction.
@@ -323,7 +296,7 @@ fmha_sm100_kernel(const __grid_constant__ FmhaParams p) {
             constexpr uint32_t kTile16 = kTileBytes >> 4;      // descriptor address units
             auto issue_s = [&](int i, int slot) {      // S = Q_i K^T into the S buffer
                 const uint64_t a0 = dq + i * kTile16, b0 = dk + slot * kTile16;
-#pragma unroll 1
+#pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk) {
                     const uint32_t off = (kk >> 2) * (kHalfBytes >> 4) + (kk & 3) * 2;
                     mma_ss_w(tmem + kColS, a0 + off, b0 + off, kIdescS, kk > 0);
@@ -331,7 +304,7 @@ fmha_sm100_kernel(const __grid_constant__ FmhaParams p) {
             };
             auto issue_pv = [&](int i, int slot, bool acc) {   // O_i += P_i V
                 const uint64_t b0 = dv + slot * kTile16;
-#pragma unroll 1
+#pragma unroll
                 for (int kk = 0; kk < kBN / 16; ++kk)
                     mma_ts_w(tmem + kColO + i * D, tmem + kColP + i * 64 + kk * 8, b0 + kk * 128,
                              kIdescO, (acc || kk > 0) ? 1u : 0u);
@@ -390,127 +363,125 @@ fmha_sm100_kernel(const __grid_constant__ FmhaParams p) {
       }
     } else {
         asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsSoftmax));
-        // ------------------------------------------------ softmax + epilogue (warps 0-15)
-        // Warp w: Q tile i = w/8, column half hh = (w/4)%2, TMEM lane quarter wq = w%4.
-        // Threads (hh=0, hh=1) of the same row hold S columns [0,64) / [64,128),
-        // write P columns [0,32) / [32,64) of P_i and own O columns
-        // [0,D/2) / [D/2,D); their running max stays identical: a named-barrier
-        // OR-reduction flags when either half needs a new max, and the halves
-        // then exchange maxima through shared memory (rare).
-        const int i = warp >> 3, hh = (warp >> 2) & 1, wq = warp & 3;
-        const int row = wq * 32 + lane;                           // row in the Q tile
-        const int row_in_pair = i * kBM + row;                    // 0..255
+        // ------------------------------------------------ softmax + epilogue (warps 0-7)
+        const int i = warp >> 2, wq = warp & 3;
+        const int row_in_pair = i * kBM + wq * 32 + lane;       // 0..255
         const uint32_t lane_off = uint32_t(wq * 32) << 16;
-        const uint32_t tS = tmem + lane_off + kColS + hh * 64;
-        const uint32_t tPi = tmem + lane_off + kColP + i * 64 + hh * 32;
-        constexpr int kDH = D / 2;                                // O columns per half
-        const uint32_t tOi = tmem + lane_off + kColO + i * D + hh * kDH;
-        const uint32_t pair_bar = 2 + i * 4 + wq;                 // the two warps of a row quarter
-        float* xm = xchg + (i * 2 + hh) * 128;                    // my half's exchange slots
-        const float* xm_other = xchg + (i * 2 + (hh ^ 1)) * 128;
+        const uint32_t tS = tmem + lane_off + kColS;
+        const uint32_t tPi = tmem + lane_off + kColP + i * 64;
+        const uint32_t tOi = tmem + lane_off + kColO + i * D;
         const float sl2 = p.scale_log2;
         uint32_t g = 0, n_item = 0;
         int tn = 0;
-        const bool tr = (wq == 0 && lane == 0 && hh == 0);
+        const bool tr = (wq == 0 && lane == 0);
         Item it;
         for (int w = blockIdx.x; get_item(p, w, it); w += gridDim.x, ++n_item) {
             float m_run = -INFINITY, l = 0.f;
             for (int j = it.lo; j < it.hi; ++j, ++g) {
-                int seg, srow, valid;
-                tile_info(p, j, seg, srow, valid);
-                uint32_t r[64];
+                int seg, row, valid;
+                tile_info(p, j, seg, row, valid);
+                uint32_t r[kBN];
                 mbar_wait(&s_full[i], g & 1);
                 if (tr) trace_ev(p, 2 + i, tn, 20);
                 tc_fence_after();
-                tmem_ld32(tS, r);
-                tmem_ld32(tS + 32, r + 32);
+#pragma unroll
+                for (int c = 0; c < kBN; c += 32) tmem_ld32(tS + c, r + c);
                 tmem_wait_ld();
                 tc_fence_before();
                 mbar_arrive(s_free);          // the S buffer may be refilled
                 if (tr) trace_ev(p, 2 + i, tn, 21);
                 if (valid < kBN) {
-                    const int vh = valid - hh * 64;           // valid columns in my half
 #pragma unroll
-                    for (int c = 0; c < 64; ++c)
-                        if (c >= vh) r[c] = 0xff800000u;      // -inf: key beyond the segment
+                    for (int c = 0; c < kBN; ++c)
+                        if (c >= valid) r[c] = 0xff800000u;   // -inf: key beyond the segment
                 }
-                // half-row max: 3-input max tree
-                float t1[22];
-#pragma unroll
-                for (int k = 0; k < 21; ++k)
-                    t1[k] = max3(__uint_as_float(r[3 * k]), __uint_as_float(r[3 * k + 1]),
-                                 __uint_as_float(r[3 * k + 2]));
-                t1[21] = __uint_as_float(r[63]);
-                float t2[8];
-#pragma unroll
-                for (int k = 0; k < 7; ++k) t2[k] = max3(t1[3 * k], t1[3 * k + 1], t1[3 * k + 2]);
-                t2[7] = t1[21];
-                const float hmax = max3(max3(t2[0], t2[1], t2[2]), max3(t2[3], t2[4], t2[5]),
-                                        fmaxf(t2[6], t2[7]));
-                // Conditional rescale: only when the row max grows by > 8 (log2
-                // units); exact after the final O / l.
-                const bool need = hmax * sl2 > m_run + 8.0f;
+                // exps of the row against the running max m_run: P -> TMEM (bf16,
+                // P_i columns), returns the row sum of this tile.  kPolyMask pairs
+                // of every 16 use the FMA-pipe polynomial, interleaved with MUFU.
+                // Before the first store into P_i, the previous PV_i (which reads
+                // P_i) must be complete: waited on o_done only then, so the wait
+                // overlaps the first chunk's exps.
                 bool pv_waited = (g == 0);
-                auto wait_prev_pv = [&]() {     // previous PV_i (reads P_i, writes O_i) complete
+                auto wait_prev_pv = [&]() {
                     if (!pv_waited) {
                         mbar_wait(&o_done[i], (g - 1) & 1);
                         tc_fence_after();
                         pv_waited = true;
                     }
                 };
-                // (the O rescale runs after the exps, when r[] is dead: less register pressure)
-                float alpha = 1.f;
-                const bool rescale = bar_red_or(pair_bar, 64, need);
-                if (rescale) {
-                    xm[row] = hmax;
-                    named_bar_sync(pair_bar, 64);
-                    const float m_new = fmaxf(m_run, fmaxf(hmax, xm_other[row]) * sl2);
-                    alpha = ex2(m_run - m_new);
+                auto exps = [&](float mrun) -> float {
+                    const float nm = (mrun == -INFINITY) ? 0.f : -mrun;
+                    const float2 sc2 = make_float2(sl2, sl2), nm2 = make_float2(nm, nm);
+                    float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                                     make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        uint32_t pk[16];
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) {
+                            const float2 x = ffma2(make_float2(__uint_as_float(r[32 * c + 2 * e]),
+                                                               __uint_as_float(r[32 * c + 2 * e + 1])),
+                                                   sc2, nm2);
+                            float2 pe;
+                            if ((kPolyMask >> e) & 1) {
+                                pe = exp2_poly2(x);
+                            } else {
+                                pe.x = ex2(x.x);
+                                pe.y = ex2(x.y);
+                            }
+                            acc[e & 3] = fadd2(acc[e & 3], pe);
+                            pk[e] = pack_bf16x2(pe.x, pe.y);
+                        }
+                        if (c == 0) wait_prev_pv();
+                        tmem_st16(tPi + c * 16, pk);
+                    }
+                    const float2 s01 = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
+                    return s01.x + s01.y;
+                };
+                auto row_max = [&]() -> float {   // 3-input max tree (depth 5)
+                    float t1[43];
+#pragma unroll
+                    for (int k = 0; k < 42; ++k)
+                        t1[k] = max3(__uint_as_float(r[3 * k]), __uint_as_float(r[3 * k + 1]),
+                                     __uint_as_float(r[3 * k + 2]));
+                    t1[42] = fmaxf(__uint_as_float(r[126]), __uint_as_float(r[127]));
+                    float t2[15];
+#pragma unroll
+                    for (int k = 0; k < 14; ++k) t2[k] = max3(t1[3 * k], t1[3 * k + 1], t1[3 * k + 2]);
+                    t2[14] = t1[42];
+                    float t3[5];
+#pragma unroll
+                    for (int k = 0; k < 5; ++k) t3[k] = max3(t2[3 * k], t2[3 * k + 1], t2[3 * k + 2]);
+                    return max3(max3(t3[0], t3[1], t3[2]), t3[3], t3[4]);
+                };
+                // Lazy running max: the first tile of an item sets m_run to its
+                // exact row max; later tiles reuse m_run and only fall back
+                // (exact max, O rescale, recompute) when some weight would
+                // exceed ~2^24 -- the result is exact either way after O / l.
+                if (j == it.lo) m_run = row_max() * sl2;
+                if (tr) trace_ev(p, 2 + i, tn, 22);
+                float tsum = exps(m_run);
+                const bool bad = !(tsum <= 16777216.f);      // also catches inf / nan
+                if (__any_sync(0xffffffffu, bad)) {
+                    const float m_new = fmaxf(m_run, row_max() * sl2);
+                    const float alpha = ex2(m_run - m_new);
                     m_run = m_new;
                     l *= alpha;
-                }
-                if (tr) trace_ev(p, 2 + i, tn, 22);
-                // exps of my 64 columns: P -> TMEM (bf16 pairs), row-sum partial.
-                const float nm = (m_run == -INFINITY) ? 0.f : -m_run;
-                const float2 sc2 = make_float2(sl2, sl2), nm2 = make_float2(nm, nm);
-                float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f),
-                                 make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+                    // O_i was last written by PV_i(j-1): complete (o_done waited).
+                    wait_prev_pv();
 #pragma unroll
-                for (int c = 0; c < 2; ++c) {
-                    uint32_t pk[16];
-#pragma unroll
-                    for (int e = 0; e < 16; ++e) {
-                        const float2 x = ffma2(make_float2(__uint_as_float(r[32 * c + 2 * e]),
-                                                           __uint_as_float(r[32 * c + 2 * e + 1])),
-                                               sc2, nm2);
-                        float2 pe;
-                        if ((kPolyMask >> e) & 1) {
-                            pe = exp2_poly2(x);
-                        } else {
-                            pe.x = ex2(x.x);
-                            pe.y = ex2(x.y);
-                        }
-                        acc[e & 3] = fadd2(acc[e & 3], pe);
-                        pk[e] = pack_bf16x2(pe.x, pe.y);
-                    }
-                    if (c == 0) wait_prev_pv();
-                    tmem_st16(tPi + c * 16, pk);
-                }
-                const float2 s01 = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
-                l += s01.x + s01.y;
-                if (rescale && j > it.lo) {
-                    // O_i was last written by PV_i(j-1): complete (o_done waited above).
-#pragma unroll
-                    for (int c = 0; c < kDH; c += 16) {
-                        uint32_t o[16];
-                        tmem_ld16(tOi + c, o);
+                    for (int c = 0; c < D; c += 32) {
+                        uint32_t o[32];
+                        tmem_ld32(tOi + c, o);
                         tmem_wait_ld();
 #pragma unroll
-                        for (int e = 0; e < 16; ++e)
+                        for (int e = 0; e < 32; ++e)
                             o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-                        tmem_st16(tOi + c, o);
+                        tmem_st32(tOi + c, o);
                     }
+                    tsum = exps(m_run);
                 }
+                l += tsum;
                 if (tr) trace_ev(p, 2 + i, tn, 23);
                 tmem_wait_st();
                 tc_fence_before();
@@ -518,18 +489,14 @@ fmha_sm100_kernel(const __grid_constant__ FmhaParams p) {
                 if (tr) trace_ev(p, 2 + i, tn, 24);
             }
             // ------------------------------------------------ epilogue
-            // row sum = both halves' partial sums
-            xm[128 * 4 + row] = l;                       // l slots follow the max slots
-            named_bar_sync(pair_bar, 64);
-            const float l_row = l + xm_other[128 * 4 + row];
             mbar_wait(&o_final[i], n_item & 1);
             tc_fence_after();
             const int q = it.qp * 2 * kBM + row_in_pair;
             if (!it.piece) {
-                const float inv_l = 1.f / l_row;
-                uint16_t* dst = p.o + ((int64_t(it.b) * p.Lq + q) * p.H + it.h) * D + hh * kDH;
+                const float inv_l = 1.f / l;
+                uint16_t* dst = p.o + ((int64_t(it.b) * p.Lq + q) * p.H + it.h) * D;
 #pragma unroll
-                for (int c = 0; c < kDH; c += 32) {
+                for (int c = 0; c < D; c += 32) {
                     uint32_t o[32];
                     tmem_ld32(tOi + c, o);
                     tmem_wait_ld();
@@ -553,22 +520,20 @@ fmha_sm100_kernel(const __grid_constant__ FmhaParams p) {
                 float* base = p.part + size_t(it.tail_unit * p.splits + it.split) * kPieceFloats;
                 float4* po = reinterpret_cast<float4*>(base);
 #pragma unroll
-                for (int c = 0; c < kDH; c += 32) {
+                for (int c = 0; c < D; c += 32) {
                     uint32_t o[32];
                     tmem_ld32(tOi + c, o);
                     tmem_wait_ld();
 #pragma unroll
                     for (int e = 0; e < 8; ++e)
-                        po[(((hh * kDH + c) >> 2) + e) * 256 + row_in_pair] =
+                        po[((c >> 2) + e) * 256 + row_in_pair] =
                             make_float4(__uint_as_float(o[4 * e]), __uint_as_float(o[4 * e + 1]),
                                         __uint_as_float(o[4 * e + 2]), __uint_as_float(o[4 * e + 3]));
                 }
                 tc_fence_before();
                 mbar_arrive(&o_empty[i]);
-                if (hh == 0) {
-                    base[256 * D + row_in_pair] = m_run;
-                    base[256 * D + 256 + row_in_pair] = l_row;
-                }
+                base[256 * D + row_in_pair] = m_run;
+                base[256 * D + 256 + row_in_pair] = l;
                 __threadfence();
                 softmax_bar();
                 if (threadIdx.x == 0)
@@ -592,7 +557,7 @@ fmha_sm100_kernel(const __grid_constant__ FmhaParams p) {
                     const float inv = 1.f / wsum;
                     uint16_t* dst = p.o + ((int64_t(it.b) * p.Lq + q) * p.H + it.h) * D;
 #pragma unroll 1
-                    for (int c4 = hh * kDH / 4; c4 < (hh + 1) * kDH / 4; c4 += 2) {
+                    for (int c4 = 0; c4 < D / 4; c4 += 2) {
                         float4 a = make_float4(0.f, 0.f, 0.f, 0.f), bq = a;
                         for (int s = 0; s < p.splits; ++s) {
                             const float* bs = b0 + size_t(s) * kPieceFloats;
@@ -614,7 +579,7 @@ fmha_sm100_kernel(const __grid_constant__ FmhaParams p) {
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == kMmaWarp) {
+    if (warp == 9) {
         tc_fence_after();
         tmem_dealloc(tmem, 512);
     }
@@ -649,8 +614,8 @@ bool make_map(CUtensorMap* m, const void* base, int d, int H, int64_t L, int B) 
 }
 
 template <int D>
-constexpr int smem_bytes() {   // align slack + Q(2) + ring + barriers (512 B) + exchange (4 KB)
-    return 1024 + (2 + kStages) * kBN * D * 2 + 512 + 4096;
+constexpr int smem_bytes() {
+    return 1024 + (2 + kStages) * kBN * D * 2 + 256;
 }
 
 int sm_count() {
