@@ -326,6 +326,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                     for (int i = 0; i < 2; ++i) {
                         if (s_count > 0) mbar_wait(s_free, (s_count - 1) & 1);
                         if (j == 0) mbar_wait(&q_full[i], n_item & 1);
+                        if (lane == 0) trace_ev(p, 1, tn, 15 + i);
                         tc_fence_after();
                         issue_s(i, sk);
                         mma_commit_w(&s_full[i]);
@@ -432,7 +433,10 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                             acc[e & 3] = fadd2(acc[e & 3], pe);
                             pk[e] = pack_bf16x2(pe.x, pe.y);
                         }
-                        if (c == 0) wait_prev_pv();
+                        if (c == 0) {
+                            wait_prev_pv();
+                            if (tr) trace_ev(p, 2 + i, tn, 25);
+                        }
                         tmem_st16(tPi + c * 16, pk);
                     }
                     const float2 s01 = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));

@@ -1,13 +1,16 @@
 #!/usr/bin/env python
-"""Run one WAN-512 chunk attention (t>=2) with TM_TRACE and print CTA 0's
-kernel timeline (debug aid; clock64 cycles).
+"""Run one WAN-512 chunk attention (t>=2) with a TM_TRACE build and print CTA 0's
+kernel timeline (debug aid; clock64 cycles).  Rebuilds libtm.so with
+-DTM_TRACE_ENABLED first (run it last in a GPU session).
 
-Roles: 0 producer (1=K slot acquired, 2=V slot acquired), 1 MMA (10=K full,
-11/12=p_full[i] seen, 13/14=S_i issued+committed), 2/3 softmax tile 0/1
-(20=s_full seen, 21=S loaded, 22=max done, 23=exp done, 24=p_full arrived).
+Events: producer 1/2 = K/V slot acquired; MMA 10 = K_j full, 15/16 = s_free
+(+q_full) seen before S_i, 13/14 = S_i issued, 11/12 = p_full_i seen before
+PV_i; softmax_i 20 = s_full seen, 21 = S loaded (s_free arrived), 22 = max
+decision, 25 = previous PV done (first P store), 23 = exps done, 24 = p_full.
 """
 import os
 import statistics
+import subprocess
 import sys
 
 import numpy as np
@@ -18,8 +21,6 @@ PATH = "/tmp/tm_trace.bin"
 if os.path.exists(PATH):
     os.unlink(PATH)
 os.environ["TM_TRACE"] = PATH
-
-import subprocess  # noqa: E402
 os.environ["TM_TRACE_BUILD"] = "1"
 subprocess.check_call([sys.executable, "-m", "paper_2506_03099_b200.build"], cwd=ROOT,
                       stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
@@ -38,45 +39,30 @@ for t in (1, 2, 3):
     ca.attend(0, 0, t, q, k, v, o)
 torch.cuda.synchronize()
 raw = np.fromfile(PATH, dtype=np.uint64).reshape(-1, 4, 4096)[-1]   # last call
-names = ["producer", "mma", "softmax0", "softmax1"]
-ev = {}
+names = ["prod", "mma", "sm0", "sm1"]
+ev = []
 for r in range(4):
     x = raw[r]
     x = x[x != 0]
-    ev[r] = [(int(v >> 8), int(v & 0xFF)) for v in x]
-t0 = min(e[0][0] for e in ev.values() if e)
-for r in range(4):
-    print(f"== {names[r]}: {len(ev[r])} events")
-    print("   ", " ".join(f"{c}@{t - t0}" for t, c in ev[r][:60]))
+    ev += [(int(v >> 8), names[r], int(v & 0xFF)) for v in x]
+ev.sort()
+t0 = ev[0][0]
+# print a window in the middle of the first item
+mid = [e for e in ev if e[1] == "sm0" and e[2] == 20]
+lo = mid[20][0] if len(mid) > 24 else ev[0][0]
+hi = mid[24][0] if len(mid) > 24 else ev[-1][0]
+print("time(rel)  role  code")
+for t, r, c in ev:
+    if lo <= t <= hi:
+        print(f"{t - lo:8d}  {r:5s} {c}")
+by = {}
+for t, r, c in ev:
+    by.setdefault((r, c), []).append(t)
 
 
-def gaps(r, a, b):
-    """durations from each code-a event to the next code-b event of role r."""
-    out, last = [], None
-    for t, c in ev[r]:
-        if c == a:
-            last = t
-        elif c == b and last is not None:
-            out.append(t - last)
-            last = None
-    return out
+def per(r, c):
+    x = by.get((r, c), [])
+    return statistics.median([b - a for a, b in zip(x, x[1:])]) if len(x) > 2 else float("nan")
 
 
-def period(r, a):
-    ts = [t for t, c in ev[r] if c == a]
-    return [y - x for x, y in zip(ts, ts[1:])]
-
-
-for r in (2, 3):
-    print(f"{names[r]}: period(s_full) median {statistics.median(period(r, 20)):.0f} cycles")
-    for a, b, what in [(20, 21, "ld S"), (21, 22, "max"), (22, 23, "exp+st"), (23, 24, "wait_st+arrive"),
-                       (24, 20, "wait for next S")]:
-        gg = gaps(r, a, b)
-        if gg:
-            print(f"   {what:18s} median {statistics.median(gg):7.0f}  mean {statistics.mean(gg):7.0f}")
-for a, b, what in [(10, 11, "K full -> p_full0"), (11, 13, "PV0+S0 issue"), (13, 12, "-> p_full1"),
-                   (12, 14, "PV1+S1 issue")]:
-    gg = gaps(1, a, b)
-    if gg:
-        print(f"mma {what:20s} median {statistics.median(gg):7.0f}")
-print("mma period(K full)", statistics.median(period(1, 10)))
+print("period sm0 s_full", per("sm0", 20), " sm1", per("sm1", 20), " mma K", per("mma", 10))
