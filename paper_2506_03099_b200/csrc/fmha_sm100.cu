@@ -55,7 +55,7 @@ namespace {
 
 constexpr int kBM = 128;          // query rows per Q tile
 constexpr int kBN = 128;          // keys per KV tile
-constexpr int kStages = 4;        // K/V smem ring slots
+constexpr int kStages = 5;        // K/V smem ring slots (Q 64 KB + 5 x 32 KB fits in 227 KB)
 constexpr int kThreads = 384;     // 2 softmax warpgroups + {TMA, MMA, 2 spare} warpgroup
 constexpr int kRegsSoftmax = 208; // setmaxnreg budgets (see the static_assert)
 constexpr int kRegsOther = 88;
@@ -270,10 +270,18 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                         tma_load_4d(sQ + i * kTileBytes + hf * kHalfBytes, &p.tq, &q_full[i],
                                     hf * 64, it.h, it.qp * 2 * kBM + i * kBM, it.b);
                 }
-                for (int j = it.lo; j < it.hi; ++j) {
+                // Load order K_lo, K_lo+1, V_lo, K_lo+2, V_lo+1, ..., V_hi-1: K runs one
+                // tile ahead of V, matching the MMA's use (S(j+1) before PV(j)).
+                const int nkv = it.hi - it.lo;
+                for (int q = 0; q < 2 * nkv; ++q, ++kv_it) {
+                    int jj, kv;
+                    if (q == 0) { jj = 0; kv = 0; }
+                    else if (q == 2 * nkv - 1) { jj = nkv - 1; kv = 1; }
+                    else if (q & 1) { jj = (q + 1) / 2; kv = 0; }
+                    else { jj = q / 2 - 1; kv = 1; }
                     int seg, row, valid;
-                    tile_info(p, j, seg, row, valid);
-                    for (int kv = 0; kv < 2; ++kv, ++kv_it) {
+                    tile_info(p, it.lo + jj, seg, row, valid);
+                    {
                         const int s = kv_it % kStages;
                         mbar_wait(&kv_empty[s], ((kv_it / kStages) & 1) ^ 1);
                         trace_ev(p, 0, tn, 1 + kv);
@@ -318,9 +326,14 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
             Item it;
             for (int w = blockIdx.x; get_item(p, w, it); w += gridDim.x, ++n_item) {
                 const int nkv = it.hi - it.lo;
+                // ring positions (see the producer's load order)
+                auto kpos = [&](int j) -> uint32_t { return kv_it + (j == 0 ? 0 : 2 * j - 1); };
+                auto vpos = [&](int j) -> uint32_t {
+                    return kv_it + (j == nkv - 1 ? 2 * nkv - 1 : 2 * j + 2);
+                };
                 for (int j = 0; j < nkv; ++j) {
-                    const uint32_t ik = kv_it + 2 * j, sk = ik % kStages;
-                    const uint32_t iv = kv_it + 2 * (j - 1) + 1, sv = iv % kStages;
+                    const uint32_t ik = kpos(j), sk = ik % kStages;
+                    const uint32_t iv = vpos(j - 1), sv = iv % kStages;
                     mbar_wait(&kv_full[sk], (ik / kStages) & 1);
                     if (lane == 0) trace_ev(p, 1, tn, 10);
                     for (int i = 0; i < 2; ++i) {
@@ -346,7 +359,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                     mma_commit_w(&kv_empty[sk]);
                     if (j > 0) mma_commit_w(&kv_empty[sv]);
                 }
-                const uint32_t iv = kv_it + 2 * (nkv - 1) + 1, sv = iv % kStages;
+                const uint32_t iv = vpos(nkv - 1), sv = iv % kStages;
                 mbar_wait(&kv_full[sv], (iv / kStages) & 1);
                 for (int i = 0; i < 2; ++i) {
                     mbar_wait(&p_full[i], (g + nkv - 1) & 1);
