@@ -21,8 +21,10 @@
 //   warp 9      tcgen05 MMA issuer (one thread) + TMEM owner:
 //                 S_i = Q_i K_j^T  (SS, M=128 N=128 K=d, fp32 in TMEM)
 //                 O_i += P_i V_j   (TS: P_i bf16 read from TMEM, V MN-major)
-//               issue order PV0_{j-1}, S0_j, PV1_{j-1}, S1_j: the tensor core
-//               works on one tile while the other tile's softmax runs.
+//               issue order S0_j, PV0_{j-1}, S1_j, PV1_{j-1} into ONE shared S
+//               buffer and separate P_i columns, so S_i(j) is computed while
+//               softmax_i is still on tile j-1 (the softmax never waits for
+//               its own PV + S round trip).
 //   warps 0-7   softmax, one warpgroup per Q tile, one thread per query row
 //               (tcgen05.ld 32x32b puts a whole S row in one thread's
 //               registers): 3-input-max tree, exp2 with scale*log2(e) folded
@@ -33,7 +35,7 @@
 //               by > 8 in log2 units -- exact after the final 1/l), P rounded
 //               to bf16 (RNE) and stored back into TMEM over S_i; epilogue
 //               O/l -> bf16 (or the unnormalised partial for split pieces).
-// TMEM: S0 [0,128) S1 [128,256) O0 [256,256+d) O1 [256+d, 256+2d).
+// TMEM: S [0,128) (shared), P0 [128,192) P1 [192,256), O0 [256,256+d) O1 [256+d,256+2d).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -61,6 +63,8 @@ constexpr int kRegsOther = 88;
 // only redistributes that pool, so the budgets must fit in 384 x 168.
 static_assert(256 * kRegsSoftmax + 128 * kRegsOther <= kThreads * 168, "register pool");
 constexpr int kHalfBytes = 128 * 128;   // one 64-column (128 B) half of a 128-row tile
+// TMEM columns: one S buffer shared by both Q tiles, P0/P1 (bf16 pairs), O0/O1.
+constexpr uint32_t kColS = 0, kColP = 128, kColO = 256;
 
 struct __align__(64) FmhaParams {
     CUtensorMap tq;                   // Q [B][Lq][H][d]
@@ -192,16 +196,6 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
 __device__ __forceinline__ void softmax_bar() {   // the 256 softmax threads only
     asm volatile("bar.sync 1, 256;" ::: "memory");
 }
-// Ping-pong of the two softmax warpgroups' exp phases (named barriers 2, 3):
-// warpgroup i syncs on barrier 2+i before its exps and arrives on 2+(i^1)
-// after them, so the MUFU/FMA pipes serve one tile at a time while the tensor
-// core works on the other.
-__device__ __forceinline__ void turn_wait(int i) {
-    asm volatile("bar.sync %0, 256;" ::"r"(2 + i) : "memory");
-}
-__device__ __forceinline__ void turn_pass(int i) {
-    asm volatile("bar.arrive %0, 256;" ::"r"(2 + (i ^ 1)) : "memory");
-}
 
 template <int D, uint32_t kPolyMask>
 __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_constant__ FmhaParams p) {
@@ -218,11 +212,13 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
     uint64_t* q_empty = q_full + 2;          // [2]
     uint64_t* kv_full = q_empty + 2;         // [kStages]
     uint64_t* kv_empty = kv_full + kStages;  // [kStages]
-    uint64_t* s_full = kv_empty + kStages;   // [2]
-    uint64_t* p_full = s_full + 2;           // [2]
-    uint64_t* o_final = p_full + 2;          // [2]
-    uint64_t* o_empty = o_final + 2;         // [2]
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(o_empty + 2);
+    uint64_t* s_full = kv_empty + kStages;   // [2]  S_i computed into the S buffer
+    uint64_t* p_full = s_full + 2;           // [2]  P_i stored into TMEM
+    uint64_t* o_final = p_full + 2;          // [2]  last PV_i of an item complete
+    uint64_t* o_empty = o_final + 2;         // [2]  epilogue done reading O_i
+    uint64_t* o_done = o_empty + 2;          // [2]  each PV_i complete (P_i reusable)
+    uint64_t* s_free = o_done + 2;           // [1]  S buffer loaded into registers
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(s_free + 1);
     int* merge_flag = reinterpret_cast<int*>(tmem_holder + 1);
 
     const int warp = threadIdx.x >> 5;
@@ -236,7 +232,9 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
             mbar_init(&p_full[i], 128);
             mbar_init(&o_final[i], 1);
             mbar_init(&o_empty[i], 128);
+            mbar_init(&o_done[i], 1);
         }
+        mbar_init(s_free, 128);
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&kv_full[s], 1);
             mbar_init(&kv_empty[s], 1);
@@ -272,10 +270,18 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                         tma_load_4d(sQ + i * kTileBytes + hf * kHalfBytes, &p.tq, &q_full[i],
                                     hf * 64, it.h, it.qp * 2 * kBM + i * kBM, it.b);
                 }
-                for (int j = it.lo; j < it.hi; ++j) {
+                // Load order K_lo, K_lo+1, V_lo, K_lo+2, V_lo+1, ..., V_hi-1: K runs one
+                // tile ahead of V, matching the MMA's use (S(j+1) before PV(j)).
+                const int nkv = it.hi - it.lo;
+                for (int q = 0; q < 2 * nkv; ++q, ++kv_it) {
+                    int jj, kv;
+                    if (q == 0) { jj = 0; kv = 0; }
+                    else if (q == 2 * nkv - 1) { jj = nkv - 1; kv = 1; }
+                    else if (q & 1) { jj = (q + 1) / 2; kv = 0; }
+                    else { jj = q / 2 - 1; kv = 1; }
                     int seg, row, valid;
-                    tile_info(p, j, seg, row, valid);
-                    for (int kv = 0; kv < 2; ++kv, ++kv_it) {
+                    tile_info(p, it.lo + jj, seg, row, valid);
+                    {
                         const int s = kv_it % kStages;
                         mbar_wait(&kv_empty[s], ((kv_it / kStages) & 1) ^ 1);
                         trace_ev(p, 0, tn, 1 + kv);
@@ -296,66 +302,71 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
             const uint64_t dk = make_sdesc_sw128(smem_u32(sKV), 16, 1024);
             const uint64_t dv = make_sdesc_sw128(smem_u32(sKV), kHalfBytes, 1024);
             constexpr uint32_t kTile16 = kTileBytes >> 4;      // descriptor address units
-            auto issue_s = [&](int i, int slot) {
+            auto issue_s = [&](int i, int slot) {      // S = Q_i K^T into the S buffer
                 const uint64_t a0 = dq + i * kTile16, b0 = dk + slot * kTile16;
 #pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk) {
                     const uint32_t off = (kk >> 2) * (kHalfBytes >> 4) + (kk & 3) * 2;
-                    mma_ss_w(tmem + i * 128, a0 + off, b0 + off, kIdescS, kk > 0);
+                    mma_ss_w(tmem + kColS, a0 + off, b0 + off, kIdescS, kk > 0);
                 }
             };
-            auto issue_pv = [&](int i, int slot, bool acc) {
+            auto issue_pv = [&](int i, int slot, bool acc) {   // O_i += P_i V
                 const uint64_t b0 = dv + slot * kTile16;
 #pragma unroll
                 for (int kk = 0; kk < kBN / 16; ++kk)
-                    mma_ts_w(tmem + 256 + i * D, tmem + i * 128 + kk * 8, b0 + kk * 128, kIdescO,
-                           (acc || kk > 0) ? 1u : 0u);
+                    mma_ts_w(tmem + kColO + i * D, tmem + kColP + i * 64 + kk * 8, b0 + kk * 128,
+                             kIdescO, (acc || kk > 0) ? 1u : 0u);
             };
-            uint32_t kv_it = 0, g = 0, n_item = 0;
+            // Issue order per KV tile j: S0(j), PV0(j-1), S1(j), PV1(j-1).  P_i has
+            // its own TMEM columns, so S_i(j) is computed while softmax_i still
+            // works on tile j-1; the single S buffer is refilled as soon as the
+            // previous S has been loaded into registers (s_free).
+            uint32_t kv_it = 0, g = 0, n_item = 0, s_count = 0;
             int tn = 0;
             Item it;
             for (int w = blockIdx.x; get_item(p, w, it); w += gridDim.x, ++n_item) {
                 const int nkv = it.hi - it.lo;
+                // ring positions (see the producer's load order)
+                auto kpos = [&](int j) -> uint32_t { return kv_it + (j == 0 ? 0 : 2 * j - 1); };
+                auto vpos = [&](int j) -> uint32_t {
+                    return kv_it + (j == nkv - 1 ? 2 * nkv - 1 : 2 * j + 2);
+                };
                 for (int j = 0; j < nkv; ++j) {
-                    const uint32_t ik = kv_it + 2 * j, sk = ik % kStages;
+                    const uint32_t ik = kpos(j), sk = ik % kStages;
+                    const uint32_t iv = vpos(j - 1), sv = iv % kStages;
                     mbar_wait(&kv_full[sk], (ik / kStages) & 1);
                     if (lane == 0) trace_ev(p, 1, tn, 10);
-                    tc_fence_after();
-                    uint32_t sv = 0;
-                    if (j > 0) {
-                        const uint32_t iv = kv_it + 2 * (j - 1) + 1;
-                        sv = iv % kStages;
-                        mbar_wait(&kv_full[sv], (iv / kStages) & 1);
-                        tc_fence_after();
-                    }
                     for (int i = 0; i < 2; ++i) {
+                        if (s_count > 0) mbar_wait(s_free, (s_count - 1) & 1);
+                        if (j == 0) mbar_wait(&q_full[i], n_item & 1);
+                        if (lane == 0) trace_ev(p, 1, tn, 15 + i);
+                        tc_fence_after();
+                        issue_s(i, sk);
+                        mma_commit_w(&s_full[i]);
+                        ++s_count;
+                        if (lane == 0) trace_ev(p, 1, tn, 13 + i);
+                        if (j == nkv - 1) mma_commit_w(&q_empty[i]);
                         if (j > 0) {
+                            if (i == 0) mbar_wait(&kv_full[sv], (iv / kStages) & 1);
                             mbar_wait(&p_full[i], (g + j - 1) & 1);
                             if (j == 1 && n_item > 0) mbar_wait(&o_empty[i], (n_item - 1) & 1);
                             if (lane == 0) trace_ev(p, 1, tn, 11 + i);
                             tc_fence_after();
                             issue_pv(i, sv, j - 1 > 0);
+                            mma_commit_w(&o_done[i]);
                         }
-                        if (j == 0) {
-                            mbar_wait(&q_full[i], n_item & 1);
-                            tc_fence_after();
-                        }
-                        issue_s(i, sk);
-                        mma_commit_w(&s_full[i]);
-                        if (lane == 0) trace_ev(p, 1, tn, 13 + i);
-                        if (j == nkv - 1) mma_commit_w(&q_empty[i]);
                     }
                     mma_commit_w(&kv_empty[sk]);
                     if (j > 0) mma_commit_w(&kv_empty[sv]);
                 }
-                const uint32_t iv = kv_it + 2 * (nkv - 1) + 1, sv = iv % kStages;
+                const uint32_t iv = vpos(nkv - 1), sv = iv % kStages;
                 mbar_wait(&kv_full[sv], (iv / kStages) & 1);
-                tc_fence_after();
                 for (int i = 0; i < 2; ++i) {
                     mbar_wait(&p_full[i], (g + nkv - 1) & 1);
                     if (nkv == 1 && n_item > 0) mbar_wait(&o_empty[i], (n_item - 1) & 1);
                     tc_fence_after();
                     issue_pv(i, sv, nkv - 1 > 0);
+                    mma_commit_w(&o_done[i]);
                     mma_commit_w(&o_final[i]);
                 }
                 mma_commit_w(&kv_empty[sv]);
@@ -370,13 +381,13 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
         const int i = warp >> 2, wq = warp & 3;
         const int row_in_pair = i * kBM + wq * 32 + lane;       // 0..255
         const uint32_t lane_off = uint32_t(wq * 32) << 16;
-        const uint32_t tSi = tmem + lane_off + i * 128;
-        const uint32_t tOi = tmem + lane_off + 256 + i * D;
+        const uint32_t tS = tmem + lane_off + kColS;
+        const uint32_t tPi = tmem + lane_off + kColP + i * 64;
+        const uint32_t tOi = tmem + lane_off + kColO + i * D;
         const float sl2 = p.scale_log2;
         uint32_t g = 0, n_item = 0;
         int tn = 0;
         const bool tr = (wq == 0 && lane == 0);
-        if (i == 1) turn_pass(1);     // warpgroup 0 takes the first turn
         Item it;
         for (int w = blockIdx.x; get_item(p, w, it); w += gridDim.x, ++n_item) {
             float m_run = -INFINITY, l = 0.f;
@@ -388,17 +399,30 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                 if (tr) trace_ev(p, 2 + i, tn, 20);
                 tc_fence_after();
 #pragma unroll
-                for (int c = 0; c < kBN; c += 32) tmem_ld32(tSi + c, r + c);
+                for (int c = 0; c < kBN; c += 32) tmem_ld32(tS + c, r + c);
                 tmem_wait_ld();
+                tc_fence_before();
+                mbar_arrive(s_free);          // the S buffer may be refilled
                 if (tr) trace_ev(p, 2 + i, tn, 21);
                 if (valid < kBN) {
 #pragma unroll
                     for (int c = 0; c < kBN; ++c)
                         if (c >= valid) r[c] = 0xff800000u;   // -inf: key beyond the segment
                 }
-                // exps of the row against the running max m_run: P -> TMEM (bf16
-                // over S_i), returns the row sum of this tile.  7 of every 16
-                // pairs use the FMA-pipe polynomial, interleaved with MUFU.
+                // exps of the row against the running max m_run: P -> TMEM (bf16,
+                // P_i columns), returns the row sum of this tile.  kPolyMask pairs
+                // of every 16 use the FMA-pipe polynomial, interleaved with MUFU.
+                // Before the first store into P_i, the previous PV_i (which reads
+                // P_i) must be complete: waited on o_done only then, so the wait
+                // overlaps the first chunk's exps.
+                bool pv_waited = (g == 0);
+                auto wait_prev_pv = [&]() {
+                    if (!pv_waited) {
+                        mbar_wait(&o_done[i], (g - 1) & 1);
+                        tc_fence_after();
+                        pv_waited = true;
+                    }
+                };
                 auto exps = [&](float mrun) -> float {
                     const float nm = (mrun == -INFINITY) ? 0.f : -mrun;
                     const float2 sc2 = make_float2(sl2, sl2), nm2 = make_float2(nm, nm);
@@ -422,7 +446,11 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                             acc[e & 3] = fadd2(acc[e & 3], pe);
                             pk[e] = pack_bf16x2(pe.x, pe.y);
                         }
-                        tmem_st16(tSi + c * 16, pk);
+                        if (c == 0) {
+                            wait_prev_pv();
+                            if (tr) trace_ev(p, 2 + i, tn, 25);
+                        }
+                        tmem_st16(tPi + c * 16, pk);
                     }
                     const float2 s01 = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
                     return s01.x + s01.y;
@@ -448,7 +476,6 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                 // (exact max, O rescale, recompute) when some weight would
                 // exceed ~2^24 -- the result is exact either way after O / l.
                 if (j == it.lo) m_run = row_max() * sl2;
-                turn_wait(i);
                 if (tr) trace_ev(p, 2 + i, tn, 22);
                 float tsum = exps(m_run);
                 const bool bad = !(tsum <= 16777216.f);      // also catches inf / nan
@@ -457,7 +484,8 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                     const float alpha = ex2(m_run - m_new);
                     m_run = m_new;
                     l *= alpha;
-                    // O_i was last written by PV_i_{j-1}, complete before s_full fired.
+                    // O_i was last written by PV_i(j-1): complete (o_done waited).
+                    wait_prev_pv();
 #pragma unroll
                     for (int c = 0; c < D; c += 32) {
                         uint32_t o[32];
@@ -472,7 +500,6 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                 }
                 l += tsum;
                 if (tr) trace_ev(p, 2 + i, tn, 23);
-                turn_pass(i);
                 tmem_wait_st();
                 tc_fence_before();
                 mbar_arrive(&p_full[i]);
@@ -566,7 +593,6 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                 }
             }
         }
-        if (i == 0) turn_wait(0);     // consume warpgroup 1's last hand-over
     }
     tc_fence_before();
     __syncthreads();
