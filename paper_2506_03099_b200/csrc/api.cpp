@@ -379,16 +379,23 @@ tm_status tm_chunk_attention(tm_ctx* ctx, int32_t layer, int32_t step, int64_t c
     void* vslot = ctx->vslot(layer, step, chunk);
     const void* qattn = q;
     void* oattn = o;
+    bool fused_append = false;
     if (Ly.P == 1) {
-        // a3: append c_t's K/V into slot chunk&1 (skipped when the caller wrote them there).
-        const size_t bytes = size_t(cf.batch) * Ly.Lc * Ly.Hl * cf.head_dim * Ly.esize;
-        if (k != kslot) {
-            st = cuda_check(cudaMemcpyAsync(kslot, k, bytes, cudaMemcpyDeviceToDevice, cs), "K append");
-            if (st) return st;
-        }
-        if (v != vslot) {
-            st = cuda_check(cudaMemcpyAsync(vslot, v, bytes, cudaMemcpyDeviceToDevice, cs), "V append");
-            if (st) return st;
+        // a3: append c_t's K/V into slot chunk&1 (skipped when the caller wrote them
+        // there).  bf16: fused into the attention kernel (TMA store of the tiles it
+        // loads); fp32 validation path: a device copy.
+        if (cf.dtype == TM_BF16 && k != kslot && v != vslot) {
+            fused_append = true;
+        } else {
+            const size_t bytes = size_t(cf.batch) * Ly.Lc * Ly.Hl * cf.head_dim * Ly.esize;
+            if (k != kslot) {
+                st = cuda_check(cudaMemcpyAsync(kslot, k, bytes, cudaMemcpyDeviceToDevice, cs), "K append");
+                if (st) return st;
+            }
+            if (v != vslot) {
+                st = cuda_check(cudaMemcpyAsync(vslot, v, bytes, cudaMemcpyDeviceToDevice, cs), "V append");
+                if (st) return st;
+            }
         }
     } else {
         // a2: seq -> head all-to-all; K/V land in the cache slot (a3), Q in workspace.
@@ -415,7 +422,13 @@ tm_status tm_chunk_attention(tm_ctx* ctx, int32_t layer, int32_t step, int64_t c
     if (chunk >= 2)
         pr.seg[pr.nseg++] = Segment{ctx->kslot(layer, step, chunk - 1),
                                     ctx->vslot(layer, step, chunk - 1), Ly.Lc};
-    pr.seg[pr.nseg++] = Segment{kslot, vslot, Ly.Lc};
+    if (fused_append) {
+        pr.seg[pr.nseg++] = Segment{k, v, Ly.Lc};     // read c_t from the caller's buffers
+        pr.store_k = kslot;                            // and append it to the cache slot
+        pr.store_v = vslot;
+    } else {
+        pr.seg[pr.nseg++] = Segment{kslot, vslot, Ly.Lc};
+    }
 
     if (ctx->trace) cudaMemsetAsync(ctx->trace, 0, 4 * 4096 * 8, cs);
     cudaError_t e = cf.dtype == TM_BF16 ? launch_fmha_sm100(pr, ctx->scratch(), cs, &ctx->launches, ctx->trace)

@@ -70,6 +70,8 @@ struct __align__(64) FmhaParams {
     CUtensorMap tq;                   // Q [B][Lq][H][d]
     CUtensorMap tk[kMaxSegments];     // K segments [B][len][H][d]
     CUtensorMap tv[kMaxSegments];     // V segments
+    CUtensorMap tk_store, tv_store;   // a3: cache slot that the current segment is copied to
+    int store_seg;                    // segment whose tiles are appended to the slot (-1: none)
     int seg_tile_start[kMaxSegments + 1];
     int seg_len[kMaxSegments];
     int nseg;
@@ -139,6 +141,21 @@ __device__ __forceinline__ void tile_info(const FmhaParams& p, int j, int& seg, 
         if (s < p.nseg && j >= p.seg_tile_start[s]) seg = s;
     row = (j - p.seg_tile_start[seg]) * kBN;
     valid = min(kBN, p.seg_len[seg] - row);
+}
+
+// Position q (0..2n-1) of an item's K/V load sequence K0, K1, V0, K2, V1, ...,
+// V_{n-1} (K one tile ahead of V) -> (tile offset jj, is_v).
+__device__ __forceinline__ void load_order(int q, int nkv, int& jj, int& kv) {
+    if (q == 0) { jj = 0; kv = 0; }
+    else if (q == 2 * nkv - 1) { jj = nkv - 1; kv = 1; }
+    else if (q & 1) { jj = (q + 1) / 2; kv = 0; }
+    else { jj = q / 2 - 1; kv = 1; }
+}
+// a3 fused append: tile `row / kBN` of the current segment is written to the
+// cache slot by exactly one item of its (b, h): the unit with qp == tile % n_qpairs
+// (or the piece of that unit whose KV range holds it).
+__device__ __forceinline__ bool stores_tile(const FmhaParams& p, const Item& it, int seg, int row) {
+    return seg == p.store_seg && (row / kBN) % p.n_qpairs == it.qp;
 }
 
 __device__ __forceinline__ float max3(float a, float b, float c) {
@@ -218,7 +235,8 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
     uint64_t* o_empty = o_final + 2;         // [2]  epilogue done reading O_i
     uint64_t* o_done = o_empty + 2;          // [2]  each PV_i complete (P_i reusable)
     uint64_t* s_free = o_done + 2;           // [1]  S buffer loaded into registers
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(s_free + 1);
+    uint64_t* store_done = s_free + 1;       // [kStages] append-store finished reading a slot
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(store_done + kStages);
     int* merge_flag = reinterpret_cast<int*>(tmem_holder + 1);
 
     const int warp = threadIdx.x >> 5;
@@ -238,6 +256,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&kv_full[s], 1);
             mbar_init(&kv_empty[s], 1);
+            mbar_init(&store_done[s], 1);
         }
         fence_mbar_init();
     }
@@ -261,6 +280,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
         if (lane == 0) {
             int tn = 0;
             uint32_t kv_it = 0, n_item = 0;
+            uint32_t pending_store = 0, store_cnt = 0;   // per slot: bit / 2-bit counters
             Item it;
             for (int w = blockIdx.x; get_item(p, w, it); w += gridDim.x, ++n_item) {
                 for (int i = 0; i < 2; ++i) {
@@ -275,22 +295,49 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                 const int nkv = it.hi - it.lo;
                 for (int q = 0; q < 2 * nkv; ++q, ++kv_it) {
                     int jj, kv;
-                    if (q == 0) { jj = 0; kv = 0; }
-                    else if (q == 2 * nkv - 1) { jj = nkv - 1; kv = 1; }
-                    else if (q & 1) { jj = (q + 1) / 2; kv = 0; }
-                    else { jj = q / 2 - 1; kv = 1; }
+                    load_order(q, nkv, jj, kv);
                     int seg, row, valid;
                     tile_info(p, it.lo + jj, seg, row, valid);
-                    {
-                        const int s = kv_it % kStages;
-                        mbar_wait(&kv_empty[s], ((kv_it / kStages) & 1) ^ 1);
-                        trace_ev(p, 0, tn, 1 + kv);
-                        const CUtensorMap* m = kv ? &p.tv[seg] : &p.tk[seg];
-                        mbar_arrive_expect_tx(&kv_full[s], kTileBytes);
-                        for (int hf = 0; hf < D / 64; ++hf)
-                            tma_load_4d(sKV + s * kTileBytes + hf * kHalfBytes, m, &kv_full[s],
-                                        hf * 64, it.h, row, it.b);
+                    const int s = kv_it % kStages;
+                    mbar_wait(&kv_empty[s], ((kv_it / kStages) & 1) ^ 1);
+                    if ((pending_store >> s) & 1) {       // previous occupant being appended
+                        mbar_wait(&store_done[s], (store_cnt >> (2 * s)) & 1);
+                        store_cnt += 1u << (2 * s);
+                        pending_store &= ~(1u << s);
                     }
+                    if (stores_tile(p, it, seg, row)) pending_store |= 1u << s;
+                    trace_ev(p, 0, tn, 1 + kv);
+                    const CUtensorMap* m = kv ? &p.tv[seg] : &p.tk[seg];
+                    mbar_arrive_expect_tx(&kv_full[s], kTileBytes);
+                    for (int hf = 0; hf < D / 64; ++hf)
+                        tma_load_4d(sKV + s * kTileBytes + hf * kHalfBytes, m, &kv_full[s],
+                                    hf * 64, it.h, row, it.b);
+                }
+            }
+        }
+      } else if (warp == 10) {
+        // ------------------------------------------------ a3 append: TMA store of c_t tiles
+        if (lane == 0 && p.store_seg >= 0) {
+            uint32_t kv_it = 0;
+            Item it;
+            for (int w = blockIdx.x; get_item(p, w, it); w += gridDim.x) {
+                const int nkv = it.hi - it.lo;
+                for (int q = 0; q < 2 * nkv; ++q, ++kv_it) {
+                    int jj, kv;
+                    load_order(q, nkv, jj, kv);
+                    int seg, row, valid;
+                    tile_info(p, it.lo + jj, seg, row, valid);
+                    if (!stores_tile(p, it, seg, row)) continue;
+                    const int s = kv_it % kStages;
+                    mbar_wait(&kv_full[s], (kv_it / kStages) & 1);
+                    fence_proxy_async_smem();
+                    const CUtensorMap* m = kv ? &p.tv_store : &p.tk_store;
+                    for (int hf = 0; hf < D / 64; ++hf)
+                        tma_store_4d(m, sKV + s * kTileBytes + hf * kHalfBytes, hf * 64, it.h, row,
+                                     it.b);
+                    tma_store_commit();
+                    tma_store_wait_read();
+                    mbar_arrive(&store_done[s]);
                 }
             }
         }
@@ -632,7 +679,7 @@ bool make_map(CUtensorMap* m, const void* base, int d, int H, int64_t L, int B) 
 
 template <int D>
 constexpr int smem_bytes() {
-    return 1024 + (2 + kStages) * kBN * D * 2 + 256;
+    return 1024 + (2 + kStages) * kBN * D * 2 + 512;
 }
 
 int sm_count() {
@@ -701,6 +748,14 @@ cudaError_t launch_fmha_sm100(const AttnProblem& pr, void* scratch, cudaStream_t
         tiles += int((pr.seg[s].len + kBN - 1) / kBN);
     }
     p.seg_tile_start[pr.nseg] = tiles;
+    p.store_seg = -1;
+    if (pr.store_k && pr.store_v) {
+        const Segment& cur = pr.seg[pr.nseg - 1];
+        if (!make_map(&p.tk_store, pr.store_k, pr.d, pr.H, cur.len, pr.B) ||
+            !make_map(&p.tv_store, pr.store_v, pr.d, pr.H, cur.len, pr.B))
+            return cudaErrorInvalidValue;
+        p.store_seg = pr.nseg - 1;
+    }
     p.nseg = pr.nseg;
     p.n_tiles = tiles;
     p.Lq = int(pr.Lq);

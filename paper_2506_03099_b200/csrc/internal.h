@@ -25,6 +25,10 @@ struct AttnProblem {
     int nseg = 0;
     Segment seg[kMaxSegments];
     float scale = 0.f;             // softmax scale (1/sqrt(d), Eq 7)
+    // a3 fused append (sm100 path): if set, the last segment's K/V tiles are also
+    // written to these [B][len][H][d] buffers (the cache slot) by the kernel.
+    void* store_k = nullptr;
+    void* store_v = nullptr;
 };
 
 // Launchers; return cudaSuccess or the launch error.  `launches` is
