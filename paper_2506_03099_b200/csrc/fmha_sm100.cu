@@ -327,9 +327,11 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                     load_order(q, nkv, jj, kv);
                     int seg, row, valid;
                     tile_info(p, it.lo + jj, seg, row, valid);
-                    if (!stores_tile(p, it, seg, row)) continue;
+                    // Observe EVERY position's kv_full phase in order: waiting only on
+                    // stored tiles could run two phases ahead on a slot (parity ABA).
                     const int s = kv_it % kStages;
                     mbar_wait(&kv_full[s], (kv_it / kStages) & 1);
+                    if (!stores_tile(p, it, seg, row)) continue;
                     fence_proxy_async_smem();
                     const CUtensorMap* m = kv ? &p.tv_store : &p.tk_store;
                     for (int hf = 0; hf < D / 64; ++hf)
