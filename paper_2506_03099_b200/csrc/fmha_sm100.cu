@@ -280,7 +280,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
         if (lane == 0) {
             int tn = 0;
             uint32_t kv_it = 0, n_item = 0;
-            uint32_t pending_store = 0, store_cnt = 0;   // per slot: bit / 2-bit counters
+            uint32_t pending_store = 0, store_par = 0;   // per slot: pending bit / phase parity bit
             Item it;
             for (int w = blockIdx.x; get_item(p, w, it); w += gridDim.x, ++n_item) {
                 for (int i = 0; i < 2; ++i) {
@@ -301,8 +301,8 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                     const int s = kv_it % kStages;
                     mbar_wait(&kv_empty[s], ((kv_it / kStages) & 1) ^ 1);
                     if ((pending_store >> s) & 1) {       // previous occupant being appended
-                        mbar_wait(&store_done[s], (store_cnt >> (2 * s)) & 1);
-                        store_cnt += 1u << (2 * s);
+                        mbar_wait(&store_done[s], (store_par >> s) & 1);
+                        store_par ^= 1u << s;
                         pending_store &= ~(1u << s);
                     }
                     if (stores_tile(p, it, seg, row)) pending_store |= 1u << s;
