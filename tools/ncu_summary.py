@@ -88,7 +88,7 @@ def main():
     ap.add_argument("--config", default="wan512")
     ap.add_argument("--n-gpus", type=int, default=1)
     ap.add_argument("--flop", type=float, default=450.97156608e9)
-    ap.add_argument("--algo-bytes", type=float, default=209.7e6)
+    ap.add_argument("--algo-bytes", type=float, default=272.6e6)
     a = ap.parse_args()
     prof = os.path.join(ROOT, "profiles")
     os.makedirs(prof, exist_ok=True)
