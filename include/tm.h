@@ -34,6 +34,11 @@
  *  - Thread-compatible, not thread-safe per ctx.  For P > 1 every call
  *    except tm_flow_euler_step is collective: all ranks call in the same
  *    order.
+ *  - Environment (debug/test only): TM_DEBUG=1 synchronises after each call
+ *    and checks outputs for NaN/Inf (TM_ERR_NONFINITE); TM_FORCE_ULYSSES=1
+ *    makes a world_size == 1 context run the full exchange path (pack, a
+ *    1-rank ncclAlltoAll, unpack) -- read by tm_workspace_bytes and
+ *    tm_attn_init, so set it before both.
  */
 #ifndef TM_H_
 #define TM_H_
@@ -147,6 +152,20 @@ tm_status tm_kvcache_ref_ptr(tm_ctx* ctx, int32_t layer, int32_t step, void** k,
  * 16-byte aligned.  n == 0 is a no-op. */
 tm_status tm_flow_euler_step(tm_ctx* ctx, float* x, const void* v, int32_t v_dtype, int64_t n,
                              float dt, void* stream);
+
+/* Host reference of the Ulysses exchange layouts, the same index map
+ * the device pack/unpack kernels use; for tests of the multi-rank host logic
+ * without GPUs.  Buffers are host memory; rows of head_dim * elem_bytes bytes
+ * (a multiple of 16).  Rank r holds tokens [r*Ls, r*Ls+Ls) of the sequence
+ * (Ls = shard_tokens, tokens >= `tokens` are padding) and heads
+ * [r*Hl, r*Hl+Hl) after the exchange (Hl = heads_per_rank, H = Hl*world_size).
+ *   mode 0: [B][Ls][H][d]     -> [P][B][Ls][Hl][d]   (pack: block p goes to rank p)
+ *   mode 1: [P][B][Ls][Hl][d] -> [B][L][Hl][d]       (unpack received blocks)
+ *   mode 2: [B][L][Hl][d]     -> [P][B][Ls][Hl][d]   (pack outputs; pad rows zero)
+ *   mode 3: [P][B][Ls][Hl][d] -> [B][Ls][H][d]       (unpack to the sequence shard) */
+tm_status tm_ulysses_shuffle_host(int32_t mode, const void* src, void* dst, int32_t batch,
+                                  int64_t shard_tokens, int64_t tokens, int32_t heads_per_rank,
+                                  int32_t world_size, int32_t head_dim, int32_t elem_bytes);
 
 /* Introspection for tests / bench: number of device kernels the last
  * tm_chunk_attention launched on this ctx, and the attention kernel

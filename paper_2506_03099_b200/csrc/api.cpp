@@ -22,6 +22,7 @@
 
 #include "comm.h"
 #include "internal.h"
+#include "ulysses_map.h"
 
 using namespace tmk;
 
@@ -64,7 +65,16 @@ tm_status validate(const tm_config* c) {
     return TM_OK;
 }
 
+// TM_FORCE_ULYSSES=1 (debug/test): a world_size == 1 context runs the full
+// Ulysses exchange path (pack, 1-rank ncclAlltoAll, unpack) so the NCCL
+// integration and the pack/unpack kernels can be checked on one GPU.
+bool force_ulysses() {
+    const char* e = getenv("TM_FORCE_ULYSSES");
+    return e && *e && strcmp(e, "0") != 0;
+}
+
 struct Layout {
+    bool exchange;                   // Ulysses path (P > 1, or forced)
     int esize, Hl, P;
     int64_t Lr, Lc, Lr_s, Lc_s;     // full and per-rank shard token counts
     size_t ref_bytes, slot_bytes, region_bytes, cache_bytes;
@@ -87,7 +97,8 @@ Layout layout_of(const tm_config* c) {
     L.cache_bytes = L.region_bytes * size_t(c->num_layers) * size_t(c->num_steps);
     L.flag_bytes = kAlign;
     L.scratch_bytes = c->dtype == TM_BF16 ? align_up(fmha_sm100_scratch_bytes(c->head_dim)) : 0;
-    if (L.P > 1) {
+    L.exchange = L.P > 1 || force_ulysses();
+    if (L.exchange) {
         const size_t full_row = size_t(c->heads) * c->head_dim * L.esize;
         const size_t qkv = 3 * align_up(size_t(c->batch) * L.Lc_s * full_row);
         const size_t kv = 2 * align_up(size_t(c->batch) * L.Lr_s * full_row);
@@ -236,7 +247,13 @@ tm_status tm_attn_init(const tm_config* cfg, const uint8_t* nccl_id, void* cache
                     L.ws_bytes);
     if (reinterpret_cast<uintptr_t>(workspace) % 256)
         return fail(TM_ERR_INVALID_ARG, "workspace must be 256-byte aligned");
-    if (cfg->world_size > 1 && !nccl_id)
+    uint8_t local_id[128];
+    if (L.exchange && cfg->world_size == 1 && !nccl_id) {   // forced 1-rank exchange
+        const char* e = comm_unique_id(local_id);
+        if (e) return fail(TM_ERR_NCCL, "%s", e);
+        nccl_id = local_id;
+    }
+    if (L.exchange && !nccl_id)
         return fail(TM_ERR_INVALID_ARG, "world_size > 1 needs an NCCL unique id");
     int cur = -1;
     if (cudaGetDevice(&cur) != cudaSuccess) return fail(TM_ERR_CUDA, "no CUDA device");
@@ -266,7 +283,7 @@ tm_status tm_attn_init(const tm_config* cfg, const uint8_t* nccl_id, void* cache
     if (const char* tp = getenv("TM_TRACE")) {
         if (*tp && cudaMalloc(&c->trace, 4 * 4096 * 8) == cudaSuccess) c->trace_path = tp;
     }
-    if (cfg->world_size > 1) {
+    if (L.exchange) {
         const char* e = comm_init(&c->comm, cfg->world_size, cfg->rank, nccl_id);
         if (e) {
             delete c;
@@ -326,7 +343,7 @@ tm_status tm_kvcache_put_reference(tm_ctx* ctx, int32_t layer, int32_t step, con
     cudaStream_t cs = static_cast<cudaStream_t>(stream);
     const Layout& Ly = ctx->lay;
     ctx->launches = 0;
-    if (Ly.P == 1) {
+    if (!Ly.exchange) {
         const size_t bytes = size_t(ctx->cfg.batch) * Ly.Lr * Ly.Hl * ctx->cfg.head_dim * Ly.esize;
         for (int s = s0; s < s1; ++s) {
             st = cuda_check(cudaMemcpyAsync(ctx->kref(layer, s), k, bytes, cudaMemcpyDeviceToDevice, cs),
@@ -380,7 +397,7 @@ tm_status tm_chunk_attention(tm_ctx* ctx, int32_t layer, int32_t step, int64_t c
     const void* qattn = q;
     void* oattn = o;
     bool fused_append = false;
-    if (Ly.P == 1) {
+    if (!Ly.exchange) {
         // a3: append c_t's K/V into slot chunk&1 (skipped when the caller wrote them
         // there).  bf16: fused into the attention kernel (TMA store of the tiles it
         // loads); fp32 validation path: a device copy.
@@ -445,7 +462,7 @@ tm_status tm_chunk_attention(tm_ctx* ctx, int32_t layer, int32_t step, int64_t c
         }
     }
 
-    if (Ly.P > 1) {
+    if (Ly.exchange) {
         // a6: head -> seq all-to-all of O.
         const size_t blk = size_t(cf.batch) * Ly.Lc_s * Ly.Hl * cf.head_dim * Ly.esize;
         st = cuda_check(launch_pack_heads_to_peers(ctx->oh(), ctx->send(), cf.batch, Ly.Lc_s, Ly.Lc,
@@ -461,7 +478,7 @@ tm_status tm_chunk_attention(tm_ctx* ctx, int32_t layer, int32_t step, int64_t c
         if (st) return st;
     }
     ctx->last[li] = chunk;
-    const int64_t n_out = int64_t(cf.batch) * (Ly.P > 1 ? Ly.Lc_s : Ly.Lc) * cf.heads * cf.head_dim;
+    const int64_t n_out = int64_t(cf.batch) * (Ly.exchange ? Ly.Lc_s : Ly.Lc) * cf.heads * cf.head_dim;
     return debug_check(ctx, o, n_out, cf.dtype == TM_BF16, cs, "tm_chunk_attention");
 }
 
@@ -482,6 +499,29 @@ tm_status tm_flow_euler_step(tm_ctx* ctx, float* x, const void* v, int32_t v_dty
                               "euler launch");
     if (st || !ctx) return st;
     return debug_check(ctx, x, n, 0, cs, "tm_flow_euler_step");
+}
+
+tm_status tm_ulysses_shuffle_host(int32_t mode, const void* src, void* dst, int32_t batch,
+                                  int64_t shard_tokens, int64_t tokens, int32_t heads_per_rank,
+                                  int32_t world_size, int32_t head_dim, int32_t elem_bytes) {
+    if (!src || !dst) return fail(TM_ERR_INVALID_ARG, "null buffer");
+    if (mode < 0 || mode > 3) return fail(TM_ERR_INVALID_ARG, "mode %d not in [0, 3]", mode);
+    if (batch <= 0 || shard_tokens <= 0 || tokens <= 0 || heads_per_rank <= 0 || world_size <= 0 ||
+        head_dim <= 0 || elem_bytes <= 0 || (int64_t(head_dim) * elem_bytes) % 16 ||
+        tokens > shard_tokens * world_size)
+        return fail(TM_ERR_SHAPE, "invalid Ulysses shape");
+    UlyssesShape s{batch, world_size, heads_per_rank, head_dim * elem_bytes / 16, shard_tokens, tokens};
+    struct W16 { uint64_t a, b; };
+    const W16* in = static_cast<const W16*>(src);
+    W16* out = static_cast<W16*>(dst);
+    const int64_t total = ulysses_words(s);
+    for (int64_t idx = 0; idx < total; ++idx) {
+        int64_t si, di;
+        ulysses_map(s, mode, idx, si, di);
+        if (di < 0) continue;
+        out[di] = si == -2 ? W16{0, 0} : in[si];
+    }
+    return TM_OK;
 }
 
 int32_t tm_last_launch_count(const tm_ctx* ctx) { return ctx ? ctx->launches : -1; }

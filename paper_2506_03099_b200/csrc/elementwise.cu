@@ -11,6 +11,7 @@
 #include <cstdint>
 
 #include "internal.h"
+#include "ulysses_map.h"
 
 namespace tmk {
 namespace {
@@ -94,51 +95,26 @@ __global__ void nonfinite_kernel(const void* __restrict__ x, int64_t n, int* fla
 }
 
 // ------------------------------------------------------------------ Ulysses
-// Rows are d*esize bytes, moved as 16-byte words (d*esize % 16 == 0).
-// mode 0  pack_seq_to_peers:    src [B][Ls][H][d]        -> dst [P][B][Ls][Hl][d]
-// mode 1  unpack_peers_to_heads: src [P][B][Ls][Hl][d]    -> dst [B][L][Hl][d]  (rows < L)
-// mode 2  pack_heads_to_peers:  src [B][L][Hl][d]         -> dst [P][B][Ls][Hl][d] (pad rows 0)
-// mode 3  unpack_peers_to_seq:  src [P][B][Ls][Hl][d]     -> dst [B][Ls][H][d]
-struct Shuffle {
-    const uint4* src;
-    uint4* dst;
-    int B, P, Hl, W;   // W = 16-byte words per row
-    int64_t Ls, L;
-    int mode;
-};
-
-__global__ void __launch_bounds__(256) ulysses_kernel(const Shuffle s) {
-    // Iterate over the [P][B][Ls][Hl][W] peer-block index space.
-    const int64_t total = int64_t(s.P) * s.B * s.Ls * s.Hl * s.W;
+// Index map in ulysses_map.h (shared with the host routine used by the tests).
+__global__ void __launch_bounds__(256) ulysses_kernel(const uint4* __restrict__ src,
+                                                      uint4* __restrict__ dst, UlyssesShape s,
+                                                      int mode) {
+    const int64_t total = ulysses_words(s);
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
     for (int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < total; idx += stride) {
-        int64_t r = idx;
-        const int w = int(r % s.W); r /= s.W;
-        const int hl = int(r % s.Hl); r /= s.Hl;
-        const int64_t t = r % s.Ls; r /= s.Ls;
-        const int b = int(r % s.B); r /= s.B;
-        const int p = int(r);
-        const int H = s.Hl * s.P;
-        const int64_t blk = idx;                                            // [P][B][Ls][Hl][W]
-        const int64_t seq = ((int64_t(b) * s.Ls + t) * H + p * s.Hl + hl) * s.W + w;   // [B][Ls][H]
-        const int64_t g = p * s.Ls + t;                                     // global token
-        const int64_t head = ((int64_t(b) * s.L + g) * s.Hl + hl) * s.W + w;  // [B][L][Hl]
-        switch (s.mode) {
-            case 0: s.dst[blk] = s.src[seq]; break;
-            case 1: if (g < s.L) s.dst[head] = s.src[blk]; break;
-            case 2: s.dst[blk] = g < s.L ? s.src[head] : make_uint4(0, 0, 0, 0); break;
-            default: s.dst[seq] = s.src[blk]; break;
-        }
+        int64_t si, di;
+        ulysses_map(s, mode, idx, si, di);
+        if (di < 0) continue;
+        dst[di] = si == -2 ? make_uint4(0, 0, 0, 0) : src[si];
     }
 }
 
 cudaError_t launch_shuffle(const void* src, void* dst, int B, int64_t Ls, int64_t L, int Hl, int P,
                            int d, int esize, int mode, cudaStream_t st, int* launches) {
     if ((d * esize) % 16) return cudaErrorInvalidValue;
-    Shuffle s{static_cast<const uint4*>(src), static_cast<uint4*>(dst), B, P, Hl, d * esize / 16,
-              Ls, L, mode};
-    const int64_t total = int64_t(P) * B * Ls * Hl * s.W;
-    ulysses_kernel<<<grid_for(total, 256), 256, 0, st>>>(s);
+    UlyssesShape s{B, P, Hl, d * esize / 16, Ls, L};
+    ulysses_kernel<<<grid_for(ulysses_words(s), 256), 256, 0, st>>>(
+        static_cast<const uint4*>(src), static_cast<uint4*>(dst), s, mode);
     if (launches) ++*launches;
     return cudaGetLastError();
 }

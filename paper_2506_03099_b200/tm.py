@@ -63,6 +63,7 @@ def _load():
         "tm_kvcache_slot_ptr": ([V, i32, i32, i64, P(V), P(V)], i32),
         "tm_kvcache_ref_ptr": ([V, i32, i32, P(V), P(V)], i32),
         "tm_flow_euler_step": ([V, V, V, i32, i64, ctypes.c_float, V], i32),
+        "tm_ulysses_shuffle_host": ([i32, V, V, i32, i64, i64, i32, i32, i32, i32], i32),
         "tm_last_launch_count": ([V], i32),
         "tm_kernel_variant": ([V], ctypes.c_char_p),
     }
@@ -78,7 +79,8 @@ lib = _load()
 EXPORTED = ("tm_version", "tm_last_error", "tm_kvcache_bytes", "tm_workspace_bytes",
             "tm_get_unique_id", "tm_attn_init", "tm_attn_destroy", "tm_stream_reset",
             "tm_kvcache_put_reference", "tm_chunk_attention", "tm_kvcache_slot_ptr",
-            "tm_kvcache_ref_ptr", "tm_flow_euler_step", "tm_last_launch_count",
+            "tm_kvcache_ref_ptr", "tm_flow_euler_step", "tm_ulysses_shuffle_host",
+            "tm_last_launch_count",
             "tm_kernel_variant")
 
 
@@ -163,6 +165,13 @@ def tm_kvcache_ref_ptr(ctx, layer, step):
 
 def tm_flow_euler_step(ctx, x, v, v_dtype, n, dt, stream=None) -> None:
     _check(lib.tm_flow_euler_step(ctx, _ptr(x), _ptr(v), v_dtype, n, dt, _stream(stream)))
+
+
+def tm_ulysses_shuffle_host(mode, src, dst, batch, shard_tokens, tokens, heads_per_rank,
+                            world_size, head_dim, elem_bytes) -> None:
+    """src/dst: contiguous numpy arrays (host memory)."""
+    _check(lib.tm_ulysses_shuffle_host(mode, src.ctypes.data, dst.ctypes.data, batch, shard_tokens,
+                                       tokens, heads_per_rank, world_size, head_dim, elem_bytes))
 
 
 def tm_last_launch_count(ctx) -> int:

@@ -305,3 +305,62 @@ def test_euler_rectified_flow_identity():
         torch.cuda.synchronize()
         target = oracle.interpolate(x0, x1, t + dt)
         assert np.abs(xd.double().cpu().numpy() - target).max() < 1e-5
+
+
+# ------------------------------------------------------------------ batch and exchange path
+
+def test_batch_of_independent_streams():
+    """B = 2 streams in one call ([B][L][H][d]); each equals its own oracle stream."""
+    H, d, Lr, Lc, B = 3, 128, 100, 260, 2
+    ins = [syn.StreamInputs(H, d, Lr, Lc, "bf16", "D0", syn.seed_for(8, 0, extra=b)) for b in range(B)]
+    ca = tm.ChunkAttention(H, d, Lr, Lc, 1, 1, batch=B)
+    sos = [oracle.StreamOracle() for _ in range(B)]
+    refs = [si.chunk(0, 0, 0) for si in ins]
+    kr = torch.stack([to_dev(r[1]) for r in refs])
+    vr = torch.stack([to_dev(r[2]) for r in refs])
+    ca.put_reference(0, 0, kr, vr)
+    for so, r in zip(sos, refs):
+        so.put_reference(0, 0, r[1].f64, r[2].f64)
+    for t in (1, 2, 3):
+        cs = [si.chunk(0, 0, t) for si in ins]
+        q, k, v = (torch.stack([to_dev(c[i]) for c in cs]) for i in range(3))
+        o = torch.empty_like(q)
+        ca.attend(0, 0, t, q, k, v, o)
+        for b in range(B):
+            ref = sos[b].attend(0, 0, t, cs[b][0].f64, cs[b][1].f64, cs[b][2].f64)
+            assert rel_err(from_dev(o[b]), ref) <= BF16_ALARM
+    ca.close()
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+def test_forced_ulysses_path_matches_direct(dtype, monkeypatch):
+    """TM_FORCE_ULYSSES=1 runs the exchange path on one GPU (pack kernel,
+    1-rank ncclAlltoAll, unpack into the cache slot, O back the same way):
+    bitwise equal to the direct path, and within tolerance of the oracle."""
+    H, d, Lr, Lc = 4, 128, 200, 333
+    si = syn.StreamInputs(H, d, Lr, Lc, dtype, "D0", syn.seed_for(9, 1))
+    outs = []
+    for forced in (False, True):
+        if forced:
+            monkeypatch.setenv("TM_FORCE_ULYSSES", "1")
+        ca = tm.ChunkAttention(H, d, Lr, Lc, 1, 1, dtype=DT[dtype])
+        monkeypatch.delenv("TM_FORCE_ULYSSES", raising=False)
+        _, kr, vr = si.chunk(0, 0, 0)
+        ca.put_reference(0, 0, to_dev(kr), to_dev(vr))
+        res = []
+        so = oracle.StreamOracle()
+        so.put_reference(0, 0, kr.f64, vr.f64)
+        for t in (1, 2, 3):
+            q, k, v = si.chunk(0, 0, t)
+            o = torch.empty_like(to_dev(q))
+            ca.attend(0, 0, t, to_dev(q), to_dev(k), to_dev(v), o)
+            torch.cuda.synchronize()
+            ref = so.attend(0, 0, t, q.f64, k.f64, v.f64)
+            assert rel_err(from_dev(o), ref) <= (FP32_TOL if dtype == "fp32" else BF16_ALARM)
+            res.append(o.view(torch.int16 if dtype == "bf16" else torch.int32).cpu().numpy())
+        if forced:
+            assert ca.launches >= 5          # pack x3, attention, pack, unpack (+ unpacks)
+        outs.append(res)
+        ca.close()
+    for a, b in zip(*outs):
+        assert (a == b).all()
