@@ -208,6 +208,8 @@ def main():
     ap.add_argument("--oracle-rows", type=int, default=256)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--stream-chunks", type=int, default=4,
+                    help="BJ.configs[3] streaming measurement over this many chunks (0: off)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -332,35 +334,96 @@ def main():
     # ---------------------------------------------------------------- end to end, host buffers
     e2e = None
     if not args.no_e2e:
+        # Host buffers through the public API, copies inside the timed region,
+        # double-buffered: H2D of step i+1 (copy stream) and D2H of step i-1
+        # overlap the kernels of step i (compute stream).
         hq = [t.cpu().pin_memory() for t in sets[0]]
-        ho = torch.empty(Lc_s, H, d, dtype=bf).pin_memory()
         hx = xlat.cpu().pin_memory()
         hv = vlat.cpu().pin_memory()
-        dq = [torch.empty_like(t) for t in sets[0]]
-        dx, dv = torch.empty_like(xlat), torch.empty_like(vlat)
+        ho = [torch.empty(Lc_s, H, d, dtype=bf).pin_memory() for _ in range(2)]
+        hxo = [torch.empty_like(hx).pin_memory() for _ in range(2)]
+        dq = [[torch.empty_like(t) for t in sets[0]] for _ in range(2)]
+        dx = [torch.empty_like(xlat) for _ in range(2)]
+        dv = [torch.empty_like(vlat) for _ in range(2)]
+        do = [torch.empty(Lc_s, H, d, device="cuda", dtype=bf) for _ in range(2)]
         h2d = sum(t.numel() * t.element_size() for t in hq) + hx.numel() * 4 + hv.numel() * 2
-        d2h = ho.numel() * 2 + hx.numel() * 4
+        d2h = ho[0].numel() * 2 + hx.numel() * 4
+        s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
         ke = max(3, min(args.steps, 10))
+        ev = lambda: torch.cuda.Event(enable_timing=False)
+        in_ready = [None, None]
+        out_done = [None, None]
         barrier()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
+        a.record(s_in)
+        stream.wait_stream(s_in)
+        s_out.wait_stream(s_in)
         for i in range(ke):
+            j = i % 2
+            with torch.cuda.stream(s_in):
+                if out_done[j] is not None:
+                    s_in.wait_event(out_done[j])
+                for dst, src in zip(dq[j], hq):
+                    dst.copy_(src, non_blocking=True)
+                dx[j].copy_(hx, non_blocking=True)
+                dv[j].copy_(hv, non_blocking=True)
+                in_ready[j] = ev()
+                in_ready[j].record(s_in)
+            stream.wait_event(in_ready[j])
             layer = i % NL
             chunk[layer] += 1
-            for dst, src in zip(dq, hq):
-                dst.copy_(src, non_blocking=True)
-            dx.copy_(hx, non_blocking=True)
-            dv.copy_(hv, non_blocking=True)
-            ca.attend(layer, 0, chunk[layer], dq[0], dq[1], dq[2], outs[0], stream)
-            ca.euler(dx, dv, tm.TM_BF16, 0.5, stream)
-            ho.copy_(outs[0], non_blocking=True)
-            hx.copy_(dx, non_blocking=True)
+            ca.attend(layer, 0, chunk[layer], dq[j][0], dq[j][1], dq[j][2], do[j], stream)
+            ca.euler(dx[j], dv[j], tm.TM_BF16, 0.5, stream)
+            done = ev()
+            done.record(stream)
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(done)
+                ho[j].copy_(do[j], non_blocking=True)
+                hxo[j].copy_(dx[j], non_blocking=True)
+                out_done[j] = ev()
+                out_done[j].record(s_out)
+        stream.wait_stream(s_out)
+        stream.wait_stream(s_in)
         b.record(stream)
         barrier()
         e_ms = max_over_ranks(a.elapsed_time(b)) / ke
         e2e = {"value": flop_per_call(c) / (e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
                "ms_per_step": e_ms, "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h)}
+               "d2h_bytes_per_step": int(d2h),
+               "note": "pinned host buffers, copies in the timed region, double-buffered streams"}
+
+    streaming = None
+    if args.stream_chunks >= 2:
+        # BJ.configs[3]: chunk-by-chunk generation in the real dependency order,
+        # every (layer, step) of a WAN-2.1-14B DiT (40 blocks x 2 NFE), the
+        # reference cached once per (layer, step), one Euler update per step.
+        NLs, NS = 40, 2
+        sc = tm.ChunkAttention(H, d, Lr, Lc, num_layers=NLs, num_steps=NS, world_size=P,
+                               rank=rank, device=local, nccl_id=nccl_id)
+        for layer in range(NLs):
+            for st in range(NS):
+                sc.put_reference(layer, st, kref, vref, stream)
+        def one_chunk(t):
+            for st in range(NS):
+                for layer in range(NLs):
+                    q, k, v = sets[(layer + st) % NB]
+                    sc.attend(layer, st, t, q, k, v, outs[layer % NB], stream)
+                sc.euler(xlat, vlat, tm.TM_BF16, 1.0 / NS, stream)
+        one_chunk(1)
+        barrier()
+        sa, sb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        sa.record(stream)
+        for t in range(2, args.stream_chunks + 1):
+            one_chunk(t)
+        sb.record(stream)
+        barrier()
+        s_ms = max_over_ranks(sa.elapsed_time(sb)) / (args.stream_chunks - 1)
+        streaming = {"config": f"BJ.configs[3] shape: {NLs} layers x {NS} steps per chunk, "
+                               f"chunks 2..{args.stream_chunks} timed (steady state, t>=2)",
+                     "ms_per_chunk": s_ms,
+                     "attention_calls_per_chunk": NLs * NS,
+                     "tflops": NLs * NS * flop_per_call(c) / (s_ms * 1e-3) / 1e12}
+        sc.close()
 
     fl = flop_per_call(c)
     ms_step = ms_total / args.steps
@@ -404,6 +467,7 @@ def main():
                          "algorithmic_bytes_per_launch": algo_bytes(c)},
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "streaming": streaming,
             "gpu_launches": gpu_launches,
             "clocks": clk,
         }
