@@ -82,31 +82,37 @@ def measured_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks / throttle reasons, polled every 20 ms around the timed
+    regions; summary(window) keeps the samples taken inside a wall-clock window."""
 
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, device_index):
         self.dev = device_index
         self.proc = None
         self.tmp = None
+        self.rows = []
 
-    def start(self):
+    def start(self, settle=1.5):
+        """Start polling; wait `settle` s so nvidia-smi's NVML start-up (which can
+        stall CUDA launches from this process) is over before timing starts."""
         try:
             self.tmp = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.dev}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=self.tmp, stderr=subprocess.DEVNULL)
+            time.sleep(settle)
         except Exception:
             self.proc = None
 
     def stop(self):
         if not self.proc:
-            return None
-        time.sleep(0.25)
+            return
+        time.sleep(0.1)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
@@ -114,15 +120,30 @@ class ClockSampler:
             self.proc.kill()
         self.tmp.flush()
         self.tmp.seek(0)
-        rows = [r.split(",") for r in self.tmp.read().strip().splitlines() if r.strip()]
+        self.rows = [r.split(",") for r in self.tmp.read().strip().splitlines() if r.strip()]
         os.unlink(self.tmp.name)
+
+    @staticmethod
+    def _ts(r):
+        import datetime
+        try:
+            return datetime.datetime.strptime(r[0].strip(), "%Y/%m/%d %H:%M:%S.%f").timestamp()
+        except Exception:
+            return None
+
+    def summary(self, window=None):
+        rows = self.rows
+        inside = False
+        if window is not None:
+            sel = [r for r in rows if self._ts(r) is not None and window[0] <= self._ts(r) <= window[1]]
+            if sel:
+                rows, inside = sel, True
         sm, smax, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for r in rows:
             try:
                 sm.append(float(r[1]))
                 smax = max(smax, float(r[2]))
-                for nm, val in zip(names, r[5:9]):
+                for nm, val in zip(self.REASONS, r[5:9]):
                     if "Active" in val and "Not" not in val:
                         reasons.add(nm)
             except Exception:
@@ -130,7 +151,7 @@ class ClockSampler:
         if not sm:
             return None
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": smax, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "in_timed_window": inside}
 
 
 # ----------------------------------------------------------------------------- reference arm
@@ -293,14 +314,15 @@ def main():
     clocks.start()
     launches[0] = 0
     barrier()
+    w0 = time.time()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for i in range(args.steps):
         step(i)
     e1.record(stream)
     barrier()
+    w1 = time.time()
     ms_total = max_over_ranks(e0.elapsed_time(e1))
-    clk = clocks.stop()
     gpu_launches = launches[0]
 
     # ---------------------------------------------------------------- attention kernel alone
@@ -313,8 +335,7 @@ def main():
         chunk[layer] += 1
         kp, vp = ca.slot_ptr(layer, 0, chunk[layer])
         ca.attend(layer, 0, chunk[layer], sets[i % NB][0], kp, vp, outs[i % NB], stream)
-    kclk = ClockSampler(local)
-    kclk.start()
+    w2 = time.time()
     for i in range(args.steps):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         layer = i % NL
@@ -326,7 +347,10 @@ def main():
         b.record(stream)
         kev.append((a, b))
     barrier()
-    kclk = kclk.stop()
+    w3 = time.time()
+    clocks.stop()
+    clk = clocks.summary(window=(w0, w1))
+    kclk = clocks.summary(window=(w2, w3))
     k_list = [a.elapsed_time(b) for a, b in kev]
     k_ms = max_over_ranks(statistics.mean(k_list))
     k_med = max_over_ranks(statistics.median(k_list))
