@@ -34,6 +34,13 @@ def call(i):
     ca.attend(l, 0, chunk[l], qs[i % 4], kp, vp, o)
 
 
+# Fill every layer's cache slots with real (random) K/V via the fused append
+# first: timing zero-copy calls on never-written (zero) slots is optimistic.
+ks, vs = mk(Lc), mk(Lc)
+for rnd in range(2):
+    for l in range(NL):
+        chunk[l] += 1
+        ca.attend(l, 0, chunk[l], qs[0], ks, vs, o)
 for i in range(3 * NL):
     call(i)
 torch.cuda.synchronize()
