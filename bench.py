@@ -49,6 +49,9 @@ CONFIGS = {
     "wan512": dict(H=40, d=128, Lr=1024, Lc=3072, latent=16 * 3 * 64 * 64,
                    workload="WAN-2.1-14B-shaped single layer, 512x512 (1024 tok/frame), "
                             "chunk t>=2 = 3 latent frames + cached reference frame + previous chunk"),
+    "wan512c7": dict(H=40, d=128, Lr=1024, Lc=7168, latent=16 * 7 * 64 * 64,
+                     workload="Table 1 variant (P:249-258): WAN-2.1-14B-shaped layer, 512x512, "
+                              "chunk = 7 latent frames + cached reference frame + previous chunk"),
     "wan720": dict(H=40, d=128, Lr=2025, Lc=6075, latent=16 * 3 * 90 * 90,
                    workload="WAN-2.1-14B-shaped single layer, 720x720 (2025 tok/frame), "
                             "chunk t>=2 = 3 latent frames + cached reference frame + previous chunk"),

@@ -100,3 +100,10 @@ def test_init_without_device_reports_cuda_error():
     with pytest.raises(tm.TMError) as e:
         tm.tm_attn_init(wan512(), None, 1024, 1 << 40, 1024, 1 << 30)
     assert e.value.status == 8
+
+
+def test_cache_bytes_table1_variants():
+    """f3: chunk 7 x 4 steps at 512^2: ref + 2 slots per (layer, step)."""
+    c = tm.make_config(40, 128, 1024, 7168, 40, 4)
+    per_tok = 40 * 128 * 2
+    assert tm.tm_kvcache_bytes(c) == 160 * (2 * 1024 * per_tok + 4 * 7168 * per_tok)

@@ -364,3 +364,20 @@ def test_forced_ulysses_path_matches_direct(dtype, monkeypatch):
         ca.close()
     for a, b in zip(*outs):
         assert (a == b).all()
+
+
+# ------------------------------------------------------------------ Table 1 variants
+
+def test_table1_chunk7_bf16_sampled():
+    """f3: chunk = 7 latent frames at 512^2 (Lc = 7168, Lk up to
+    15360 at t >= 2), row-sampled against the oracle."""
+    rows = sample_rows(7168, k=16)
+    err = run_stream(40, 128, 1024, 7168, "bf16", chunks=2, rows=rows)
+    assert err <= BF16_ALARM, err
+
+
+def test_table1_four_steps_cache_slots():
+    """f3: 4 denoising steps -> 4 cache step slots per layer (P:255-257);
+    every (layer, step) keeps its own reference and previous chunk."""
+    err = run_stream(4, 128, 128, 384, "bf16", chunks=3, layers=2, steps=4)
+    assert err <= BF16_ALARM, err
