@@ -137,6 +137,18 @@ tm_status tm_chunk_attention(tm_ctx* ctx, int32_t layer, int32_t step, int64_t c
                              const void* q, const void* k, const void* v, void* o,
                              void* stream);
 
+/* the full-window form (P:130-143 and Eq 7 over a whole
+ * training window, e.g. 21 latent frames = 7 chunks x 3 frames, P:134-136;
+ * the DMD student's teacher-forcing pattern): q, k, v, o are device
+ * [B][L][H][d] over the window [c_0 | c_1 | ... | c_{n-1}] with chunk_len[c]
+ * tokens in chunk c (host array, L = sum); every query of chunk c attends the
+ * keys of chunks {0, c-1, c} as a set (chunk 0 attends itself only).
+ * No cache is read or written; B, H, d, dtype and the scale come from ctx
+ * (world_size must be 1, else TM_ERR_UNSUPPORTED).  An empty chunk returns
+ * TM_ERR_DEGENERATE_MASK.  One kernel launch per chunk. */
+tm_status tm_window_attention(tm_ctx* ctx, const void* q, const void* k, const void* v, void* o,
+                              const int64_t* chunk_len, int32_t n_chunks, void* stream);
+
 /* Device pointers of the cache slot that chunk `chunk` at (layer, step) is
  * stored in ([B][Lc][H/P][d] each).  A caller may write the chunk's K/V
  * there before tm_chunk_attention to skip the append copy. */

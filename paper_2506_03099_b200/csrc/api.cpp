@@ -482,6 +482,58 @@ tm_status tm_chunk_attention(tm_ctx* ctx, int32_t layer, int32_t step, int64_t c
     return debug_check(ctx, o, n_out, cf.dtype == TM_BF16, cs, "tm_chunk_attention");
 }
 
+tm_status tm_window_attention(tm_ctx* ctx, const void* q, const void* k, const void* v, void* o,
+                              const int64_t* chunk_len, int32_t n_chunks, void* stream) {
+    if (!ctx || !q || !k || !v || !o || !chunk_len) return fail(TM_ERR_INVALID_ARG, "null argument");
+    if (ctx->lay.exchange)
+        return fail(TM_ERR_UNSUPPORTED, "tm_window_attention needs a world_size == 1 context");
+    if (n_chunks <= 0) return fail(TM_ERR_SHAPE, "n_chunks = %d <= 0", n_chunks);
+    if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o))
+        return fail(TM_ERR_INVALID_ARG, "q, k, v, o must be 16-byte aligned");
+    std::vector<int64_t> start(n_chunks + 1, 0);
+    for (int c = 0; c < n_chunks; ++c) {
+        if (chunk_len[c] <= 0)
+            return fail(TM_ERR_DEGENERATE_MASK, "chunk %d is empty: its queries have no keys (S:39)", c);
+        start[c + 1] = start[c] + chunk_len[c];
+    }
+    const tm_config& cf = ctx->cfg;
+    const int64_t L = start[n_chunks];
+    const size_t row = size_t(cf.heads) * cf.head_dim * ctx->lay.esize;     // one token
+    const uint8_t* qb = static_cast<const uint8_t*>(q);
+    const uint8_t* kb = static_cast<const uint8_t*>(k);
+    const uint8_t* vb = static_cast<const uint8_t*>(v);
+    uint8_t* ob = static_cast<uint8_t*>(o);
+    cudaStream_t cs = static_cast<cudaStream_t>(stream);
+    ctx->launches = 0;
+    // a4 per query chunk c: key chunks {0, c-1, c} as a set (P:137-143, S:271:
+    // chunk 0 attends itself only), each a token sub-range of the window.
+    for (int c = 0; c < n_chunks; ++c) {
+        AttnProblem pr;
+        pr.q = qb + start[c] * row;
+        pr.o = ob + start[c] * row;
+        pr.Lq = chunk_len[c];
+        pr.q_bstride = L;
+        pr.B = cf.batch;
+        pr.H = cf.heads;
+        pr.d = cf.head_dim;
+        pr.scale = ctx->scale;
+        int kc[3], nk = 0;
+        kc[nk++] = 0;
+        if (c - 1 > 0) kc[nk++] = c - 1;
+        if (c > 0) kc[nk++] = c;
+        for (int i = 0; i < nk; ++i)
+            pr.seg[pr.nseg++] = Segment{kb + start[kc[i]] * row, vb + start[kc[i]] * row,
+                                        chunk_len[kc[i]], L};
+        const cudaError_t e = cf.dtype == TM_BF16
+                                  ? launch_fmha_sm100(pr, ctx->scratch(), cs, &ctx->launches)
+                                  : launch_fmha_fp32(pr, cs, &ctx->launches);
+        tm_status st = cuda_check(e, "window attention launch");
+        if (st) return st;
+    }
+    return debug_check(ctx, o, int64_t(cf.batch) * L * cf.heads * cf.head_dim, cf.dtype == TM_BF16,
+                       cs, "tm_window_attention");
+}
+
 tm_status tm_flow_euler_step(tm_ctx* ctx, float* x, const void* v, int32_t v_dtype, int64_t n,
                              float dt, void* stream) {
     if (n < 0) return fail(TM_ERR_SHAPE, "n = %lld < 0", (long long)n);

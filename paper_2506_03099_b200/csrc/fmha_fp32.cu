@@ -30,8 +30,10 @@ struct Fp32Params {
     const float* k[kMaxSegments];
     const float* v[kMaxSegments];
     int64_t len[kMaxSegments];
+    int64_t bstride[kMaxSegments];   // tokens between batch elements of each segment
     int nseg;
     int64_t Lq;
+    int64_t q_bstride;                // tokens between batch elements of q / o
     int H;
     float scale;
 };
@@ -63,7 +65,7 @@ __global__ void __launch_bounds__(kWarps * 32) fmha_fp32_kernel(const Fp32Params
     for (int idx = threadIdx.x; idx < kRows * D; idx += blockDim.x) {
         const int rr = idx / D, c = idx % D;
         const int64_t q = r0 + rr;
-        sq[rr][c] = q < p.Lq ? p.q[((int64_t(b) * p.Lq + q) * H + h) * D + c] : 0.f;
+        sq[rr][c] = q < p.Lq ? p.q[((int64_t(b) * p.q_bstride + q) * H + h) * D + c] : 0.f;
     }
 
     float m[kRowsPerWarp], l[kRowsPerWarp], acc[kRowsPerWarp][PER];
@@ -77,6 +79,7 @@ __global__ void __launch_bounds__(kWarps * 32) fmha_fp32_kernel(const Fp32Params
 
     for (int s = 0; s < p.nseg; ++s) {
         const int64_t len = p.len[s];
+        const int64_t bst = p.bstride[s];
         const float* K = p.k[s];
         const float* V = p.v[s];
         for (int64_t j0 = 0; j0 < len; j0 += kKeys) {
@@ -85,7 +88,7 @@ __global__ void __launch_bounds__(kWarps * 32) fmha_fp32_kernel(const Fp32Params
                 const int jj = idx / D, c = idx % D;
                 const int64_t j = j0 + jj;
                 const bool ok = j < len;
-                const int64_t g = ((int64_t(b) * len + j) * H + h) * D + c;
+                const int64_t g = ((int64_t(b) * bst + j) * H + h) * D + c;
                 sk[jj][c] = ok ? K[g] : 0.f;
                 sv[jj][c] = ok ? V[g] : 0.f;
             }
@@ -135,7 +138,7 @@ __global__ void __launch_bounds__(kWarps * 32) fmha_fp32_kernel(const Fp32Params
         const int64_t q = r0 + warp * kRowsPerWarp + r;
         if (q >= p.Lq) continue;
         const float inv = 1.f / l[r];
-        float* dst = p.o + ((int64_t(b) * p.Lq + q) * H + h) * D;
+        float* dst = p.o + ((int64_t(b) * p.q_bstride + q) * H + h) * D;
 #pragma unroll
         for (int e = 0; e < PER; ++e) dst[lane + 32 * e] = acc[r][e] * inv;
     }
@@ -152,8 +155,10 @@ cudaError_t launch_fmha_fp32(const AttnProblem& pr, cudaStream_t stream, int* la
         p.k[s] = static_cast<const float*>(pr.seg[s].k);
         p.v[s] = static_cast<const float*>(pr.seg[s].v);
         p.len[s] = pr.seg[s].len;
+        p.bstride[s] = pr.seg[s].bstride > 0 ? pr.seg[s].bstride : pr.seg[s].len;
     }
     p.Lq = pr.Lq;
+    p.q_bstride = pr.q_bstride > 0 ? pr.q_bstride : pr.Lq;
     p.H = pr.H;
     p.scale = pr.scale;
     dim3 grid(unsigned((pr.Lq + kRows - 1) / kRows), pr.H, pr.B);

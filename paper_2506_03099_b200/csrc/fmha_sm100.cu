@@ -77,6 +77,7 @@ struct __align__(64) FmhaParams {
     int nseg;
     int n_tiles;                      // KV tiles of a whole unit
     int Lq, H, B;
+    int64_t o_bstride;                // tokens between batch elements of o
     float scale_log2;                 // softmax scale * log2(e)
     uint16_t* o;                      // bf16 bits [B][Lq][H][d]
     // persistent schedule
@@ -560,7 +561,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
             const int q = it.qp * 2 * kBM + row_in_pair;
             if (!it.piece) {
                 const float inv_l = 1.f / l;
-                uint16_t* dst = p.o + ((int64_t(it.b) * p.Lq + q) * p.H + it.h) * D;
+                uint16_t* dst = p.o + ((int64_t(it.b) * p.o_bstride + q) * p.H + it.h) * D;
 #pragma unroll
                 for (int c = 0; c < D; c += 32) {
                     uint32_t o[32];
@@ -621,7 +622,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                                 __ldcg(bs + 256 * D + 256 + row_in_pair);
                     }
                     const float inv = 1.f / wsum;
-                    uint16_t* dst = p.o + ((int64_t(it.b) * p.Lq + q) * p.H + it.h) * D;
+                    uint16_t* dst = p.o + ((int64_t(it.b) * p.o_bstride + q) * p.H + it.h) * D;
 #pragma unroll 1
                     for (int c4 = 0; c4 < D / 4; c4 += 2) {
                         float4 a = make_float4(0.f, 0.f, 0.f, 0.f), bq = a;
@@ -666,11 +667,13 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 // Token-major bf16 [B][L][H][d]: dims (inner first) {d, H, L, B}; box {64, 1, 128, 1}.
-bool make_map(CUtensorMap* m, const void* base, int d, int H, int64_t L, int B) {
+// `bstride` = tokens between batch elements (>= L; a sub-range of a longer sequence).
+bool make_map(CUtensorMap* m, const void* base, int d, int H, int64_t L, int B, int64_t bstride = 0) {
+    if (bstride <= 0) bstride = L;
     auto fn = encode_fn();
     if (!fn) return false;
     cuuint64_t dims[4] = {cuuint64_t(d), cuuint64_t(H), cuuint64_t(L), cuuint64_t(B)};
-    cuuint64_t strides[3] = {cuuint64_t(d) * 2, cuuint64_t(H) * d * 2, cuuint64_t(L) * H * d * 2};
+    cuuint64_t strides[3] = {cuuint64_t(d) * 2, cuuint64_t(H) * d * 2, cuuint64_t(bstride) * H * d * 2};
     cuuint32_t box[4] = {64, 1, 128, 1};
     cuuint32_t es[4] = {1, 1, 1, 1};
     CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides,
@@ -739,11 +742,11 @@ cudaError_t launch_fmha_sm100(const AttnProblem& pr, void* scratch, cudaStream_t
     if (pr.d != 64 && pr.d != 128) return cudaErrorInvalidValue;
     FmhaParams p;
     memset(&p, 0, sizeof(p));
-    if (!make_map(&p.tq, pr.q, pr.d, pr.H, pr.Lq, pr.B)) return cudaErrorInvalidValue;
+    if (!make_map(&p.tq, pr.q, pr.d, pr.H, pr.Lq, pr.B, pr.q_bstride)) return cudaErrorInvalidValue;
     int tiles = 0;
     for (int s = 0; s < pr.nseg; ++s) {
-        if (!make_map(&p.tk[s], pr.seg[s].k, pr.d, pr.H, pr.seg[s].len, pr.B) ||
-            !make_map(&p.tv[s], pr.seg[s].v, pr.d, pr.H, pr.seg[s].len, pr.B))
+        if (!make_map(&p.tk[s], pr.seg[s].k, pr.d, pr.H, pr.seg[s].len, pr.B, pr.seg[s].bstride) ||
+            !make_map(&p.tv[s], pr.seg[s].v, pr.d, pr.H, pr.seg[s].len, pr.B, pr.seg[s].bstride))
             return cudaErrorInvalidValue;
         p.seg_tile_start[s] = tiles;
         p.seg_len[s] = int(pr.seg[s].len);
@@ -765,6 +768,7 @@ cudaError_t launch_fmha_sm100(const AttnProblem& pr, void* scratch, cudaStream_t
     p.B = pr.B;
     p.scale_log2 = pr.scale * 1.4426950408889634f;
     p.o = static_cast<uint16_t*>(pr.o);
+    p.o_bstride = pr.q_bstride > 0 ? pr.q_bstride : pr.Lq;
     const int qtiles = int((pr.Lq + kBM - 1) / kBM);
     p.n_qpairs = (qtiles + 1) / 2;
     // Persistent schedule: R whole rounds over C CTAs, then the T tail units

@@ -14,6 +14,7 @@ struct Segment {
     const void* k = nullptr;
     const void* v = nullptr;
     int64_t len = 0;               // tokens (0 = absent)
+    int64_t bstride = 0;           // tokens between batch elements (0: = len)
 };
 
 // a4: the segment schedule of one chunk-attention call.
@@ -21,6 +22,7 @@ struct AttnProblem {
     const void* q = nullptr;       // [B][Lq][H][d]
     void* o = nullptr;             // [B][Lq][H][d]
     int64_t Lq = 0;
+    int64_t q_bstride = 0;         // tokens between batch elements of q / o (0: = Lq)
     int B = 1, H = 1, d = 128;     // H = heads resident on this rank
     int nseg = 0;
     Segment seg[kMaxSegments];

@@ -64,6 +64,7 @@ def _load():
         "tm_kvcache_ref_ptr": ([V, i32, i32, P(V), P(V)], i32),
         "tm_flow_euler_step": ([V, V, V, i32, i64, ctypes.c_float, V], i32),
         "tm_ulysses_shuffle_host": ([i32, V, V, i32, i64, i64, i32, i32, i32, i32], i32),
+        "tm_window_attention": ([V, V, V, V, V, P(i64), i32, V], i32),
         "tm_last_launch_count": ([V], i32),
         "tm_kernel_variant": ([V], ctypes.c_char_p),
     }
@@ -80,6 +81,7 @@ EXPORTED = ("tm_version", "tm_last_error", "tm_kvcache_bytes", "tm_workspace_byt
             "tm_get_unique_id", "tm_attn_init", "tm_attn_destroy", "tm_stream_reset",
             "tm_kvcache_put_reference", "tm_chunk_attention", "tm_kvcache_slot_ptr",
             "tm_kvcache_ref_ptr", "tm_flow_euler_step", "tm_ulysses_shuffle_host",
+            "tm_window_attention",
             "tm_last_launch_count",
             "tm_kernel_variant")
 
@@ -167,6 +169,12 @@ def tm_flow_euler_step(ctx, x, v, v_dtype, n, dt, stream=None) -> None:
     _check(lib.tm_flow_euler_step(ctx, _ptr(x), _ptr(v), v_dtype, n, dt, _stream(stream)))
 
 
+def tm_window_attention(ctx, q, k, v, o, chunk_lens, stream=None) -> None:
+    arr = (ctypes.c_int64 * len(chunk_lens))(*[int(x) for x in chunk_lens])
+    _check(lib.tm_window_attention(ctx, _ptr(q), _ptr(k), _ptr(v), _ptr(o), arr, len(chunk_lens),
+                                   _stream(stream)))
+
+
 def tm_ulysses_shuffle_host(mode, src, dst, batch, shard_tokens, tokens, heads_per_rank,
                             world_size, head_dim, elem_bytes) -> None:
     """src/dst: contiguous numpy arrays (host memory)."""
@@ -235,6 +243,10 @@ class ChunkAttention:
 
     def ref_ptr(self, layer, step):
         return tm_kvcache_ref_ptr(self.ctx, layer, step)
+
+    def window(self, q, k, v, o, chunk_lens, stream=None):
+        tm_window_attention(self.ctx, q, k, v, o, chunk_lens, stream)
+        return o
 
     def euler(self, x, v, v_dtype, dt, stream=None):
         tm_flow_euler_step(self.ctx, x, v, v_dtype, x.numel(), dt, stream)

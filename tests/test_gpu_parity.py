@@ -381,3 +381,63 @@ def test_table1_four_steps_cache_slots():
     every (layer, step) keeps its own reference and previous chunk."""
     err = run_stream(4, 128, 128, 384, "bf16", chunks=3, layers=2, steps=4)
     assert err <= BF16_ALARM, err
+
+
+# ------------------------------------------------------------------ SURVEY Sec 8(f) f1: full window
+
+def _window_inputs(H, d, lens, dtype, dist, seed):
+    rng = np.random.default_rng(seed)
+    q, k, v = syn.chunk_qkv(rng, int(sum(lens)), H, d, dtype, dist)
+    return q, k, v
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+@pytest.mark.parametrize("lens", [[16, 32, 32], [130, 1, 257, 128, 5], [64] * 7, [300, 200, 100, 50]])
+def test_window_attention_vs_oracle(dtype, lens):
+    """f1: tm_window_attention (every chunk c attends {0, c-1, c}) vs the
+    oracle's full-window form c1."""
+    H, d = 3, 128
+    q, k, v = _window_inputs(H, d, lens, dtype, "D0", syn.seed_for(10, 0, extra=len(lens)))
+    ca = tm.ChunkAttention(H, d, 16, 16, 1, 1, dtype=DT[dtype])
+    o = torch.empty_like(to_dev(q))
+    ca.window(to_dev(q), to_dev(k), to_dev(v), o, lens)
+    ref = oracle.window_attention(q.f64, k.f64, v.f64, lens)
+    assert ca.launches == len(lens)
+    assert rel_err(from_dev(o), ref) <= (FP32_TOL if dtype == "fp32" else BF16_ALARM)
+    with pytest.raises(tm.TMError) as e:
+        ca.window(to_dev(q), to_dev(k), to_dev(v), o, lens[:-1] + [0, lens[-1]])
+    assert e.value.status == 3                       # empty chunk: degenerate mask (S:39)
+    ca.close()
+
+
+def test_window_wan512_21_frames_sampled():
+    """f1 at WAN scale: the 21-latent-frame window = 7 chunks x 3 frames of
+    1024 tokens, 21504 tokens, 40 heads; row-sampled in every chunk."""
+    H, d, lens = 40, 128, [3072] * 7
+    q, k, v = _window_inputs(H, d, lens, "bf16", "D0", syn.seed_for(10, 1))
+    ca = tm.ChunkAttention(H, d, 16, 16, 1, 1)
+    o = torch.empty_like(to_dev(q))
+    ca.window(to_dev(q), to_dev(k), to_dev(v), o, lens)
+    rows = np.concatenate([c * 3072 + sample_rows(3072, k=3, seed=c) for c in range(7)])
+    ref = oracle.window_attention(q.f64, k.f64, v.f64, lens, rows=rows)
+    assert rel_err(from_dev(o)[rows], ref) <= BF16_ALARM
+    ca.close()
+
+
+def test_window_equals_streaming_bitwise():
+    """S:303 on the GPU: the window form and the cache-streaming form run the
+    same segment schedule, so each chunk's rows agree bit for bit."""
+    H, d, Lr, Lc, n = 4, 128, 200, 384, 5
+    lens = [Lr] + [Lc] * (n - 1)
+    q, k, v = _window_inputs(H, d, lens, "bf16", "D0", syn.seed_for(10, 2))
+    qd, kd, vd = to_dev(q), to_dev(k), to_dev(v)
+    ca = tm.ChunkAttention(H, d, Lr, Lc, 1, 1)
+    ow = torch.empty_like(qd)
+    ca.window(qd, kd, vd, ow, lens)
+    ca.put_reference(0, 0, kd[:Lr].contiguous(), vd[:Lr].contiguous())
+    for t in range(1, n):
+        sl = slice(Lr + (t - 1) * Lc, Lr + t * Lc)
+        os_ = torch.empty_like(qd[sl])
+        ca.attend(0, 0, t, qd[sl].contiguous(), kd[sl].contiguous(), vd[sl].contiguous(), os_)
+        assert torch.equal(os_.view(torch.int16), ow[sl].view(torch.int16)), t
+    ca.close()
