@@ -28,9 +28,9 @@
 //   warps 0-7   softmax, one warpgroup per Q tile, one thread per query row
 //               (tcgen05.ld 32x32b puts a whole S row in one thread's
 //               registers): 3-input-max tree, exp2 with scale*log2(e) folded
-//               into one packed FFMA2, 75% of the exponentials on the MUFU
-//               pipe and 25% as a degree-3 polynomial on the FMA pipe (the
-//               MUFU rate equals the tensor rate at d=128), packed FADD2 row
+//               into one packed FFMA2, exponentials on the MUFU pipe (a
+//               degree-3 polynomial on the FMA pipe for a selectable share,
+//               TM_POLY; off by default: power-capped, see profiles/README.md), packed FADD2 row
 //               sums, conditional O rescale (only when the running max grows
 //               by > 8 in log2 units -- exact after the final 1/l), P rounded
 //               to bf16 (RNE) and stored back into TMEM over S_i; epilogue
@@ -713,16 +713,19 @@ cudaError_t launch_t(const FmhaParams& p, int grid, cudaStream_t stream) {
 }
 
 // Which of every 16 exp2 pairs run as the FMA-pipe polynomial (bit e set) --
-// the MUFU/FMA balance.  Default 4/16 (fastest in the TM_POLY sweep).
-constexpr uint32_t kPolyDefault = 0x4444u;   // e in {2,6,10,14} (sweep: fastest)
+// the MUFU/FMA balance.  Default: all MUFU -- with real data the kernel is
+// power-capped and the polynomial's extra FMA-pipe work costs more energy than
+// the MUFU time it saves (sweep on random data: 1282 vs 1271 TFLOP/s at 512^2,
+// 1187 vs 1147 at 720^2; on zero data 4/16 was ahead).
+constexpr uint32_t kPolyDefault = 0x0000u;
 template <int D>
 cudaError_t launch_d(const FmhaParams& p, int grid, cudaStream_t stream) {
     static int sel = [] {
         const char* e = getenv("TM_POLY");
-        return e ? atoi(e) : 4;
+        return e ? atoi(e) : 0;
     }();
     switch (sel) {
-        case 0: return launch_t<D, 0x0000u>(p, grid, stream);
+        case 4: return launch_t<D, 0x4444u>(p, grid, stream);   // {2,6,10,14}
         case 7: return launch_t<D, 0xA54Au>(p, grid, stream);   // {1,3,6,8,10,13,15}
         case 5: return launch_t<D, 0x2492u>(p, grid, stream);   // {1,4,7,10,13}
         case 6: return launch_t<D, 0x4A4Au>(p, grid, stream);   // {1,3,6,9,11,14}
