@@ -165,6 +165,22 @@ tm_status tm_kvcache_ref_ptr(tm_ctx* ctx, int32_t layer, int32_t step, void** k,
 tm_status tm_flow_euler_step(tm_ctx* ctx, float* x, const void* v, int32_t v_dtype, int64_t n,
                              float dt, void* stream);
 
+/* one schedule entry of the few-step student (2 NFE,
+ * P:153), fused: with the state x (device fp32 [n], in place)
+ * at time t_cur (Eq 1 convention: 0 = noise, 1 = data) and the
+ * predicted velocity v (TM_BF16 / TM_FP32 [n]):
+ *     x1_hat = x + (1 - t_cur) * v
+ *     x     <- t_next * x1_hat + (1 - t_next) * eps     (Eq 1 re-noise), or
+ *     x     <- x1_hat                                     if t_next >= 1 (final)
+ * eps: device fp32 [n], or NULL to draw N(0,1) in-kernel from Philox4x32-10
+ * (counter = (i / 4, offset), key = seed; Box-Muller on word pairs) --
+ * deterministic per (seed, offset, i).  x_bf16_out (nullable): bf16 copy of
+ * the new x, the next NFE's model input.  Needs 0 <= t_cur < 1 and
+ * t_next > t_cur.  x, v, eps 4-byte aligned. */
+tm_status tm_flow_sampler_step(tm_ctx* ctx, float* x, const void* v, int32_t v_dtype, int64_t n,
+                               float t_cur, float t_next, const float* eps, uint64_t seed,
+                               uint64_t offset, void* x_bf16_out, void* stream);
+
 /* Host reference of the Ulysses exchange layouts, the same index map
  * the device pack/unpack kernels use; for tests of the multi-rank host logic
  * without GPUs.  Buffers are host memory; rows of head_dim * elem_bytes bytes

@@ -67,6 +67,7 @@ def lib():
             getattr(L, f).argtypes = [P(d), P(d), d, i64, P(d)]
         L.orc_velocity_target.argtypes = [P(d), P(d), i64, P(d)]
         L.orc_euler.argtypes = [P(d), P(d), i64, d, P(d)]
+        L.orc_sampler_step.argtypes = [P(d), P(d), P(d), i64, d, d, P(d)]
         L.orc_set_num_threads.argtypes = [ctypes.c_int]
         L.orc_num_threads.restype = ctypes.c_int
         _lib = L
@@ -183,6 +184,62 @@ def euler(x, v, dt):
     if rc:
         raise OracleError(rc)
     return out
+
+
+def sampler_step(x, u, eps, t_cur, t_next):
+    """S:224 few-step update: x1_hat = x + (1 - t_cur) u, then Eq 1 re-noise
+    to t_next with eps (x1_hat itself when t_next >= 1)."""
+    x, u = _f64(x), _f64(u)
+    eps = _f64(eps)
+    if x.shape != u.shape or (eps is not None and eps.shape != x.shape):
+        raise OracleError(-1)
+    out = np.empty_like(x)
+    rc = lib().orc_sampler_step(_dp(x), _dp(u), _dp(eps), x.size, float(t_cur), float(t_next),
+                                _dp(out))
+    if rc:
+        raise OracleError(rc)
+    return out
+
+
+def philox4x32_10(counter, key):
+    """Philox4x32-10 (Salmon et al., SC'11), numpy uint32 words: counter
+    [..., 4], key [..., 2] -> [..., 4].  The oracle side's own implementation
+    of the counter-based generator the sampler kernel uses."""
+    M0, M1 = np.uint64(0xD2511F53), np.uint64(0xCD9E8D57)
+    W0, W1 = np.uint32(0x9E3779B9), np.uint32(0xBB67AE85)
+    c = [np.asarray(counter[..., i], dtype=np.uint32) for i in range(4)]
+    k0 = np.asarray(key[..., 0], dtype=np.uint32)
+    k1 = np.asarray(key[..., 1], dtype=np.uint32)
+    for _ in range(10):
+        p0 = c[0].astype(np.uint64) * M0
+        p1 = c[2].astype(np.uint64) * M1
+        hi0, lo0 = (p0 >> np.uint64(32)).astype(np.uint32), p0.astype(np.uint32)
+        hi1, lo1 = (p1 >> np.uint64(32)).astype(np.uint32), p1.astype(np.uint32)
+        c = [hi1 ^ c[1] ^ k0, lo1, hi0 ^ c[3] ^ k1, lo0]
+        k0 = k0 + W0
+        k1 = k1 + W1
+    return np.stack(c, axis=-1)
+
+
+def philox_normal(n, seed, offset):
+    """N(0,1) draws of the sampler's generator, in fp64: element i uses word
+    i % 4 of Philox(counter = (i // 4, 0, offset_lo, offset_hi), key = seed);
+    uniforms (w + 0.5) / 2^32 and the Box-Muller pairs (w0, w1), (w2, w3)."""
+    n4 = (n + 3) // 4
+    ctr = np.zeros((n4, 4), dtype=np.uint32)
+    idx = np.arange(n4, dtype=np.uint64)
+    ctr[:, 0] = (idx & np.uint64(0xFFFFFFFF)).astype(np.uint32)
+    ctr[:, 1] = (idx >> np.uint64(32)).astype(np.uint32)
+    ctr[:, 2] = np.uint32(offset & 0xFFFFFFFF)
+    ctr[:, 3] = np.uint32((offset >> 32) & 0xFFFFFFFF)
+    key = np.array([[seed & 0xFFFFFFFF, (seed >> 32) & 0xFFFFFFFF]], dtype=np.uint32)
+    w = philox4x32_10(ctr, np.repeat(key, n4, axis=0)).astype(np.float64)
+    uu = (w + 0.5) / 4294967296.0
+    r0 = np.sqrt(-2.0 * np.log(uu[:, 0]))
+    r1 = np.sqrt(-2.0 * np.log(uu[:, 2]))
+    z = np.stack([r0 * np.cos(2 * np.pi * uu[:, 1]), r0 * np.sin(2 * np.pi * uu[:, 1]),
+                  r1 * np.cos(2 * np.pi * uu[:, 3]), r1 * np.sin(2 * np.pi * uu[:, 3])], axis=1)
+    return z.reshape(-1)[:n]
 
 
 class StreamOracle:

@@ -20,6 +20,8 @@
  *   - orc_interpolate          P:60 (Eq 1)
  *   - orc_velocity_target      P:65 (Eq 2)
  *   - orc_euler                P:55 (ODE integration, x <- x + dt*v)
+ *   - orc_sampler_step         few-step student update:
+ *                              x1_hat = x + (1 - t) u; re-noise by Eq 1
  *
  * Tensor layout (all fp64, row-major, token-major as the API's
  * [L][H][d]):  element (token i, head h, dim c) at ((i*H)+h)*d + c.
@@ -233,5 +235,23 @@ int orc_velocity_target(const double* x0, const double* x1, int64_t n, double* o
 int orc_euler(const double* x, const double* v, int64_t n, double dt, double* out) {
     if (n < 0 || (n > 0 && (!x || !v || !out))) return ORC_ERR_DIM;
     for (int64_t i = 0; i < n; ++i) out[i] = x[i] + dt * v[i];
+    return ORC_OK;
+}
+
+/* Few-step generator update (student with 2 NFE), one
+ * schedule entry: given the state x at time t_cur (Eq 1 convention: t = 0
+ * noise, t = 1 data) and the predicted velocity u,
+ *   x1_hat = x + (1 - t_cur) * u                     (the implied clean sample)
+ *   x_next = t_next * x1_hat + (1 - t_next) * eps     (Eq 1 re-noise to t_next)
+ * and for the final entry (t_next >= 1) x_next = x1_hat.  eps may be NULL
+ * only when t_next >= 1. */
+int orc_sampler_step(const double* x, const double* u, const double* eps, int64_t n, double t_cur,
+                     double t_next, double* x_next) {
+    if (n < 0 || (n > 0 && (!x || !u || !x_next))) return ORC_ERR_DIM;
+    if (t_next < 1.0 && n > 0 && !eps) return ORC_ERR_ARG;
+    for (int64_t i = 0; i < n; ++i) {
+        const double x1_hat = x[i] + (1.0 - t_cur) * u[i];
+        x_next[i] = t_next >= 1.0 ? x1_hat : t_next * x1_hat + (1.0 - t_next) * eps[i];
+    }
     return ORC_OK;
 }

@@ -576,6 +576,27 @@ tm_status tm_ulysses_shuffle_host(int32_t mode, const void* src, void* dst, int3
     return TM_OK;
 }
 
+tm_status tm_flow_sampler_step(tm_ctx* ctx, float* x, const void* v, int32_t v_dtype, int64_t n,
+                               float t_cur, float t_next, const float* eps, uint64_t seed,
+                               uint64_t offset, void* x_bf16_out, void* stream) {
+    if (n < 0) return fail(TM_ERR_SHAPE, "n = %lld < 0", (long long)n);
+    if (n == 0) return TM_OK;
+    if (!x || !v) return fail(TM_ERR_INVALID_ARG, "null argument");
+    if (v_dtype != TM_BF16 && v_dtype != TM_FP32)
+        return fail(TM_ERR_INVALID_ARG, "v_dtype %d not in {TM_BF16, TM_FP32}", v_dtype);
+    if (!(t_cur >= 0.f && t_cur < 1.f) || !(t_next > t_cur) || !std::isfinite(t_next))
+        return fail(TM_ERR_INVALID_ARG, "need 0 <= t_cur < 1 and t_next > t_cur (Eq 1 time)");
+    int dummy = 0;
+    int* counter = ctx ? &ctx->launches : &dummy;
+    if (ctx) ctx->launches = 0;
+    cudaStream_t cs = static_cast<cudaStream_t>(stream);
+    tm_status st = cuda_check(launch_sampler(x, v, v_dtype == TM_BF16, eps, n, t_cur, t_next, seed,
+                                             offset, x_bf16_out, cs, counter),
+                              "sampler launch");
+    if (st || !ctx) return st;
+    return debug_check(ctx, x, n, 0, cs, "tm_flow_sampler_step");
+}
+
 int32_t tm_last_launch_count(const tm_ctx* ctx) { return ctx ? ctx->launches : -1; }
 
 const char* tm_kernel_variant(const tm_ctx* ctx) {

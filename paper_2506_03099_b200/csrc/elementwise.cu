@@ -81,6 +81,70 @@ __global__ void __launch_bounds__(256) euler_kernel(float* __restrict__ x,
     }
 }
 
+// ------------------------------------------------------------------ f2 sampler step
+// Philox4x32-10 (Salmon et al., SC'11): counter-based, so element i's noise is
+// a pure function of (seed, offset, i) -- deterministic and order-free.
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+        const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+        c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+        k.x += 0x9E3779B9u;
+        k.y += 0xBB67AE85u;
+    }
+    return c;
+}
+
+// S:224 one schedule entry of the few-step student, fused with the
+// noise draw and the bf16 cast of the next NFE's input:
+//   x1_hat = x + (1 - t_cur) v ;  x <- t_next x1_hat + (1 - t_next) eps  (Eq 1)
+// or x <- x1_hat for the final entry (t_next >= 1).  eps: caller's fp32 buffer
+// (kEps) or N(0,1) from Philox(counter = (i/4, offset), key = seed) with the
+// Box-Muller pairs (w0,w1), (w2,w3).  Each thread handles 4 elements.
+template <bool kBf16V, bool kEps>
+__global__ void __launch_bounds__(256) sampler_kernel(float* __restrict__ x,
+                                                      const void* __restrict__ vv,
+                                                      const float* __restrict__ eps, int64_t n,
+                                                      float t_cur, float t_next, uint2 seed,
+                                                      uint2 offset, uint16_t* __restrict__ xb) {
+    const int64_t groups = (n + 3) / 4;
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    const bool final_step = t_next >= 1.f;
+    for (int64_t gi = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; gi < groups; gi += stride) {
+        float e[4] = {0.f, 0.f, 0.f, 0.f};
+        if (!final_step) {
+            if constexpr (kEps) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (4 * gi + j < n) e[j] = eps[4 * gi + j];
+            } else {
+                const uint4 w = philox4x32_10(
+                    make_uint4(uint32_t(gi), uint32_t(uint64_t(gi) >> 32), offset.x, offset.y), seed);
+                const float k32 = 2.3283064365386963e-10f;      // 2^-32
+                const float u0 = fmaf(float(w.x), k32, 0.5f * k32), u1 = fmaf(float(w.y), k32, 0.5f * k32);
+                const float u2 = fmaf(float(w.z), k32, 0.5f * k32), u3 = fmaf(float(w.w), k32, 0.5f * k32);
+                const float r0 = sqrtf(-2.f * logf(u0)), r1 = sqrtf(-2.f * logf(u2));
+                float s0, c0, s1, c1;
+                sincospif(2.f * u1, &s0, &c0);
+                sincospif(2.f * u3, &s1, &c1);
+                e[0] = r0 * c0; e[1] = r0 * s0; e[2] = r1 * c1; e[3] = r1 * s1;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int64_t i = 4 * gi + j;
+            if (i >= n) break;
+            const float vi = kBf16V ? __uint_as_float(uint32_t(static_cast<const uint16_t*>(vv)[i]) << 16)
+                                    : static_cast<const float*>(vv)[i];
+            const float x1 = __fmaf_rn(1.f - t_cur, vi, x[i]);
+            const float xn = final_step ? x1 : __fmaf_rn(t_next, x1, (1.f - t_next) * e[j]);
+            x[i] = xn;
+            if (xb) xb[i] = __bfloat16_as_ushort(__float2bfloat16_rn(xn));
+        }
+    }
+}
+
 // ------------------------------------------------------------------ finiteness
 template <bool kBf16>
 __global__ void nonfinite_kernel(const void* __restrict__ x, int64_t n, int* flag) {
@@ -129,6 +193,25 @@ cudaError_t launch_euler(float* x, const void* v, int v_is_bf16, int64_t n, floa
         euler_kernel<true><<<grid, 256, 0, s>>>(x, v, n, dt);
     else
         euler_kernel<false><<<grid, 256, 0, s>>>(x, v, n, dt);
+    if (launches) ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sampler(float* x, const void* v, int v_is_bf16, const float* eps, int64_t n,
+                           float t_cur, float t_next, uint64_t seed, uint64_t offset,
+                           void* x_bf16, cudaStream_t s, int* launches) {
+    if (n <= 0) return cudaSuccess;
+    const unsigned grid = grid_for((n + 3) / 4, 256, 4);
+    const uint2 sd = make_uint2(uint32_t(seed), uint32_t(seed >> 32));
+    const uint2 of = make_uint2(uint32_t(offset), uint32_t(offset >> 32));
+    uint16_t* xb = static_cast<uint16_t*>(x_bf16);
+    if (v_is_bf16) {
+        if (eps) sampler_kernel<true, true><<<grid, 256, 0, s>>>(x, v, eps, n, t_cur, t_next, sd, of, xb);
+        else sampler_kernel<true, false><<<grid, 256, 0, s>>>(x, v, eps, n, t_cur, t_next, sd, of, xb);
+    } else {
+        if (eps) sampler_kernel<false, true><<<grid, 256, 0, s>>>(x, v, eps, n, t_cur, t_next, sd, of, xb);
+        else sampler_kernel<false, false><<<grid, 256, 0, s>>>(x, v, eps, n, t_cur, t_next, sd, of, xb);
+    }
     if (launches) ++*launches;
     return cudaGetLastError();
 }

@@ -44,6 +44,10 @@ cudaError_t launch_fmha_sm100(const AttnProblem& p, void* scratch, cudaStream_t 
 cudaError_t launch_fmha_fp32(const AttnProblem& p, cudaStream_t s, int* launches);
 cudaError_t launch_euler(float* x, const void* v, int v_is_bf16, int64_t n, float dt,
                          cudaStream_t s, int* launches);
+// f2: few-step sampler entry (see elementwise.cu); eps == nullptr -> Philox noise.
+cudaError_t launch_sampler(float* x, const void* v, int v_is_bf16, const float* eps, int64_t n,
+                           float t_cur, float t_next, uint64_t seed, uint64_t offset,
+                           void* x_bf16, cudaStream_t s, int* launches);
 // Non-finite check: sets *flag (device int) to 1 if any element is NaN/Inf.
 cudaError_t launch_nonfinite(const void* x, int is_bf16, int64_t n, int* flag, cudaStream_t s,
                              int* launches);

@@ -65,6 +65,8 @@ def _load():
         "tm_flow_euler_step": ([V, V, V, i32, i64, ctypes.c_float, V], i32),
         "tm_ulysses_shuffle_host": ([i32, V, V, i32, i64, i64, i32, i32, i32, i32], i32),
         "tm_window_attention": ([V, V, V, V, V, P(i64), i32, V], i32),
+        "tm_flow_sampler_step": ([V, V, V, i32, i64, ctypes.c_float, ctypes.c_float, V,
+                                  ctypes.c_uint64, ctypes.c_uint64, V, V], i32),
         "tm_last_launch_count": ([V], i32),
         "tm_kernel_variant": ([V], ctypes.c_char_p),
     }
@@ -81,7 +83,7 @@ EXPORTED = ("tm_version", "tm_last_error", "tm_kvcache_bytes", "tm_workspace_byt
             "tm_get_unique_id", "tm_attn_init", "tm_attn_destroy", "tm_stream_reset",
             "tm_kvcache_put_reference", "tm_chunk_attention", "tm_kvcache_slot_ptr",
             "tm_kvcache_ref_ptr", "tm_flow_euler_step", "tm_ulysses_shuffle_host",
-            "tm_window_attention",
+            "tm_window_attention", "tm_flow_sampler_step",
             "tm_last_launch_count",
             "tm_kernel_variant")
 
@@ -167,6 +169,12 @@ def tm_kvcache_ref_ptr(ctx, layer, step):
 
 def tm_flow_euler_step(ctx, x, v, v_dtype, n, dt, stream=None) -> None:
     _check(lib.tm_flow_euler_step(ctx, _ptr(x), _ptr(v), v_dtype, n, dt, _stream(stream)))
+
+
+def tm_flow_sampler_step(ctx, x, v, v_dtype, n, t_cur, t_next, eps=None, seed=0, offset=0,
+                         x_bf16_out=None, stream=None) -> None:
+    _check(lib.tm_flow_sampler_step(ctx, _ptr(x), _ptr(v), v_dtype, n, t_cur, t_next, _ptr(eps),
+                                    seed, offset, _ptr(x_bf16_out), _stream(stream)))
 
 
 def tm_window_attention(ctx, q, k, v, o, chunk_lens, stream=None) -> None:

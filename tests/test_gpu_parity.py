@@ -441,3 +441,46 @@ def test_window_equals_streaming_bitwise():
         ca.attend(0, 0, t, qd[sl].contiguous(), kd[sl].contiguous(), vd[sl].contiguous(), os_)
         assert torch.equal(os_.view(torch.int16), ow[sl].view(torch.int16)), t
     ca.close()
+
+
+# ------------------------------------------------------------------ sampler step
+
+@pytest.mark.parametrize("v_dtype", ["fp32", "bf16"])
+def test_sampler_step_with_given_noise_vs_oracle(v_dtype):
+    """f2: x1_hat = x + (1 - t) v, Eq 1 re-noise with eps; the 2-NFE
+    student schedule t = 0 -> 0.5 -> final (reading Q10), vs the oracle."""
+    n = 196_608 + 5
+    x, v = syn.euler_inputs(n, syn.seed_for(11, 0), v_dtype)
+    eps = syn.euler_inputs(n, syn.seed_for(11, 1))[0]
+    xd, vd, ed = to_dev(x), to_dev(v), to_dev(eps)
+    xb = torch.empty(n, dtype=torch.bfloat16, device="cuda")
+    ref = oracle.sampler_step(x.f64, v.f64, eps.f64, 0.0, 0.5)
+    tm.tm_flow_sampler_step(None, xd, vd, DT[v_dtype], n, 0.0, 0.5, eps=ed, x_bf16_out=xb)
+    torch.cuda.synchronize()
+    assert np.abs(from_dev(xd) - ref).max() <= 1e-6 * np.abs(ref).max()
+    assert torch.equal(xb, xd.to(torch.bfloat16))            # bf16 RNE of the new state
+    ref2 = oracle.sampler_step(from_dev(xd), v.f64, None, 0.5, 1.0)
+    tm.tm_flow_sampler_step(None, xd, vd, DT[v_dtype], n, 0.5, 1.0)
+    torch.cuda.synchronize()
+    assert np.abs(from_dev(xd) - ref2).max() <= 1e-6 * np.abs(ref2).max()
+
+
+def test_sampler_in_kernel_philox_matches_oracle_generator():
+    """f2 noise: with x = v = 0, t: 0 -> 0.5 the new state is eps / 2; the
+    kernel's Philox4x32-10 + Box-Muller draws equal the oracle side's own
+    implementation (KAT-pinned) to fp32 rounding; deterministic per seed."""
+    n = 1_000_003
+    for seed, offset in ((2506030990, 0), (7, 12345)):
+        xd = torch.zeros(n, device="cuda")
+        vd = torch.zeros(n, device="cuda")
+        tm.tm_flow_sampler_step(None, xd, vd, tm.TM_FP32, n, 0.0, 0.5, seed=seed, offset=offset)
+        torch.cuda.synchronize()
+        z = 2.0 * xd.double().cpu().numpy()
+        ref = oracle.philox_normal(n, seed, offset)
+        assert np.abs(z - ref).max() < 2e-4
+        x2 = torch.zeros(n, device="cuda")
+        tm.tm_flow_sampler_step(None, x2, vd, tm.TM_FP32, n, 0.0, 0.5, seed=seed, offset=offset)
+        torch.cuda.synchronize()
+        assert torch.equal(x2, xd)
+    with pytest.raises(tm.TMError):
+        tm.tm_flow_sampler_step(None, xd, vd, tm.TM_FP32, n, 0.5, 0.5)     # t_next must exceed t

@@ -290,3 +290,46 @@ def test_euler_lands_on_the_interpolant():
     assert np.abs(fd - v).max() < 1e-8
     assert (oracle.interpolate(x0, x1, 0.0) == x0).all()
     assert (oracle.interpolate(x0, x1, 1.0) == x1).all()
+
+
+# --------------------------------------------------------------------------
+# f2: few-step sampler update and its noise generator
+# --------------------------------------------------------------------------
+
+def test_sampler_point_mass_recovers_x1():
+    """a student exact for a point-mass dataset (u = (x1 - x_t)/(1 - t))
+    returns x1; re-noising to t' lands on the Eq 1 interpolant of (eps, x1)."""
+    rng = np.random.default_rng(21)
+    x0, x1, eps = (rng.standard_normal(500) for _ in range(3))
+    for t, t2 in [(0.0, 0.5), (0.25, 0.75), (0.5, 1.0)]:
+        xt = oracle.interpolate(x0, x1, t)
+        u = (x1 - xt) / (1.0 - t)
+        out = oracle.sampler_step(xt, u, eps, t, t2)
+        expect = x1 if t2 >= 1.0 else oracle.interpolate(eps, x1, t2)
+        assert np.abs(out - expect).max() < 1e-12
+
+
+def test_sampler_final_step_is_an_euler_step():
+    """S:220 (reading Q10): the last schedule entry is one Euler step of
+    dt = 1 - t (no re-noise)."""
+    rng = np.random.default_rng(22)
+    x, u = rng.standard_normal(300), rng.standard_normal(300)
+    for t in (0.0, 0.5, 0.9):
+        assert np.abs(oracle.sampler_step(x, u, None, t, 1.0) - oracle.euler(x, u, 1.0 - t)).max() == 0
+    with pytest.raises(oracle.OracleError):
+        oracle.sampler_step(x, u, None, 0.0, 0.5)       # re-noise needs eps
+
+
+def test_philox_known_answers():
+    g = gold("philox_kat.json")
+    for vec in g["vectors"]:
+        c = np.array([[int(w, 16) for w in vec["counter"]]], dtype=np.uint32)
+        k = np.array([[int(w, 16) for w in vec["key"]]], dtype=np.uint32)
+        out = oracle.philox4x32_10(c, k)[0]
+        assert [int(w) for w in out] == [int(w, 16) for w in vec["out"]]
+
+
+def test_philox_normal_moments():
+    z = oracle.philox_normal(2_000_000, seed=2506030990, offset=3)
+    assert abs(z.mean()) < 3e-3 and abs(z.var() - 1) < 4e-3
+    assert abs(np.mean(z ** 4) - 3) < 0.03            # Gaussian kurtosis
