@@ -149,6 +149,28 @@ tm_status tm_chunk_attention(tm_ctx* ctx, int32_t layer, int32_t step, int64_t c
 tm_status tm_window_attention(tm_ctx* ctx, const void* q, const void* k, const void* v, void* o,
                               const int64_t* chunk_len, int32_t n_chunks, void* stream);
 
+/* audio cross-attention with a face-region query mask
+ * (keys/values from audio tokens, cross-attended by the latent-frame
+ * queries, "local attention masks that focus on facial regions"; P:125:
+ * "each latent frame will attend only to the audio tokens within a window of
+ * five latent frames centered around itself").
+ *   q: device [B][frames][T][H][d]      latent tokens of `frames` latent frames
+ *   k_audio, v_audio: device [B][frames][A][H][d]   projected audio tokens
+ *   o: device [B][frames][T][H][d]      face rows: attention output; others 0
+ *   face_ids: DEVICE int32 [n_face], token indices in [0, T) (the face region)
+ *   window: odd, <= 5; frames outside [0, frames) are clamped by repeating the
+ *   boundary frame (SPEC S:117 design decision; frame 0 -> {0,0,0,1,2}).
+ *   scratch: device, >= tm_audio_scratch_bytes(ctx, frames, n_face), 1024-B
+ *   aligned (gathered face rows of q and o).
+ * n_face == 0 -> TM_ERR_DEGENERATE_MASK.  B, H, d, dtype, scale from
+ * ctx (world_size 1).  Launches: gather, one attention per frame, scatter. */
+size_t tm_audio_scratch_bytes(const tm_ctx* ctx, int64_t frames, int64_t n_face);
+tm_status tm_audio_cross_attention(tm_ctx* ctx, const void* q, const void* k_audio,
+                                   const void* v_audio, void* o, int64_t frames,
+                                   int64_t tokens_per_frame, int64_t audio_tokens_per_frame,
+                                   const int32_t* face_ids, int64_t n_face, int32_t window,
+                                   void* scratch, size_t scratch_bytes, void* stream);
+
 /* Device pointers of the cache slot that chunk `chunk` at (layer, step) is
  * stored in ([B][Lc][H/P][d] each).  A caller may write the chunk's K/V
  * there before tm_chunk_attention to skip the append copy. */

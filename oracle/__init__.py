@@ -68,6 +68,9 @@ def lib():
         L.orc_velocity_target.argtypes = [P(d), P(d), i64, P(d)]
         L.orc_euler.argtypes = [P(d), P(d), i64, d, P(d)]
         L.orc_sampler_step.argtypes = [P(d), P(d), P(d), i64, d, d, P(d)]
+        L.orc_audio_window.argtypes = [i64, i64, ctypes.c_int, P(i64)]
+        L.orc_audio_cross_attention.argtypes = [P(d), P(d), P(d), i64, i64, i64, ctypes.c_int,
+                                                ctypes.c_int, P(i64), i64, ctypes.c_int, d, P(d)]
         L.orc_set_num_threads.argtypes = [ctypes.c_int]
         L.orc_num_threads.restype = ctypes.c_int
         _lib = L
@@ -196,6 +199,34 @@ def sampler_step(x, u, eps, t_cur, t_next):
     out = np.empty_like(x)
     rc = lib().orc_sampler_step(_dp(x), _dp(u), _dp(eps), x.size, float(t_cur), float(t_next),
                                 _dp(out))
+    if rc:
+        raise OracleError(rc)
+    return out
+
+
+def audio_window(frames, f, window=5):
+    """P:125 window of latent frames around f, edges clamped by repetition."""
+    out = (ctypes.c_int64 * window)()
+    rc = lib().orc_audio_window(int(frames), int(f), int(window), out)
+    if rc:
+        raise OracleError(rc)
+    return [int(out[i]) for i in range(window)]
+
+
+def audio_cross_attention(q, k, v, face_ids, window=5, scale=None):
+    """P:123-125 / S:120-129: q [frames][T][H][d], k/v [frames][A][H][d];
+    face-token rows attend their frame's audio window; other rows are 0."""
+    q, k, v = _f64(q), _f64(k), _f64(v)
+    frames, T, H, d = q.shape
+    A = k.shape[1]
+    if k.shape != (frames, A, H, d) or v.shape != k.shape:
+        raise OracleError(-1)
+    fid = np.ascontiguousarray(face_ids, dtype=np.int64)
+    scale = 1.0 / np.sqrt(d) if scale is None else float(scale)
+    out = np.empty_like(q)
+    rc = lib().orc_audio_cross_attention(_dp(q), _dp(k), _dp(v), frames, T, A, H, d,
+                                         fid.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                         len(fid), int(window), scale, _dp(out))
     if rc:
         raise OracleError(rc)
     return out

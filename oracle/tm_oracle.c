@@ -22,6 +22,10 @@
  *   - orc_euler                P:55 (ODE integration, x <- x + dt*v)
  *   - orc_sampler_step         few-step student update:
  *                              x1_hat = x + (1 - t) u; re-noise by Eq 1
+ *   - orc_audio_window         5-latent-frame audio window, edges
+ *                              clamped by repeating the boundary frame
+ *   - orc_audio_cross_attention audio cross-attention of the face-region query
+ *                              tokens of each latent frame
  *
  * Tensor layout (all fp64, row-major, token-major as the API's
  * [L][H][d]):  element (token i, head h, dim c) at ((i*H)+h)*d + c.
@@ -254,4 +258,68 @@ int orc_sampler_step(const double* x, const double* u, const double* eps, int64_
         x_next[i] = t_next >= 1.0 ? x1_hat : t_next * x1_hat + (1.0 - t_next) * eps[i];
     }
     return ORC_OK;
+}
+
+/* "each latent frame will attend only to the audio tokens within a
+ * window of five latent frames centered around itself"; SPEC S:116-118 and its
+ * design decision: frames [f - W/2, f + W/2] clamped to [0, frames - 1] by
+ * repeating the boundary frame (f = 0 -> {0, 0, 0, 1, 2}).  Writes W frame
+ * indices. */
+int orc_audio_window(int64_t frames, int64_t f, int window, int64_t* out) {
+    if (frames <= 0 || f < 0 || f >= frames || window <= 0 || window % 2 == 0) return ORC_ERR_ARG;
+    for (int i = 0; i < window; ++i) {
+        int64_t g = f - window / 2 + i;
+        if (g < 0) g = 0;
+        if (g > frames - 1) g = frames - 1;
+        out[i] = g;
+    }
+    return ORC_OK;
+}
+
+/* P:123 (audio cross attention restricted to facial-region queries) with the
+ * P:125 window: q [frames][T][H][d] latent-frame tokens, k/v [frames][A][H][d]
+ * audio tokens; for every frame f and face token t (face_ids, a subset of
+ * [0, T)) the keys/values are the concatenation of the audio tokens of the
+ * window frames of f (orc_audio_window), softmax(q k^T * scale) v (Eq 7's
+ * form).  Non-face rows of out are 0 (no residual update). */
+int orc_audio_cross_attention(const double* q, const double* k, const double* v, int64_t frames,
+                              int64_t T, int64_t A, int H, int d, const int64_t* face_ids,
+                              int64_t n_face, int window, double scale, double* out) {
+    if (frames <= 0 || T <= 0 || A <= 0 || H <= 0 || d <= 0 || !q || !k || !v || !out) return ORC_ERR_DIM;
+    if (n_face <= 0 || !face_ids) return ORC_ERR_DEGENERATE;      /* empty face mask */
+    for (int64_t i = 0; i < n_face; ++i)
+        if (face_ids[i] < 0 || face_ids[i] >= T) return ORC_ERR_DIM;
+    const int64_t row = (int64_t)H * d;
+    memset(out, 0, sizeof(double) * (size_t)(frames * T * row));
+    int64_t* win = (int64_t*)malloc(sizeof(int64_t) * (size_t)window);
+    if (!win) return ORC_ERR_ARG;
+    int status = ORC_OK;
+    for (int64_t f = 0; f < frames && status == ORC_OK; ++f) {
+        status = orc_audio_window(frames, f, window, win);
+        if (status) break;
+        const int64_t Lk = (int64_t)window * A;
+#pragma omp parallel
+        {
+            const double** kr = (const double**)malloc(sizeof(double*) * (size_t)Lk);
+            const double** vr = (const double**)malloc(sizeof(double*) * (size_t)Lk);
+            double* s = (double*)malloc(sizeof(double) * (size_t)Lk);
+#pragma omp for collapse(2)
+            for (int64_t i = 0; i < n_face; ++i) {
+                for (int h = 0; h < H; ++h) {
+                    for (int w = 0; w < window; ++w)
+                        for (int64_t a = 0; a < A; ++a) {
+                            const int64_t tok = win[w] * A + a;
+                            kr[w * A + a] = k + tok * row + (int64_t)h * d;
+                            vr[w * A + a] = v + tok * row + (int64_t)h * d;
+                        }
+                    const int64_t t = face_ids[i];
+                    attend_row(q + (f * T + t) * row + (int64_t)h * d, d, kr, vr, Lk, scale, s,
+                               out + (f * T + t) * row + (int64_t)h * d);
+                }
+            }
+            free(kr); free(vr); free(s);
+        }
+    }
+    free(win);
+    return status;
 }

@@ -534,6 +534,90 @@ tm_status tm_window_attention(tm_ctx* ctx, const void* q, const void* k, const v
                        cs, "tm_window_attention");
 }
 
+size_t tm_audio_scratch_bytes(const tm_ctx* ctx, int64_t frames, int64_t n_face) {
+    if (!ctx || frames <= 0 || n_face <= 0) return 0;
+    const size_t rows = size_t(ctx->cfg.batch) * frames * n_face;
+    return 2 * align_up(rows * ctx->cfg.heads * ctx->cfg.head_dim * ctx->lay.esize);
+}
+
+tm_status tm_audio_cross_attention(tm_ctx* ctx, const void* q, const void* k_audio,
+                                   const void* v_audio, void* o, int64_t frames,
+                                   int64_t tokens_per_frame, int64_t audio_tokens_per_frame,
+                                   const int32_t* face_ids, int64_t n_face, int32_t window,
+                                   void* scratch, size_t scratch_bytes, void* stream) {
+    if (!ctx || !q || !k_audio || !v_audio || !o || !scratch)
+        return fail(TM_ERR_INVALID_ARG, "null argument");
+    if (ctx->lay.exchange)
+        return fail(TM_ERR_UNSUPPORTED, "tm_audio_cross_attention needs a world_size == 1 context");
+    if (frames <= 0 || tokens_per_frame <= 0 || audio_tokens_per_frame <= 0)
+        return fail(TM_ERR_SHAPE, "non-positive frames / tokens");
+    if (n_face <= 0 || !face_ids)
+        return fail(TM_ERR_DEGENERATE_MASK, "empty face mask: no query attends the audio (S:124)");
+    if (n_face > tokens_per_frame) return fail(TM_ERR_SHAPE, "more face tokens than frame tokens");
+    if (window <= 0 || window % 2 == 0) return fail(TM_ERR_INVALID_ARG, "window must be odd, got %d", window);
+    if (window > kMaxSegments)
+        return fail(TM_ERR_UNSUPPORTED, "window %d > %d: an edge window needs more segments",
+                    window, kMaxSegments);
+    if (scratch_bytes < tm_audio_scratch_bytes(ctx, frames, n_face))
+        return fail(TM_ERR_INVALID_ARG, "scratch %zu bytes < tm_audio_scratch_bytes", scratch_bytes);
+    if (!aligned16(q) || !aligned16(k_audio) || !aligned16(v_audio) || !aligned16(o) ||
+        reinterpret_cast<uintptr_t>(scratch) % kAlign)
+        return fail(TM_ERR_INVALID_ARG, "q, k, v, o 16-byte and scratch 1024-byte aligned required");
+    const tm_config& cf = ctx->cfg;
+    const int row = cf.heads * cf.head_dim * ctx->lay.esize;          // bytes per token
+    const int64_t BF = int64_t(cf.batch) * frames;
+    uint8_t* qf = static_cast<uint8_t*>(scratch);
+    uint8_t* of = qf + scratch_bytes / 2;
+    cudaStream_t cs = static_cast<cudaStream_t>(stream);
+    ctx->launches = 0;
+    tm_status st = cuda_check(launch_face_rows(q, qf, face_ids, BF, tokens_per_frame, n_face, row, 0,
+                                               cs, &ctx->launches), "face gather");
+    if (st) return st;
+    const uint8_t* kb = static_cast<const uint8_t*>(k_audio);
+    const uint8_t* vb = static_cast<const uint8_t*>(v_audio);
+    for (int64_t f = 0; f < frames; ++f) {
+        // P:125 window, edges clamped by repetition, as runs of
+        // consecutive frames = contiguous audio-token segments (<= W of them).
+        int64_t win[kMaxSegments];
+        for (int i = 0; i < window; ++i) {
+            int64_t g = f - window / 2 + i;
+            win[i] = g < 0 ? 0 : (g > frames - 1 ? frames - 1 : g);
+        }
+        AttnProblem pr;
+        pr.q = qf + f * n_face * row;
+        pr.o = of + f * n_face * row;
+        pr.Lq = n_face;
+        pr.q_bstride = frames * n_face;
+        pr.B = cf.batch;
+        pr.H = cf.heads;
+        pr.d = cf.head_dim;
+        pr.scale = ctx->scale;
+        int i = 0;
+        while (i < window) {
+            int j = i;
+            while (j + 1 < window && win[j + 1] == win[j] + 1) ++j;
+            const int64_t tok0 = win[i] * audio_tokens_per_frame;
+            pr.seg[pr.nseg++] = Segment{kb + tok0 * row, vb + tok0 * row,
+                                        (j - i + 1) * audio_tokens_per_frame,
+                                        frames * audio_tokens_per_frame};
+            i = j + 1;
+        }
+        const cudaError_t e = cf.dtype == TM_BF16
+                                  ? launch_fmha_sm100(pr, ctx->scratch(), cs, &ctx->launches)
+                                  : launch_fmha_fp32(pr, cs, &ctx->launches);
+        st = cuda_check(e, "audio cross-attention launch");
+        if (st) return st;
+    }
+    // non-face rows get no update: zero, then scatter the face rows
+    st = cuda_check(cudaMemsetAsync(o, 0, size_t(BF) * tokens_per_frame * row, cs), "zero output");
+    if (st) return st;
+    st = cuda_check(launch_face_rows(of, o, face_ids, BF, tokens_per_frame, n_face, row, 1, cs,
+                                     &ctx->launches), "face scatter");
+    if (st) return st;
+    return debug_check(ctx, o, BF * tokens_per_frame * cf.heads * cf.head_dim, cf.dtype == TM_BF16,
+                       cs, "tm_audio_cross_attention");
+}
+
 tm_status tm_flow_euler_step(tm_ctx* ctx, float* x, const void* v, int32_t v_dtype, int64_t n,
                              float dt, void* stream) {
     if (n < 0) return fail(TM_ERR_SHAPE, "n = %lld < 0", (long long)n);

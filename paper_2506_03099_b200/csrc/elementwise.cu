@@ -145,6 +145,27 @@ __global__ void __launch_bounds__(256) sampler_kernel(float* __restrict__ x,
     }
 }
 
+// ------------------------------------------------------------------ f4 face-row gather / scatter
+// Rows of W 16-byte words.  gather: dst[bf][i] = src[bf][ids[i]]  (bf = b * frames + f)
+//                           scatter: dst[bf][ids[i]] = src[bf][i]
+template <bool kScatter>
+__global__ void __launch_bounds__(256) face_rows_kernel(const uint4* __restrict__ src,
+                                                        uint4* __restrict__ dst,
+                                                        const int32_t* __restrict__ ids,
+                                                        int64_t BF, int64_t T, int64_t nf, int W) {
+    const int64_t total = BF * nf * W;
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < total; idx += stride) {
+        const int w = int(idx % W);
+        const int64_t r = idx / W;
+        const int64_t i = r % nf, bf = r / nf;
+        const int64_t full = (bf * T + ids[i]) * W + w;
+        const int64_t comp = (bf * nf + i) * W + w;
+        if (kScatter) dst[full] = src[comp];
+        else dst[comp] = src[full];
+    }
+}
+
 // ------------------------------------------------------------------ finiteness
 template <bool kBf16>
 __global__ void nonfinite_kernel(const void* __restrict__ x, int64_t n, int* flag) {
@@ -212,6 +233,21 @@ cudaError_t launch_sampler(float* x, const void* v, int v_is_bf16, const float* 
         if (eps) sampler_kernel<false, true><<<grid, 256, 0, s>>>(x, v, eps, n, t_cur, t_next, sd, of, xb);
         else sampler_kernel<false, false><<<grid, 256, 0, s>>>(x, v, eps, n, t_cur, t_next, sd, of, xb);
     }
+    if (launches) ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_face_rows(const void* src, void* dst, const int32_t* ids, int64_t BF, int64_t T,
+                            int64_t nf, int row_bytes, int scatter, cudaStream_t s, int* launches) {
+    if (row_bytes % 16) return cudaErrorInvalidValue;
+    const int W = row_bytes / 16;
+    const unsigned grid = grid_for(BF * nf * W, 256, 8);
+    if (scatter)
+        face_rows_kernel<true><<<grid, 256, 0, s>>>(static_cast<const uint4*>(src),
+                                                    static_cast<uint4*>(dst), ids, BF, T, nf, W);
+    else
+        face_rows_kernel<false><<<grid, 256, 0, s>>>(static_cast<const uint4*>(src),
+                                                     static_cast<uint4*>(dst), ids, BF, T, nf, W);
     if (launches) ++*launches;
     return cudaGetLastError();
 }

@@ -6,7 +6,7 @@
 
 namespace tmk {
 
-constexpr int kMaxSegments = 3;   // {c_0, c_{t-1}, c_t}
+constexpr int kMaxSegments = 5;   // {c_0, c_{t-1}, c_t}; f4 audio windows need up to 5
 constexpr int kMaxPersistentCtas = 160;   // persistent grid cap (B200: 148 SMs)
 
 // One contiguous K/V segment in token-major layout [B][len][H][d].
@@ -48,6 +48,9 @@ cudaError_t launch_euler(float* x, const void* v, int v_is_bf16, int64_t n, floa
 cudaError_t launch_sampler(float* x, const void* v, int v_is_bf16, const float* eps, int64_t n,
                            float t_cur, float t_next, uint64_t seed, uint64_t offset,
                            void* x_bf16, cudaStream_t s, int* launches);
+// f4: gather (scatter = 0) / scatter (1) of face-token rows, ids device int32.
+cudaError_t launch_face_rows(const void* src, void* dst, const int32_t* ids, int64_t BF, int64_t T,
+                            int64_t nf, int row_bytes, int scatter, cudaStream_t s, int* launches);
 // Non-finite check: sets *flag (device int) to 1 if any element is NaN/Inf.
 cudaError_t launch_nonfinite(const void* x, int is_bf16, int64_t n, int* flag, cudaStream_t s,
                              int* launches);

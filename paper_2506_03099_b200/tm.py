@@ -65,6 +65,8 @@ def _load():
         "tm_flow_euler_step": ([V, V, V, i32, i64, ctypes.c_float, V], i32),
         "tm_ulysses_shuffle_host": ([i32, V, V, i32, i64, i64, i32, i32, i32, i32], i32),
         "tm_window_attention": ([V, V, V, V, V, P(i64), i32, V], i32),
+        "tm_audio_scratch_bytes": ([V, i64, i64], S),
+        "tm_audio_cross_attention": ([V, V, V, V, V, i64, i64, i64, V, i64, i32, V, S, V], i32),
         "tm_flow_sampler_step": ([V, V, V, i32, i64, ctypes.c_float, ctypes.c_float, V,
                                   ctypes.c_uint64, ctypes.c_uint64, V, V], i32),
         "tm_last_launch_count": ([V], i32),
@@ -83,7 +85,8 @@ EXPORTED = ("tm_version", "tm_last_error", "tm_kvcache_bytes", "tm_workspace_byt
             "tm_get_unique_id", "tm_attn_init", "tm_attn_destroy", "tm_stream_reset",
             "tm_kvcache_put_reference", "tm_chunk_attention", "tm_kvcache_slot_ptr",
             "tm_kvcache_ref_ptr", "tm_flow_euler_step", "tm_ulysses_shuffle_host",
-            "tm_window_attention", "tm_flow_sampler_step",
+            "tm_window_attention", "tm_flow_sampler_step", "tm_audio_scratch_bytes",
+            "tm_audio_cross_attention",
             "tm_last_launch_count",
             "tm_kernel_variant")
 
@@ -177,6 +180,19 @@ def tm_flow_sampler_step(ctx, x, v, v_dtype, n, t_cur, t_next, eps=None, seed=0,
                                     seed, offset, _ptr(x_bf16_out), _stream(stream)))
 
 
+def tm_audio_scratch_bytes(ctx, frames, n_face) -> int:
+    return lib.tm_audio_scratch_bytes(ctx, frames, n_face)
+
+
+def tm_audio_cross_attention(ctx, q, k_audio, v_audio, o, frames, tokens_per_frame,
+                             audio_tokens_per_frame, face_ids, n_face, window, scratch,
+                             scratch_bytes, stream=None) -> None:
+    _check(lib.tm_audio_cross_attention(ctx, _ptr(q), _ptr(k_audio), _ptr(v_audio), _ptr(o), frames,
+                                        tokens_per_frame, audio_tokens_per_frame, _ptr(face_ids),
+                                        n_face, window, _ptr(scratch), scratch_bytes,
+                                        _stream(stream)))
+
+
 def tm_window_attention(ctx, q, k, v, o, chunk_lens, stream=None) -> None:
     arr = (ctypes.c_int64 * len(chunk_lens))(*[int(x) for x in chunk_lens])
     _check(lib.tm_window_attention(ctx, _ptr(q), _ptr(k), _ptr(v), _ptr(o), arr, len(chunk_lens),
@@ -254,6 +270,20 @@ class ChunkAttention:
 
     def window(self, q, k, v, o, chunk_lens, stream=None):
         tm_window_attention(self.ctx, q, k, v, o, chunk_lens, stream)
+        return o
+
+    def audio(self, q, k_audio, v_audio, o, face_ids, window=5, stream=None):
+        """q/o [B][frames][T][H][d], k/v [B][frames][A][H][d] (or without B for
+        batch 1); face_ids: torch int32 CUDA tensor.  Scratch allocated here."""
+        import torch
+        frames, T = q.shape[-4], q.shape[-3]
+        A = k_audio.shape[-3]
+        n = face_ids.numel()
+        nb = tm_audio_scratch_bytes(self.ctx, frames, n)
+        scratch = torch.empty(nb + 1024, dtype=torch.uint8, device=q.device)
+        ptr = (scratch.data_ptr() + 1023) // 1024 * 1024
+        tm_audio_cross_attention(self.ctx, q, k_audio, v_audio, o, frames, T, A, face_ids, n,
+                                 window, ptr, nb, stream)
         return o
 
     def euler(self, x, v, v_dtype, dt, stream=None):

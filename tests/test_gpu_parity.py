@@ -484,3 +484,57 @@ def test_sampler_in_kernel_philox_matches_oracle_generator():
         assert torch.equal(x2, xd)
     with pytest.raises(tm.TMError):
         tm.tm_flow_sampler_step(None, xd, vd, tm.TM_FP32, n, 0.5, 0.5)     # t_next must exceed t
+
+
+# ------------------------------------------------------------------ audio cross-attention
+
+def _audio_case(frames, T, A, H, d, n_face, dtype, seed, B=1):
+    rng = np.random.default_rng(seed)
+    q, _, _ = syn.chunk_qkv(rng, B * frames * T, H, d, dtype, "D0")
+    k, v, _ = syn.chunk_qkv(rng, B * frames * A, H, d, dtype, "D0")
+    face = np.sort(rng.choice(T, size=n_face, replace=False)).astype(np.int32)
+    return q, k, v, face
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+@pytest.mark.parametrize("frames,T,A,n_face", [(3, 64, 8, 20), (7, 40, 5, 40), (1, 33, 3, 1), (2, 50, 16, 7)])
+def test_audio_cross_attention_vs_oracle(dtype, frames, T, A, n_face):
+    """f4: face rows attend the clamped 5-frame audio
+    window; non-face rows are exactly zero."""
+    H, d = 4, 128
+    q, k, v, face = _audio_case(frames, T, A, H, d, n_face, dtype, syn.seed_for(12, frames, extra=T))
+    ca = tm.ChunkAttention(H, d, 16, 16, 1, 1, dtype=DT[dtype])
+    qd = to_dev(q).view(frames, T, H, d)
+    kd, vd = to_dev(k).view(frames, A, H, d), to_dev(v).view(frames, A, H, d)
+    o = torch.full_like(qd, 7.0)
+    ca.audio(qd, kd, vd, o, torch.from_numpy(face).cuda())
+    ref = oracle.audio_cross_attention(q.f64.reshape(frames, T, H, d), k.f64.reshape(frames, A, H, d),
+                                       v.f64.reshape(frames, A, H, d), face)
+    got = from_dev(o)
+    non_face = np.setdiff1d(np.arange(T), face)
+    assert (got[:, non_face] == 0).all()
+    assert rel_err(got[:, face], ref[:, face]) <= (FP32_TOL if dtype == "fp32" else BF16_ALARM)
+    ca.close()
+
+
+def test_audio_cross_attention_wan512_chunk_batch2():
+    """f4 at WAN-512 shape: a chunk of 3 latent frames of 32x32 tokens, a
+    16x16 face region (256 tokens), 32 audio tokens per frame (synthetic), 40
+    heads, batch of 2 streams."""
+    frames, T, A, H, d, B = 3, 1024, 32, 40, 128, 2
+    rng = np.random.default_rng(syn.seed_for(12, 99))
+    qs, ks, vs = syn.chunk_qkv(rng, B * frames * T, H, d, "bf16", "D0")
+    ka, va, _ = syn.chunk_qkv(rng, B * frames * A, H, d, "bf16", "D0")
+    face = np.array([r * 32 + c for r in range(8, 24) for c in range(8, 24)], dtype=np.int32)
+    ca = tm.ChunkAttention(H, d, 16, 16, 1, 1, batch=B)
+    qd = to_dev(qs).view(B, frames, T, H, d)
+    o = torch.empty_like(qd)
+    ca.audio(qd, to_dev(ka).view(B, frames, A, H, d), to_dev(va).view(B, frames, A, H, d), o,
+             torch.from_numpy(face).cuda())
+    got = from_dev(o)
+    for b in range(B):
+        ref = oracle.audio_cross_attention(qs.f64.reshape(B, frames, T, H, d)[b],
+                                           ka.f64.reshape(B, frames, A, H, d)[b],
+                                           va.f64.reshape(B, frames, A, H, d)[b], face)
+        assert rel_err(got[b][:, face], ref[:, face]) <= BF16_ALARM
+    ca.close()

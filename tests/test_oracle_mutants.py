@@ -23,6 +23,8 @@ MUTANTS = {
     "head_index": ("kr[j] = K + j * row + (int64_t)h * d;", "kr[j] = K + j * row;"),
     "interp_swapped": ("out[i] = t * x1[i] + (1.0 - t) * x0[i];", "out[i] = t * x0[i] + (1.0 - t) * x1[i];"),
     "prev_segment_dropped": ("if (Lp) { memcpy(K + Lr * row", "if (0) { memcpy(K + Lr * row"),
+    "audio_window_unclamped": ("if (g < 0) g = 0;", "if (g < 0) g = -g;"),
+    "audio_window_offset": ("int64_t g = f - window / 2 + i;", "int64_t g = f - window / 2 + i + 1;"),
     "sampler_no_time_factor": ("x[i] + (1.0 - t_cur) * u[i]", "x[i] + u[i]"),
     "sampler_renoise_swapped": ("t_next * x1_hat + (1.0 - t_next) * eps[i]",
                                 "(1.0 - t_next) * x1_hat + t_next * eps[i]"),

@@ -333,3 +333,73 @@ def test_philox_normal_moments():
     z = oracle.philox_normal(2_000_000, seed=2506030990, offset=3)
     assert abs(z.mean()) < 3e-3 and abs(z.var() - 1) < 4e-3
     assert abs(np.mean(z ** 4) - 3) < 0.03            # Gaussian kurtosis
+
+
+# --------------------------------------------------------------------------
+# f4: audio cross-attention with face-region query mask
+# --------------------------------------------------------------------------
+
+def test_audio_window_examples():
+    for c in gold("audio_window.json")["cases"]:
+        assert oracle.audio_window(c["frames"], c["frame_idx"], c["window"]) == c["window_frames"]
+
+
+def _audio_inputs(frames=5, T=6, A=3, H=2, d=4, seed=30):
+    rng = np.random.default_rng(seed)
+    return (rng.standard_normal((frames, T, H, d)), rng.standard_normal((frames, A, H, d)),
+            rng.standard_normal((frames, A, H, d)))
+
+
+def test_audio_non_face_rows_untouched_and_bruteforce():
+    """S:126 (non-face rows receive no update -> exactly 0 here) and the face
+    rows vs the independent dense double loop over the clamped window."""
+    q, k, v = _audio_inputs()
+    frames, T, A = q.shape[0], q.shape[1], k.shape[1]
+    face = [1, 4]
+    out = oracle.audio_cross_attention(q, k, v, face)
+    non_face = [t for t in range(T) if t not in face]
+    assert (out[:, non_face] == 0).all()
+    for f in range(frames):
+        lo = [min(max(g, 0), frames - 1) for g in range(f - 2, f + 3)]   # restated rule (S:117)
+        K = np.concatenate([k[g] for g in lo])
+        V = np.concatenate([v[g] for g in lo])
+        Lk = K.shape[0]
+        for t in face:
+            qq = np.concatenate([np.zeros((Lk - 1,) + q.shape[2:]), q[f, t][None]])
+            mask = [[True] * Lk for _ in range(Lk)]
+            bf = np.array(dense_masked_attention(qq.tolist(), K.tolist(), V.tolist(), mask,
+                                                 1 / math.sqrt(q.shape[-1])))[-1]
+            assert np.abs(out[f, t] - bf).max() < 1e-10
+
+
+def test_audio_single_face_single_token_is_v():
+    """one face token, one audio token, window 1 -> O == V exactly."""
+    q, k, v = _audio_inputs(frames=3, T=4, A=1)
+    out = oracle.audio_cross_attention(q, k, v, [2], window=1)
+    assert (out[:, 2] == v[:, 0]).all()
+
+
+def test_audio_locality():
+    """changing the audio of frame j changes frame i only if |i-j| <= 2."""
+    q, k, v = _audio_inputs(frames=9, seed=31)
+    base = oracle.audio_cross_attention(q, k, v, [0, 3, 5])
+    k2 = k.copy()
+    k2[4] += 1.0
+    out = oracle.audio_cross_attention(q, k2, v, [0, 3, 5])
+    changed = [f for f in range(9) if np.abs(out[f] - base[f]).max() > 0]
+    assert changed == [2, 3, 4, 5, 6]
+
+
+def test_audio_uniform_closed_form_with_edge_repetition():
+    """q = 0: O = mean over the window's audio tokens, counting a repeated
+    edge frame as often as it appears (frame 0 -> 3x frame 0 + frames 1, 2)."""
+    q, k, v = _audio_inputs(frames=4, T=2, A=2, seed=32)
+    out = oracle.audio_cross_attention(np.zeros_like(q), k, v, [0, 1])
+    expect0 = (3 * v[0].sum(0) + v[1].sum(0) + v[2].sum(0)) / 10.0
+    assert np.abs(out[0, 0] - expect0).max() < 1e-12
+
+
+def test_audio_empty_face_mask_is_error():
+    q, k, v = _audio_inputs()
+    with pytest.raises(oracle.OracleError):
+        oracle.audio_cross_attention(q, k, v, [])
