@@ -219,6 +219,72 @@ def reference_arm(args, c):
     print(json.dumps(out))
 
 
+# ----------------------------------------------------------------------------- Sec 8(f) rows
+
+def _time_ms(torch, fn, reps=10, warm=3):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    ev = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        ev.append((a, b))
+    torch.cuda.synchronize()
+    return statistics.median(x.elapsed_time(y) for x, y in ev)
+
+
+def measure_extras(tm, c, torch, stream):
+    """SURVEY Sec 8(f) rows at WAN shapes, random data: f1 full 21-frame window,
+    f2 fused sampler step (HBM roofline), f4 audio cross-attention."""
+    H, d = c["H"], c["d"]
+    bf = torch.bfloat16
+    g = torch.Generator(device="cuda").manual_seed(2506030990 + 77)
+    out = {}
+    # f1: 7 chunks x 3 latent frames of 1024 tokens (P:134-136)
+    lens = [3 * 1024] * 7
+    L = sum(lens)
+    q, k, v = (torch.randn(L, H, d, device="cuda", dtype=bf, generator=g) for _ in range(3))
+    o = torch.empty_like(q)
+    ca = tm.ChunkAttention(H, d, 16, 16, 1, 1)
+    ms = _time_ms(torch, lambda: ca.window(q, k, v, o, lens))
+    Lc = lens[0]
+    fl = 4.0 * d * H * Lc * Lc * (1 + 2 + 3 * 5)
+    out["f1_window"] = {"workload": "21-latent-frame window, 7 chunks x 3072 tokens, 40 heads",
+                        "ms": ms, "tflops": fl / (ms * 1e-3) / 1e12, "gflop": fl / 1e9}
+    del q, k, v, o
+    # f2: one sampler step over 64 chunks' latents (16 ch x 3 x 64 x 64 each)
+    n = 64 * 16 * 3 * 64 * 64
+    x = torch.randn(n, device="cuda", generator=g)
+    vv = torch.randn(n, device="cuda", generator=g).to(bf)
+    xb = torch.empty(n, device="cuda", dtype=bf)
+    ms = _time_ms(torch, lambda: tm.tm_flow_sampler_step(ca.ctx, x, vv, tm.TM_BF16, n, 0.0, 0.5,
+                                                          seed=1, x_bf16_out=xb))
+    byts = n * (4 + 4 + 2 + 2)        # x read + write, v bf16, bf16 copy; noise in-kernel
+    out["f2_sampler"] = {"workload": f"{n} elements (64 chunks of 16x3x64x64), in-kernel Philox",
+                         "ms": ms, "gbs": byts / (ms * 1e-3) / 1e9, "bytes": byts,
+                         "bound": "hbm"}
+    del x, vv, xb
+    # f4: a chunk of 3 frames, 16x16 face region, 32 audio tokens per frame
+    frames, T, A = 3, 1024, 32
+    qa = torch.randn(frames, T, H, d, device="cuda", dtype=bf, generator=g)
+    ka = torch.randn(frames, A, H, d, device="cuda", dtype=bf, generator=g)
+    va = torch.randn(frames, A, H, d, device="cuda", dtype=bf, generator=g)
+    oa = torch.empty_like(qa)
+    face = torch.tensor([r * 32 + cc for r in range(8, 24) for cc in range(8, 24)], dtype=torch.int32,
+                        device="cuda")
+    ms = _time_ms(torch, lambda: ca.audio(qa, ka, va, oa, face))
+    fl = 4.0 * frames * face.numel() * 5 * A * d * H
+    byts = (frames * T * H * d * 2) * 2 + 2 * frames * A * H * d * 2
+    out["f4_audio"] = {"workload": "3 latent frames x 1024 tokens, 256 face tokens, window 5 x 32 "
+                                   "audio tokens, 40 heads", "ms": ms,
+                       "tflops": fl / (ms * 1e-3) / 1e12, "gbs_io": byts / (ms * 1e-3) / 1e9}
+    ca.close()
+    return out
+
+
 # ----------------------------------------------------------------------------- tm arm
 
 def main():
@@ -232,6 +298,8 @@ def main():
     ap.add_argument("--oracle-rows", type=int, default=256)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the SURVEY Sec 8(f) rows (f1 window, f2 sampler, f4 audio)")
     ap.add_argument("--stream-chunks", type=int, default=4,
                     help="BJ.configs[3] streaming measurement over this many chunks (0: off)")
     args = ap.parse_args()
@@ -452,6 +520,10 @@ def main():
                      "tflops": NLs * NS * flop_per_call(c) / (s_ms * 1e-3) / 1e12}
         sc.close()
 
+    extras = None
+    if not args.no_extras and P == 1:
+        extras = measure_extras(tm, c, torch, stream)
+
     fl = flop_per_call(c)
     ms_step = ms_total / args.steps
     value = fl * args.steps / (ms_total * 1e-3) / 1e12
@@ -495,6 +567,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "streaming": streaming,
+            "next_rows": extras,
             "gpu_launches": gpu_launches,
             "clocks": clk,
         }
