@@ -111,6 +111,8 @@ __global__ void __launch_bounds__(256) sampler_kernel(float* __restrict__ x,
     const int64_t groups = (n + 3) / 4;
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
     const bool final_step = t_next >= 1.f;
+    const bool aligned = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(vv) |
+                           reinterpret_cast<uintptr_t>(xb)) & 15) == 0;
     for (int64_t gi = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; gi < groups; gi += stride) {
         float e[4] = {0.f, 0.f, 0.f, 0.f};
         if (!final_step) {
@@ -130,6 +132,35 @@ __global__ void __launch_bounds__(256) sampler_kernel(float* __restrict__ x,
                 sincospif(2.f * u3, &s1, &c1);
                 e[0] = r0 * c0; e[1] = r0 * s0; e[2] = r1 * c1; e[3] = r1 * s1;
             }
+        }
+        const int64_t i0 = 4 * gi;
+        if (i0 + 4 <= n && aligned) {            // vector path: 16 B x, 8 / 16 B v, 8 B bf16 out
+            const float4 xv = reinterpret_cast<const float4*>(x)[gi];
+            float vf[4];
+            if constexpr (kBf16V) {
+                const uint2 w = reinterpret_cast<const uint2*>(vv)[gi];
+                vf[0] = __uint_as_float(w.x << 16); vf[1] = __uint_as_float(w.x & 0xffff0000u);
+                vf[2] = __uint_as_float(w.y << 16); vf[3] = __uint_as_float(w.y & 0xffff0000u);
+            } else {
+                const float4 w = reinterpret_cast<const float4*>(vv)[gi];
+                vf[0] = w.x; vf[1] = w.y; vf[2] = w.z; vf[3] = w.w;
+            }
+            const float xs[4] = {xv.x, xv.y, xv.z, xv.w};
+            float xn[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const float x1 = __fmaf_rn(1.f - t_cur, vf[j], xs[j]);
+                xn[j] = final_step ? x1 : __fmaf_rn(t_next, x1, (1.f - t_next) * e[j]);
+            }
+            reinterpret_cast<float4*>(x)[gi] = make_float4(xn[0], xn[1], xn[2], xn[3]);
+            if (xb) {
+                const uint32_t lo = uint32_t(__bfloat16_as_ushort(__float2bfloat16_rn(xn[0]))) |
+                                    (uint32_t(__bfloat16_as_ushort(__float2bfloat16_rn(xn[1]))) << 16);
+                const uint32_t hi = uint32_t(__bfloat16_as_ushort(__float2bfloat16_rn(xn[2]))) |
+                                    (uint32_t(__bfloat16_as_ushort(__float2bfloat16_rn(xn[3]))) << 16);
+                reinterpret_cast<uint2*>(xb)[gi] = make_uint2(lo, hi);
+            }
+            continue;
         }
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
