@@ -266,6 +266,11 @@ def measure_extras(tm, c, torch, stream):
     out["f2_sampler"] = {"workload": f"{n} elements (64 chunks of 16x3x64x64), in-kernel Philox",
                          "ms": ms, "gbs": byts / (ms * 1e-3) / 1e9, "bytes": byts,
                          "bound": "hbm"}
+    # a7 at the same size (report GB/s at n = 12.6 M)
+    ms = _time_ms(torch, lambda: tm.tm_flow_euler_step(ca.ctx, x, vv, tm.TM_BF16, n, 0.5))
+    byts = n * (4 + 4 + 2)
+    out["a7_euler_12.6M"] = {"ms": ms, "gbs": byts / (ms * 1e-3) / 1e9, "bytes": byts,
+                             "bound": "hbm"}
     del x, vv, xb
     # f4: a chunk of 3 frames, 16x16 face region, 32 audio tokens per frame
     frames, T, A = 3, 1024, 32

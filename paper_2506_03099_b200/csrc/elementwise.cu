@@ -240,7 +240,7 @@ cudaError_t launch_shuffle(const void* src, void* dst, int B, int64_t Ls, int64_
 cudaError_t launch_euler(float* x, const void* v, int v_is_bf16, int64_t n, float dt,
                          cudaStream_t s, int* launches) {
     if (n <= 0) return cudaSuccess;
-    const unsigned grid = grid_for((n + 7) / 8, 256, 4);
+    const unsigned grid = grid_for((n + 7) / 8, 256, 16);
     if (v_is_bf16)
         euler_kernel<true><<<grid, 256, 0, s>>>(x, v, n, dt);
     else
@@ -253,7 +253,7 @@ cudaError_t launch_sampler(float* x, const void* v, int v_is_bf16, const float* 
                            float t_cur, float t_next, uint64_t seed, uint64_t offset,
                            void* x_bf16, cudaStream_t s, int* launches) {
     if (n <= 0) return cudaSuccess;
-    const unsigned grid = grid_for((n + 3) / 4, 256, 4);
+    const unsigned grid = grid_for((n + 3) / 4, 256, 16);
     const uint2 sd = make_uint2(uint32_t(seed), uint32_t(seed >> 32));
     const uint2 of = make_uint2(uint32_t(offset), uint32_t(offset >> 32));
     uint16_t* xb = static_cast<uint16_t*>(x_bf16);
