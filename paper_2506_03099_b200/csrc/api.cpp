@@ -281,7 +281,7 @@ tm_status tm_attn_init(const tm_config* cfg, const uint8_t* nccl_id, void* cache
     const char* dbg = getenv("TM_DEBUG");
     c->debug = dbg && *dbg && strcmp(dbg, "0") != 0;
     if (const char* tp = getenv("TM_TRACE")) {
-        if (*tp && cudaMalloc(&c->trace, 4 * 4096 * 8) == cudaSuccess) c->trace_path = tp;
+        if (*tp && cudaMalloc(&c->trace, 13 * 4096 * 8) == cudaSuccess) c->trace_path = tp;
     }
     if (L.exchange) {
         const char* e = comm_init(&c->comm, cfg->world_size, cfg->rank, nccl_id);
@@ -447,13 +447,13 @@ tm_status tm_chunk_attention(tm_ctx* ctx, int32_t layer, int32_t step, int64_t c
         pr.seg[pr.nseg++] = Segment{kslot, vslot, Ly.Lc};
     }
 
-    if (ctx->trace) cudaMemsetAsync(ctx->trace, 0, 4 * 4096 * 8, cs);
+    if (ctx->trace) cudaMemsetAsync(ctx->trace, 0, 13 * 4096 * 8, cs);
     cudaError_t e = cf.dtype == TM_BF16 ? launch_fmha_sm100(pr, ctx->scratch(), cs, &ctx->launches, ctx->trace)
                                         : launch_fmha_fp32(pr, cs, &ctx->launches);
     st = cuda_check(e, "attention kernel launch");
     if (st) return st;
     if (ctx->trace) {   // debug only: dump CTA 0's timeline (synchronises)
-        std::vector<unsigned long long> h(4 * 4096);
+        std::vector<unsigned long long> h(13 * 4096);
         cudaMemcpyAsync(h.data(), ctx->trace, h.size() * 8, cudaMemcpyDeviceToHost, cs);
         cudaStreamSynchronize(cs);
         if (FILE* f = fopen(ctx->trace_path.c_str(), "ab")) {

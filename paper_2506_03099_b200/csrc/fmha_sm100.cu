@@ -14,26 +14,27 @@
 // into S = C/T pieces so the last wave fills the machine (split-KV tail);
 // the last piece of a unit to finish merges the pieces' (O, m, l) in fixed
 // piece order (deterministic, no floating-point atomics).
-// Warp roles (384 threads; setmaxnreg gives the softmax warpgroups 232 regs):
-//   warp 8      TMA producer: Q_i per unit (reloaded per tile as soon as its
-//               last S MMA completes), K_j / V_j through a 4-slot smem ring
-//               (cp.async.bulk.tensor, 128B swizzle).
-//   warp 9      tcgen05 MMA issuer (one thread) + TMEM owner:
-//                 S_i = Q_i K_j^T  (SS, M=128 N=128 K=d, fp32 in TMEM)
-//                 O_i += P_i V_j   (TS: P_i bf16 read from TMEM, V MN-major)
-//               issue order S0_j, PV0_{j-1}, S1_j, PV1_{j-1} into ONE shared S
-//               buffer and separate P_i columns, so S_i(j) is computed while
-//               softmax_i is still on tile j-1 (the softmax never waits for
-//               its own PV + S round trip).
+// Warp roles (384 threads; setmaxnreg gives the softmax warpgroups 216 regs):
+//   warp 8      TMA producer: Q_i per unit, K_j / V_j through a 5-slot smem
+//               ring in the order K0, K1, V0, K2, V1, ... (K one tile ahead of
+//               V; cp.async.bulk.tensor, 128B swizzle).
+//   warp 9      S issuer + TMEM owner: S_i(j) = Q_i K_j^T (SS, M=128 N=128
+//               K=d, fp32) into ONE S buffer shared by both Q tiles, refilled
+//               as soon as the previous S is in registers (s_free).
+//   warp 11     PV issuer: O_i += P_i(j) V_j (TS: P_i bf16 from TMEM, V
+//               MN-major).  Independent of warp 9 (a blocked PV issue never
+//               delays the next S); each commits only its own MMAs.
+//   warp 10     a3 append: TMA-stores the current chunk's K/V tiles from the
+//               ring to the cache slot.
 //   warps 0-7   softmax, one warpgroup per Q tile, one thread per query row
 //               (tcgen05.ld 32x32b puts a whole S row in one thread's
-//               registers): 3-input-max tree, exp2 with scale*log2(e) folded
-//               into one packed FFMA2, exponentials on the MUFU pipe (a
-//               degree-3 polynomial on the FMA pipe for a selectable share,
-//               TM_POLY; off by default: power-capped, see profiles/README.md), packed FADD2 row
-//               sums, conditional O rescale (only when the running max grows
-//               by > 8 in log2 units -- exact after the final 1/l), P rounded
-//               to bf16 (RNE) and stored back into TMEM over S_i; epilogue
+//               registers): exact tile max (3-input max tree), running max
+//               moved only when it grows by > 8 in log2 units (O and l
+//               rescaled then; exact after the final 1/l), exp2 with
+//               scale*log2(e) folded into one packed FFMA2, exponentials on the
+//               MUFU pipe with a share on an FMA-pipe polynomial (kPolyMask),
+//               packed FADD2 row sums, P rounded to bf16 (RNE) and held in
+//               registers until the previous PV_i has consumed P_i; epilogue
 //               O/l -> bf16 (or the unnormalised partial for split pieces).
 // TMEM: S [0,128) (shared), P0 [128,192) P1 [192,256), O0 [256,256+d) O1 [256+d,256+2d).
 #include <cuda.h>
@@ -57,14 +58,16 @@ constexpr int kBM = 128;          // query rows per Q tile
 constexpr int kBN = 128;          // keys per KV tile
 constexpr int kStages = 5;        // K/V smem ring slots (Q 64 KB + 5 x 32 KB fits in 227 KB)
 constexpr int kThreads = 384;     // 2 softmax warpgroups + {TMA, MMA, 2 spare} warpgroup
-constexpr int kRegsSoftmax = 208; // setmaxnreg budgets (see the static_assert)
-constexpr int kRegsOther = 88;
+constexpr int kRegsSoftmax = 216; // setmaxnreg budgets (see the static_assert)
+constexpr int kRegsOther = 72;
 // The CTA launches with 168 regs/thread (64K / 384 rounded down to 8); setmaxnreg
 // only redistributes that pool, so the budgets must fit in 384 x 168.
 static_assert(256 * kRegsSoftmax + 128 * kRegsOther <= kThreads * 168, "register pool");
 constexpr int kHalfBytes = 128 * 128;   // one 64-column (128 B) half of a 128-row tile
 // TMEM columns: one S buffer shared by both Q tiles, P0/P1 (bf16 pairs), O0/O1.
 constexpr uint32_t kColS = 0, kColP = 128, kColO = 256;
+// Lazy running-max threshold (log2 units): weights stay <= 2^8 between rescales.
+constexpr float kLazyLog2 = 8.f;
 
 struct __align__(64) FmhaParams {
     CUtensorMap tq;                   // Q [B][Lq][H][d]
@@ -90,7 +93,7 @@ struct __align__(64) FmhaParams {
     unsigned long long* trace;        // debug timeline (TM_TRACE=1), CTA 0 only; may be null
 };
 
-// Debug timeline: role r in [0,4) owns trace[r*kTraceCap ..]; entry =
+// Debug timeline: role r in [0,13) owns trace[r*kTraceCap ..]; entry =
 // clock64() << 8 | event code.  Only CTA 0 records; off when p.trace == 0.
 constexpr int kTraceCap = 4096;
 // Compiled in only with -DTM_TRACE_ENABLED (TM_TRACE_BUILD=1 python -m
@@ -300,11 +303,13 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                     int seg, row, valid;
                     tile_info(p, it.lo + jj, seg, row, valid);
                     const int s = kv_it % kStages;
+                    trace_ev(p, 0, tn, 3 + kv);
                     mbar_wait(&kv_empty[s], ((kv_it / kStages) & 1) ^ 1);
                     if ((pending_store >> s) & 1) {       // previous occupant being appended
                         mbar_wait(&store_done[s], (store_par >> s) & 1);
                         store_par ^= 1u << s;
                         pending_store &= ~(1u << s);
+                        trace_ev(p, 0, tn, 5);
                     }
                     if (stores_tile(p, it, seg, row)) pending_store |= 1u << s;
                     trace_ev(p, 0, tn, 1 + kv);
@@ -317,9 +322,29 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
             }
         }
       } else if (warp == 10) {
+#ifdef TM_TRACE_ENABLED
+        if (lane == 1) {
+        // ------------------------------------------------ trace observer (debug build)
+        // Records when each S MMA group lands (30+i = S_i(j) complete).  Only
+        // s_full is observed: its phases are strictly ordered S0(j), S1(j),
+        // S0(j+1) by the shared S buffer, so a lagging observer cannot alias.
+        if (p.trace != nullptr && blockIdx.x == 0) {
+            int tn = 0;
+            uint32_t g = 0;
+            Item it;
+            for (int w = blockIdx.x; get_item(p, w, it); w += gridDim.x)
+                for (int j = it.lo; j < it.hi; ++j, ++g)
+                    for (int i = 0; i < 2; ++i) {
+                        mbar_wait(&s_full[i], g & 1);
+                        trace_ev(p, 4, tn, 30 + i);
+                    }
+        }
+        }
+#endif
         // ------------------------------------------------ a3 append: TMA store of c_t tiles
         if (lane == 0 && p.store_seg >= 0) {
             uint32_t kv_it = 0;
+            int tn = 0;
             Item it;
             for (int w = blockIdx.x; get_item(p, w, it); w += gridDim.x) {
                 const int nkv = it.hi - it.lo;
@@ -332,6 +357,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                     // stored tiles could run two phases ahead on a slot (parity ABA).
                     const int s = kv_it % kStages;
                     mbar_wait(&kv_full[s], (kv_it / kStages) & 1);
+                    trace_ev(p, 2, tn, 40 + kv);
                     if (!stores_tile(p, it, seg, row)) continue;
                     fence_proxy_async_smem();
                     const CUtensorMap* m = kv ? &p.tv_store : &p.tk_store;
@@ -344,46 +370,30 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                 }
             }
         }
-      } else if (warp == 9) {
-        // ------------------------------------------------ MMA issuer
-        {   // the whole warp runs the loop (uniform operands live in uniform
-            // registers); one elected lane issues each tcgen05 instruction.
-            const uint64_t dq = make_sdesc_sw128(smem_u32(sQ), 16, 1024);
-            const uint64_t dk = make_sdesc_sw128(smem_u32(sKV), 16, 1024);
-            const uint64_t dv = make_sdesc_sw128(smem_u32(sKV), kHalfBytes, 1024);
-            constexpr uint32_t kTile16 = kTileBytes >> 4;      // descriptor address units
-            auto issue_s = [&](int i, int slot) {      // S = Q_i K^T into the S buffer
-                const uint64_t a0 = dq + i * kTile16, b0 = dk + slot * kTile16;
-#pragma unroll
-                for (int kk = 0; kk < D / 16; ++kk) {
-                    const uint32_t off = (kk >> 2) * (kHalfBytes >> 4) + (kk & 3) * 2;
-                    mma_ss_w(tmem + kColS, a0 + off, b0 + off, kIdescS, kk > 0);
-                }
-            };
-            auto issue_pv = [&](int i, int slot, bool acc) {   // O_i += P_i V
-                const uint64_t b0 = dv + slot * kTile16;
-#pragma unroll
-                for (int kk = 0; kk < kBN / 16; ++kk)
-                    mma_ts_w(tmem + kColO + i * D, tmem + kColP + i * 64 + kk * 8, b0 + kk * 128,
-                             kIdescO, (acc || kk > 0) ? 1u : 0u);
-            };
-            // Issue order per KV tile j: S0(j), PV0(j-1), S1(j), PV1(j-1).  P_i has
-            // its own TMEM columns, so S_i(j) is computed while softmax_i still
-            // works on tile j-1; the single S buffer is refilled as soon as the
-            // previous S has been loaded into registers (s_free).
-            uint32_t kv_it = 0, g = 0, n_item = 0, s_count = 0;
-            int tn = 0;
-            Item it;
-            for (int w = blockIdx.x; get_item(p, w, it); w += gridDim.x, ++n_item) {
-                const int nkv = it.hi - it.lo;
-                // ring positions (see the producer's load order)
-                auto kpos = [&](int j) -> uint32_t { return kv_it + (j == 0 ? 0 : 2 * j - 1); };
-                auto vpos = [&](int j) -> uint32_t {
-                    return kv_it + (j == nkv - 1 ? 2 * nkv - 1 : 2 * j + 2);
-                };
+      } else if (warp == 9 || warp == 11) {
+        // ------------------------------------------------ MMA issuers
+        // Two independent issuers so that neither waits behind the other:
+        //   warp 9   S_i(j) = Q_i K_j^T into the shared S buffer, i = 0, 1, gated
+        //            by K_j landing and s_free (previous S loaded by a softmax WG);
+        //   warp 11  O_i += P_i(j) V_j, gated by V_j landing and p_full_i.
+        // They touch disjoint TMEM (S vs P_i / O_i) and each commits only its
+        // own MMAs (tcgen05.commit tracks the issuing thread's operations).
+        // A tcgen05.mma issue blocks while the tensor pipe's queue is full, so a
+        // single issuer held every S behind the PV issued before it.
+        // The whole warp runs its loop; one elected lane issues each group.
+        const uint64_t dq = make_sdesc_sw128(smem_u32(sQ), 16, 1024);
+        const uint64_t dk = make_sdesc_sw128(smem_u32(sKV), 16, 1024);
+        const uint64_t dv = make_sdesc_sw128(smem_u32(sKV), kHalfBytes, 1024);
+        constexpr uint32_t kTile16 = kTileBytes >> 4;      // descriptor address units
+        uint32_t kv_it = 0, g = 0, n_item = 0, s_count = 0;
+        int tn = 0;
+        Item it;
+        for (int w = blockIdx.x; get_item(p, w, it); w += gridDim.x, ++n_item) {
+            const int nkv = it.hi - it.lo;
+            if (warp == 9) {
                 for (int j = 0; j < nkv; ++j) {
-                    const uint32_t ik = kpos(j), sk = ik % kStages;
-                    const uint32_t iv = vpos(j - 1), sv = iv % kStages;
+                    // ring position of K_j (producer's order K0, K1, V0, K2, V1, ...)
+                    const uint32_t ik = kv_it + (j == 0 ? 0 : 2 * j - 1), sk = ik % kStages;
                     mbar_wait(&kv_full[sk], (ik / kStages) & 1);
                     if (lane == 0) trace_ev(p, 1, tn, 10);
                     for (int i = 0; i < 2; ++i) {
@@ -391,38 +401,35 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                         if (j == 0) mbar_wait(&q_full[i], n_item & 1);
                         if (lane == 0) trace_ev(p, 1, tn, 15 + i);
                         tc_fence_after();
-                        issue_s(i, sk);
+                        static_assert(kHalfBytes >> 4 == 1024, "S k-step offsets in mma_ss_group");
+                        mma_ss_group<D / 16>(tmem + kColS, dq + i * kTile16, dk + sk * kTile16, kIdescS);
                         mma_commit_w(&s_full[i]);
                         ++s_count;
                         if (lane == 0) trace_ev(p, 1, tn, 13 + i);
                         if (j == nkv - 1) mma_commit_w(&q_empty[i]);
-                        if (j > 0) {
-                            if (i == 0) mbar_wait(&kv_full[sv], (iv / kStages) & 1);
-                            mbar_wait(&p_full[i], (g + j - 1) & 1);
-                            if (j == 1 && n_item > 0) mbar_wait(&o_empty[i], (n_item - 1) & 1);
-                            if (lane == 0) trace_ev(p, 1, tn, 11 + i);
-                            tc_fence_after();
-                            issue_pv(i, sv, j - 1 > 0);
-                            mma_commit_w(&o_done[i]);
-                        }
                     }
-                    mma_commit_w(&kv_empty[sk]);
-                    if (j > 0) mma_commit_w(&kv_empty[sv]);
+                    mma_commit_w(&kv_empty[sk]);   // K_j free once S_0(j), S_1(j) complete
                 }
-                const uint32_t iv = vpos(nkv - 1), sv = iv % kStages;
-                mbar_wait(&kv_full[sv], (iv / kStages) & 1);
-                for (int i = 0; i < 2; ++i) {
-                    mbar_wait(&p_full[i], (g + nkv - 1) & 1);
-                    if (nkv == 1 && n_item > 0) mbar_wait(&o_empty[i], (n_item - 1) & 1);
-                    tc_fence_after();
-                    issue_pv(i, sv, nkv - 1 > 0);
-                    mma_commit_w(&o_done[i]);
-                    mma_commit_w(&o_final[i]);
+            } else {
+                for (int j = 0; j < nkv; ++j) {
+                    const uint32_t iv = kv_it + (j == nkv - 1 ? 2 * nkv - 1 : 2 * j + 2), sv = iv % kStages;
+                    mbar_wait(&kv_full[sv], (iv / kStages) & 1);
+                    for (int i = 0; i < 2; ++i) {
+                        mbar_wait(&p_full[i], (g + j) & 1);
+                        if (j == 0 && n_item > 0) mbar_wait(&o_empty[i], (n_item - 1) & 1);
+                        if (lane == 0) trace_ev(p, 3, tn, 11 + i);
+                        tc_fence_after();
+                        static_assert(kBN == 128 && kHalfBytes == 16384, "PV k-step offsets in mma_ts_group8");
+                        mma_ts_group8(tmem + kColO + i * D, tmem + kColP + i * 64, dv + sv * kTile16,
+                                      kIdescO, j > 0 ? 1u : 0u);
+                        mma_commit_w(&o_done[i]);
+                        if (j == nkv - 1) mma_commit_w(&o_final[i]);
+                    }
+                    mma_commit_w(&kv_empty[sv]);   // V_j free once PV_0(j), PV_1(j) complete
                 }
-                mma_commit_w(&kv_empty[sv]);
-                kv_it += 2 * nkv;
-                g += nkv;
             }
+            kv_it += 2 * nkv;
+            g += nkv;
         }
       }
     } else {
@@ -437,7 +444,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
         const float sl2 = p.scale_log2;
         uint32_t g = 0, n_item = 0;
         int tn = 0;
-        const bool tr = (wq == 0 && lane == 0);
+        const bool tr = (lane == 0);   // every softmax warp records (equal trace overhead)
         Item it;
         for (int w = blockIdx.x; get_item(p, w, it); w += gridDim.x, ++n_item) {
             float m_run = -INFINITY, l = 0.f;
@@ -446,25 +453,23 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                 tile_info(p, j, seg, row, valid);
                 uint32_t r[kBN];
                 mbar_wait(&s_full[i], g & 1);
-                if (tr) trace_ev(p, 2 + i, tn, 20);
+                if (tr) trace_ev(p, 5 + warp, tn, 20);
                 tc_fence_after();
 #pragma unroll
                 for (int c = 0; c < kBN; c += 32) tmem_ld32(tS + c, r + c);
                 tmem_wait_ld();
                 tc_fence_before();
                 mbar_arrive(s_free);          // the S buffer may be refilled
-                if (tr) trace_ev(p, 2 + i, tn, 21);
+                if (tr) trace_ev(p, 5 + warp, tn, 21);
                 if (valid < kBN) {
 #pragma unroll
                     for (int c = 0; c < kBN; ++c)
                         if (c >= valid) r[c] = 0xff800000u;   // -inf: key beyond the segment
                 }
-                // exps of the row against the running max m_run: P -> TMEM (bf16,
-                // P_i columns), returns the row sum of this tile.  kPolyMask pairs
-                // of every 16 use the FMA-pipe polynomial, interleaved with MUFU.
-                // Before the first store into P_i, the previous PV_i (which reads
-                // P_i) must be complete: waited on o_done only then, so the wait
-                // overlaps the first chunk's exps.
+                // The previous PV_i reads P_i: it must be complete before P_i is
+                // overwritten.  Waited on only once this tile's exps are done (P is
+                // held packed in registers meanwhile), so a late PV never stalls
+                // the exponentials.
                 bool pv_waited = (g == 0);
                 auto wait_prev_pv = [&]() {
                     if (!pv_waited) {
@@ -473,39 +478,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                         pv_waited = true;
                     }
                 };
-                auto exps = [&](float mrun) -> float {
-                    const float nm = (mrun == -INFINITY) ? 0.f : -mrun;
-                    const float2 sc2 = make_float2(sl2, sl2), nm2 = make_float2(nm, nm);
-                    float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f),
-                                     make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) {
-                        uint32_t pk[16];
-#pragma unroll
-                        for (int e = 0; e < 16; ++e) {
-                            const float2 x = ffma2(make_float2(__uint_as_float(r[32 * c + 2 * e]),
-                                                               __uint_as_float(r[32 * c + 2 * e + 1])),
-                                                   sc2, nm2);
-                            float2 pe;
-                            if ((kPolyMask >> e) & 1) {
-                                pe = exp2_poly2(x);
-                            } else {
-                                pe.x = ex2(x.x);
-                                pe.y = ex2(x.y);
-                            }
-                            acc[e & 3] = fadd2(acc[e & 3], pe);
-                            pk[e] = pack_bf16x2(pe.x, pe.y);
-                        }
-                        if (c == 0) {
-                            wait_prev_pv();
-                            if (tr) trace_ev(p, 2 + i, tn, 25);
-                        }
-                        tmem_st16(tPi + c * 16, pk);
-                    }
-                    const float2 s01 = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
-                    return s01.x + s01.y;
-                };
-                auto row_max = [&]() -> float {   // 3-input max tree (depth 5)
+                auto row_max = [&]() -> float {   // 3-input max tree (depth 5), ALU pipe
                     float t1[43];
 #pragma unroll
                     for (int k = 0; k < 42; ++k)
@@ -521,39 +494,70 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                     for (int k = 0; k < 5; ++k) t3[k] = max3(t2[3 * k], t2[3 * k + 1], t2[3 * k + 2]);
                     return max3(max3(t3[0], t3[1], t3[2]), t3[3], t3[4]);
                 };
-                // Lazy running max: the first tile of an item sets m_run to its
-                // exact row max; later tiles reuse m_run and only fall back
-                // (exact max, O rescale, recompute) when some weight would
-                // exceed ~2^24 -- the result is exact either way after O / l.
-                if (j == it.lo) m_run = row_max() * sl2;
-                if (tr) trace_ev(p, 2 + i, tn, 22);
-                float tsum = exps(m_run);
-                const bool bad = !(tsum <= 16777216.f);      // also catches inf / nan
-                if (__any_sync(0xffffffffu, bad)) {
-                    const float m_new = fmaxf(m_run, row_max() * sl2);
-                    const float alpha = ex2(m_run - m_new);
+                // Running max with a lazy threshold: m_run (log2 units) moves only
+                // when this tile's exact max exceeds it by more than kLazyLog2, so
+                // every weight is <= 2^kLazyLog2 and nothing is ever recomputed.
+                // O_i and l are rescaled by 2^(m_old - m_new) when it moves (exact
+                // after the final O / l either way).
+                const float mt = row_max() * sl2;
+                const bool grow = mt > m_run + kLazyLog2;      // always on an item's first tile
+                if (__any_sync(0xffffffffu, grow)) {
+                    const float m_new = grow ? mt : m_run;
+                    const float alpha = grow ? ex2(m_run - m_new) : 1.f;   // 0 on the first tile
                     m_run = m_new;
                     l *= alpha;
-                    // O_i was last written by PV_i(j-1): complete (o_done waited).
-                    wait_prev_pv();
+                    if (j != it.lo) {   // O_i holds PV_i(it.lo .. j-1): complete first
+                        wait_prev_pv();
 #pragma unroll
-                    for (int c = 0; c < D; c += 32) {
-                        uint32_t o[32];
-                        tmem_ld32(tOi + c, o);
-                        tmem_wait_ld();
+                        for (int c = 0; c < D; c += 16) {
+                            uint32_t o[16];
+                            tmem_ld16(tOi + c, o);
+                            tmem_wait_ld();
 #pragma unroll
-                        for (int e = 0; e < 32; ++e)
-                            o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-                        tmem_st32(tOi + c, o);
+                            for (int e = 0; e < 16; ++e)
+                                o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+                            tmem_st16(tOi + c, o);
+                        }
                     }
-                    tsum = exps(m_run);
                 }
+                if (tr) trace_ev(p, 5 + warp, tn, 22);
+                // p = 2^(s * scale * log2 e - m_run), kPolyMask pairs of every 16 on
+                // the FMA-pipe polynomial; row sum in fp32, P rounded to bf16 (RNE).
+                uint32_t pk[kBN / 2];
+                float tsum;
+                {
+                    const float nm = (m_run == -INFINITY) ? 0.f : -m_run;
+                    const float2 sc2 = make_float2(sl2, sl2), nm2 = make_float2(nm, nm);
+                    float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                                     make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+                    for (int e = 0; e < kBN / 2; ++e) {
+                        const float2 x = ffma2(make_float2(__uint_as_float(r[2 * e]),
+                                                           __uint_as_float(r[2 * e + 1])),
+                                               sc2, nm2);
+                        float2 pe;
+                        if ((kPolyMask >> (e & 15)) & 1) {
+                            pe = exp2_poly2(x);
+                        } else {
+                            pe.x = ex2(x.x);
+                            pe.y = ex2(x.y);
+                        }
+                        acc[e & 3] = fadd2(acc[e & 3], pe);
+                        pk[e] = pack_bf16x2(pe.x, pe.y);
+                    }
+                    const float2 s01 = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
+                    tsum = s01.x + s01.y;
+                }
+                wait_prev_pv();
+                if (tr) trace_ev(p, 5 + warp, tn, 25);
+#pragma unroll
+                for (int c = 0; c < 4; ++c) tmem_st16(tPi + c * 16, pk + c * 16);
                 l += tsum;
-                if (tr) trace_ev(p, 2 + i, tn, 23);
+                if (tr) trace_ev(p, 5 + warp, tn, 23);
                 tmem_wait_st();
                 tc_fence_before();
                 mbar_arrive(&p_full[i]);
-                if (tr) trace_ev(p, 2 + i, tn, 24);
+                if (tr) trace_ev(p, 5 + warp, tn, 24);
             }
             // ------------------------------------------------ epilogue
             mbar_wait(&o_final[i], n_item & 1);
@@ -725,6 +729,8 @@ cudaError_t launch_d(const FmhaParams& p, int grid, cudaStream_t stream) {
         return e ? atoi(e) : 0;
     }();
     switch (sel) {
+        case 2: return launch_t<D, 0x0808u>(p, grid, stream);   // {3,11}
+        case 3: return launch_t<D, 0x1084u>(p, grid, stream);   // {2,7,12}
         case 4: return launch_t<D, 0x4444u>(p, grid, stream);   // {2,6,10,14}
         case 7: return launch_t<D, 0xA54Au>(p, grid, stream);   // {1,3,6,8,10,13,15}
         case 5: return launch_t<D, 0x2492u>(p, grid, stream);   // {1,4,7,10,13}

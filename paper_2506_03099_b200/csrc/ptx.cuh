@@ -140,6 +140,59 @@ __device__ __forceinline__ void mma_ts_w(uint32_t d_tmem, uint32_t a_tmem, uint6
         "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+// A whole K loop of MMAs in ONE asm block with one elect.sync: the MMA warp
+// shares its SM sub-partition with two MUFU-bound softmax warps, so every
+// instruction in the issue path costs issue slots (per-MMA elect/vote/R2UR
+// sequences measured ~47 cycles per MMA in the kernel).
+//   S:  K-major SW128 A and B, k-step = 32 B within a 64-column half, halves
+//       16 KB apart (descriptor units: +2 per step, +1024 per half); NK = D/16.
+//   PV: A = P in TMEM (+8 columns per 16 keys), B = V MN-major (+2048 B per step).
+#define TM_SS_STEP(OFF)                                            \
+    "add.s64 a, %1, " #OFF ";\n\tadd.s64 b, %2, " #OFF ";\n\t"      \
+    "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n\t"
+template <int NK>
+__device__ __forceinline__ void mma_ss_group(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                             uint32_t idesc) {
+    static_assert(NK == 4 || NK == 8, "k steps");
+    if constexpr (NK == 8) {
+        asm volatile(
+            "{\n\t.reg .pred e, f, t;\n\t.reg .b32 r;\n\t.reg .b64 a, b;\n\t"
+            "elect.sync r|e, 0xffffffff;\n\t"
+            "setp.ne.b32 f, 0, 0;\n\tsetp.eq.b32 t, 0, 0;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, f;\n\t"
+            TM_SS_STEP(2) TM_SS_STEP(4) TM_SS_STEP(6) TM_SS_STEP(1024) TM_SS_STEP(1026)
+            TM_SS_STEP(1028) TM_SS_STEP(1030) "}" ::"r"(d_tmem),
+            "l"(adesc), "l"(bdesc), "r"(idesc)
+            : "memory");
+    } else {
+        asm volatile(
+            "{\n\t.reg .pred e, f, t;\n\t.reg .b32 r;\n\t.reg .b64 a, b;\n\t"
+            "elect.sync r|e, 0xffffffff;\n\t"
+            "setp.ne.b32 f, 0, 0;\n\tsetp.eq.b32 t, 0, 0;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, f;\n\t"
+            TM_SS_STEP(2) TM_SS_STEP(4) TM_SS_STEP(6) "}" ::"r"(d_tmem),
+            "l"(adesc), "l"(bdesc), "r"(idesc)
+            : "memory");
+    }
+}
+#undef TM_SS_STEP
+#define TM_TS_STEP(AOFF, BOFF)                                         \
+    "add.u32 ta, %1, " #AOFF ";\n\tadd.s64 b, %2, " #BOFF ";\n\t"       \
+    "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], b, %3, t;\n\t"
+// 8 steps over 128 keys; the first accumulates into D only if `accumulate`.
+__device__ __forceinline__ void mma_ts_group8(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc,
+                                              uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred e, f, t;\n\t.reg .b32 r, ta;\n\t.reg .b64 b;\n\t"
+        "elect.sync r|e, 0xffffffff;\n\t"
+        "setp.ne.b32 f, %4, 0;\n\tsetp.eq.b32 t, 0, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, f;\n\t"
+        TM_TS_STEP(8, 128) TM_TS_STEP(16, 256) TM_TS_STEP(24, 384) TM_TS_STEP(32, 512)
+        TM_TS_STEP(40, 640) TM_TS_STEP(48, 768) TM_TS_STEP(56, 896) "}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+#undef TM_TS_STEP
 __device__ __forceinline__ void mma_commit_w(uint64_t* bar) {
     asm volatile(
         "{\n\t.reg .pred e;\n\t.reg .b32 r;\n\t"
@@ -174,6 +227,13 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* r) {
         "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
         "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
         : TM_R8(0), TM_R8(8), TM_R8(16), TM_R8(24)
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* r) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : TM_R8(0), TM_R8(8)
         : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* r) {

@@ -11,7 +11,8 @@ import ctypes
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libtm.so")
+# TM_LIB_PATH: A/B tuning of an alternative in-tree build (tools/); default libtm.so
+LIB_PATH = os.environ.get("TM_LIB_PATH") or os.path.join(_PKG, "libtm.so")
 
 TM_OK = 0
 STATUS = {0: "TM_OK", 1: "TM_ERR_INVALID_ARG", 2: "TM_ERR_SHAPE", 3: "TM_ERR_DEGENERATE_MASK",
