@@ -717,11 +717,14 @@ cudaError_t launch_t(const FmhaParams& p, int grid, cudaStream_t stream) {
 }
 
 // Which of every 16 exp2 pairs run as the FMA-pipe polynomial (bit e set) --
-// the MUFU/FMA balance.  Default: all MUFU -- with real data the kernel is
-// power-capped and the polynomial's extra FMA-pipe work costs more energy than
-// the MUFU time it saves (sweep on random data: 1282 vs 1271 TFLOP/s at 512^2,
-// 1187 vs 1147 at 720^2; on zero data 4/16 was ahead).
-constexpr uint32_t kPolyDefault = 0x0000u;
+// the MUFU/FMA balance.  At d = 128 the MUFU exp rate (16/clk/SM) equals the
+// tensor rate in score elements, so some offload gives the softmax slack; more
+// polynomial costs FMA/ALU issue and energy (the kernel is power-capped when
+// sustained).  Measured (random data, independent S/PV issuers, exact tile max):
+// 2/16 vs all-MUFU 1382 vs 1363 TFLOP/s burst, 1172 vs 1156 sustained;
+// 3/16 = 2/16, 4/16 and more slower (profiles/README.md).  TM_POLY selects
+// another split for tuning: 1 = all MUFU, 3 = 3/16, 4 = 4/16.
+constexpr uint32_t kPolyDefault = 0x0808u;   // pairs {3, 11} of every 16
 template <int D>
 cudaError_t launch_d(const FmhaParams& p, int grid, cudaStream_t stream) {
     static int sel = [] {
@@ -729,13 +732,9 @@ cudaError_t launch_d(const FmhaParams& p, int grid, cudaStream_t stream) {
         return e ? atoi(e) : 0;
     }();
     switch (sel) {
-        case 2: return launch_t<D, 0x0808u>(p, grid, stream);   // {3,11}
+        case 1: return launch_t<D, 0x0000u>(p, grid, stream);   // all MUFU
         case 3: return launch_t<D, 0x1084u>(p, grid, stream);   // {2,7,12}
         case 4: return launch_t<D, 0x4444u>(p, grid, stream);   // {2,6,10,14}
-        case 7: return launch_t<D, 0xA54Au>(p, grid, stream);   // {1,3,6,8,10,13,15}
-        case 5: return launch_t<D, 0x2492u>(p, grid, stream);   // {1,4,7,10,13}
-        case 6: return launch_t<D, 0x4A4Au>(p, grid, stream);   // {1,3,6,9,11,14}
-        case 8: return launch_t<D, 0xAAAAu>(p, grid, stream);
         default: return launch_t<D, kPolyDefault>(p, grid, stream);
     }
 }

@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Kernel-only timing of the WAN-512 t>=2 chunk attention for the env-selected
 variant (e.g. TM_POLY); prints one line.  Used for tuning sweeps:
-    for v in 0 4 5 6 7 8; do TM_POLY=$v python tools/sweep.py; done
+    for v in 0 1 3 4; do TM_POLY=$v python tools/sweep.py; done   (0 = default split)
 """
 import os
 import statistics
