@@ -95,7 +95,7 @@ struct __align__(64) FmhaParams {
 
 // Debug timeline: role r in [0,13) owns trace[r*kTraceCap ..]; entry =
 // clock64() << 8 | event code.  Only CTA 0 records; off when p.trace == 0.
-constexpr int kTraceCap = 4096;
+[[maybe_unused]] constexpr int kTraceCap = 4096;
 // Compiled in only with -DTM_TRACE_ENABLED (TM_TRACE_BUILD=1 python -m
 // paper_2506_03099_b200.build); the production build has no trace code.
 __device__ __forceinline__ void trace_ev(const FmhaParams& p, int role, int& n, int code) {

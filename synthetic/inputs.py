@@ -81,6 +81,22 @@ def _finish(x: np.ndarray, dtype: str) -> Tensor:
     return Tensor(x, "fp32")
 
 
+def ramp_qkv(rng: np.random.Generator, L: int, H: int, d: int, dtype: str, slope: float,
+             q_norm: float = 4.0):
+    """Keys whose logits grow (slope > 0) or shrink (slope < 0) linearly along
+    the sequence: q = q_norm * u_h + small noise, k_j = slope * j * u_h + noise,
+    v ~ N(0, 1), with u_h a random unit direction per head.  The logit of key
+    j is ~ q_norm * slope * j * <u, u> -- the running max moves on every KV
+    tile (the online-softmax rescale path).  Input recipe only."""
+    u = rng.standard_normal((H, d))
+    u /= np.linalg.norm(u, axis=1, keepdims=True)
+    q = q_norm * u[None] + 0.05 * rng.standard_normal((L, H, d))
+    j = np.arange(L, dtype=np.float64)[:, None, None]
+    k = slope * j * u[None] + 0.05 * rng.standard_normal((L, H, d))
+    v = rng.standard_normal((L, H, d))
+    return _finish(q, dtype), _finish(k, dtype), _finish(v, dtype)
+
+
 def chunk_qkv(rng: np.random.Generator, L: int, H: int, d: int, dtype: str,
               dist: str = "D0", role: str = "cur", shared_dir=None):
     """Q, K, V for one block of L tokens, token-major [L][H][d].

@@ -538,3 +538,26 @@ def test_audio_cross_attention_wan512_chunk_batch2():
                                            va.f64.reshape(B, frames, A, H, d)[b], face)
         assert rel_err(got[b][:, face], ref[:, face]) <= BF16_ALARM
     ca.close()
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+@pytest.mark.parametrize("growth", [9.0, 5.0, 30.0, -9.0])
+def test_running_max_moves_every_tile(dtype, growth):
+    """Online-softmax rescale path: logits ramp along the keys so the row max
+    grows (or, for growth < 0, shrinks) by `growth` log2 units per 128-key
+    tile.  The kernel moves its running max only when a tile's max exceeds it
+    by more than 8 (O and l rescaled then), so 9 and 30 rescale at every tile,
+    5 skips (weights up to 2^8 are carried), -9 never moves after the first
+    tile.  Exact after the final O / l either way: compared with the oracle."""
+    H, d, L = 2, 128, 1000
+    scale_log2 = np.log2(np.e) / np.sqrt(d)
+    q_norm = 4.0
+    slope = growth / (128 * q_norm * scale_log2)      # logit slope per key, log2 units
+    rng = np.random.default_rng(syn.seed_for(11, 0, extra=int(growth) + 100))
+    q, k, v = syn.ramp_qkv(rng, L, H, d, dtype, slope, q_norm)
+    ca = tm.ChunkAttention(H, d, 16, 16, 1, 1, dtype=DT[dtype])
+    o = torch.empty_like(to_dev(q))
+    ca.window(to_dev(q), to_dev(k), to_dev(v), o, [L])
+    ref = oracle.window_attention(q.f64, k.f64, v.f64, [L])
+    assert rel_err(from_dev(o), ref) <= (FP32_TOL if dtype == "fp32" else BF16_ALARM)
+    ca.close()
