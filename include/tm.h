@@ -25,8 +25,8 @@
  *  - Every device pointer is owned by the CALLER (allocated e.g. with torch)
  *    and must stay valid until the stream reaches the call.  The library
  *    owns only the opaque host tm_ctx (and, for P > 1, its NCCL
- *    communicator).  The library never allocates device memory after
- *    tm_attn_init.
+ *    communicator or its mappings of the peers' windows).  The library never
+ *    allocates device memory.
  *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default).
  *  - Argument, shape and ordering errors are detected on the host before
  *    any launch; the call then has no side effects.  Device / NCCL errors
@@ -65,6 +65,39 @@ typedef enum {
 
 typedef enum { TM_BF16 = 0, TM_FP32 = 1 } tm_dtype;
 
+/* How the Ulysses exchange moves data between the ranks.
+ *  TM_TRANSPORT_NCCL: pack kernel -> ncclAlltoAll -> unpack kernel, each way.
+ *  TM_TRANSPORT_PEER: no NCCL on the data path.  Every rank's workspace holds
+ *    a window that all ranks map (CUDA IPC over NVLink, see tm_peer_export /
+ *    tm_peer_connect).  The attention kernel itself pushes this rank's
+ *    sequence shard of Q, K, V into the head owners' windows (NVLink stores),
+ *    waits per Q tile / per K-V tile only for the source ranks that tile comes
+ *    from (so the cached c_0 and c_{t-1} segments are attended while the
+ *    current chunk is still in flight), and its epilogue stores each output
+ *    row straight into the window of the rank that owns that token; a small
+ *    receive kernel copies the finished O window to `o`.  bf16 only,
+ *    world_size <= 8. */
+typedef enum { TM_TRANSPORT_NCCL = 0, TM_TRANSPORT_PEER = 1 } tm_transport;
+
+/* Phases of one collective call (tm_chunk_attention_phases,
+ * tm_kvcache_put_reference_phases), TM_TRANSPORT_PEER only.  A call runs the
+ * requested phases in order; the next call continues with the next phase of
+ * the same operation.  Splitting lets ranks that share one device and one
+ * process (tests) enqueue every rank's SEND before any rank's ATTEND.
+ *   SEND    push this rank's shard into the owners' windows
+ *   ATTEND  chunk: attention (waits for the pushes; O rows to their owners);
+ *           reference: copy the received K/V window into the cache
+ *   RECV    chunk: wait for every rank's O rows, copy them to o;
+ *           reference: barrier (windows free again)
+ * SEND|ATTEND in one call fuses the push into the attention kernel. */
+#define TM_PHASE_SEND 1u
+#define TM_PHASE_ATTEND 2u
+#define TM_PHASE_RECV 4u
+#define TM_PHASE_ALL 7u
+
+/* Bytes of the handle tm_peer_export writes (CUDA IPC handle + offset). */
+#define TM_PEER_HANDLE_BYTES 72
+
 typedef struct {
     int32_t heads;         /* H, global number of attention heads (MHA; H_kv == H)   */
     int32_t head_dim;      /* d in {64, 128}                                          */
@@ -78,12 +111,13 @@ typedef struct {
     int32_t world_size;    /* P, Ulysses group size; H % P == 0                       */
     int32_t rank;          /* this process's rank in [0, P)                           */
     int32_t device;        /* CUDA device ordinal used by this ctx                    */
+    int32_t transport;     /* tm_transport (ignored when world_size == 1 and NCCL)    */
 } tm_config;
 
 typedef struct tm_ctx tm_ctx;
 
 /* Version of the ABI (major * 100 + minor). */
-int32_t tm_version(void);
+int32_t tm_version(void);   /* 101: tm_config.transport, peer transport */
 
 /* Thread-local message for the last non-OK status returned on this thread. */
 const char* tm_last_error(void);
@@ -94,8 +128,10 @@ const char* tm_last_error(void);
  * the config, independent of stream length.  0 on invalid config. */
 size_t tm_kvcache_bytes(const tm_config* cfg);
 
-/* Bytes of device workspace: Ulysses staging when world_size > 1, plus a
- * small debug/scratch area.  0 is never returned for a valid config. */
+/* Bytes of device workspace: split-KV scratch and a debug flag, plus the
+ * Ulysses staging (NCCL transport, world_size > 1) or the peer window
+ * (TM_TRANSPORT_PEER: counters and Q, K, V windows [B][max(Lc,Lr)][H/P][d],
+ * O window [B][Lc/P][H][d]).  0 is never returned for a valid config. */
 size_t tm_workspace_bytes(const tm_config* cfg);
 
 /* NCCL unique id for world_size > 1 (rank 0 calls it; the harness
@@ -171,6 +207,38 @@ tm_status tm_audio_cross_attention(tm_ctx* ctx, const void* q, const void* k_aud
                                    const int32_t* face_ids, int64_t n_face, int32_t window,
                                    void* scratch, size_t scratch_bytes, void* stream);
 
+/* Phased forms of tm_chunk_attention / tm_kvcache_put_reference for
+ * TM_TRANSPORT_PEER (see TM_PHASE_*); `phases` = TM_PHASE_ALL is the plain
+ * call.  Arguments are validated on the operation's first phase; the later
+ * phases of the same operation must repeat them (TM_ERR_STREAM_ORDER
+ * otherwise, or if a phase is skipped or a new operation starts before the
+ * previous one finished its RECV phase).  NCCL contexts accept only ALL. */
+tm_status tm_chunk_attention_phases(tm_ctx* ctx, int32_t layer, int32_t step, int64_t chunk,
+                                    const void* q, const void* k, const void* v, void* o,
+                                    uint32_t phases, void* stream);
+tm_status tm_kvcache_put_reference_phases(tm_ctx* ctx, int32_t layer, int32_t step,
+                                          const void* k, const void* v, uint32_t phases,
+                                          void* stream);
+
+/* TM_TRANSPORT_PEER group setup (collective; after tm_attn_init on every rank,
+ * before any other call).  tm_peer_export writes this rank's window handle
+ * (TM_PEER_HANDLE_BYTES: the CUDA IPC handle of the workspace allocation and
+ * the window's offset in it); the harness all-gathers the handles (e.g.
+ * torch.distributed) and every rank passes all of them, in rank order, to
+ * tm_peer_connect, which maps the peers' windows (cudaIpcOpenMemHandle with
+ * lazy peer access; closed by tm_attn_destroy).  The workspace must come from
+ * cudaMalloc (torch's default caching allocator), not VMM.
+ * tm_peer_connect_local connects `n` contexts of ONE process (virtual ranks,
+ * e.g. several on one device for tests): ctxs[i] must have rank i. */
+tm_status tm_peer_export(tm_ctx* ctx, uint8_t handle[TM_PEER_HANDLE_BYTES]);
+tm_status tm_peer_connect(tm_ctx* ctx, const uint8_t* handles);
+tm_status tm_peer_connect_local(tm_ctx* const* ctxs, int32_t n);
+
+/* Synchronises the device and reports whether a device-side peer wait timed
+ * out (10 s without the expected peer signal) since the last check:
+ * TM_ERR_CUDA with a message, else TM_OK.  Clears the flag. */
+tm_status tm_peer_check(tm_ctx* ctx);
+
 /* Device pointers of the cache slot that chunk `chunk` at (layer, step) is
  * stored in ([B][Lc][H/P][d] each).  A caller may write the chunk's K/V
  * there before tm_chunk_attention to skip the append copy. */
@@ -216,6 +284,23 @@ tm_status tm_flow_sampler_step(tm_ctx* ctx, float* x, const void* v, int32_t v_d
 tm_status tm_ulysses_shuffle_host(int32_t mode, const void* src, void* dst, int32_t batch,
                                   int64_t shard_tokens, int64_t tokens, int32_t heads_per_rank,
                                   int32_t world_size, int32_t head_dim, int32_t elem_bytes);
+
+/* Host reference of the peer transport's index maps (TM_TRANSPORT_PEER; the
+ * same code the device push and attention epilogue use), for tests of the
+ * multi-rank host logic without GPUs.  Host buffers; rows of head_dim *
+ * elem_bytes bytes (a multiple of 16); Ls = shard_tokens, L = tokens,
+ * Lw = window_tokens (>= L), Hl = heads_per_rank, H = Hl * world_size.
+ *   mode 0 (push, row a2): src = rank's sequence shard [B][Ls][H][d];
+ *          dst = the world_size windows [P][B][Lw][Hl][d]: head block p of
+ *          token t goes to window p, row rank*Ls + t (padding tokens dropped).
+ *   mode 1 (output, row a6): src = rank's head-shard output [B][L][Hl][d];
+ *          dst = the world_size O windows [P][B][Ls][H][d]: row q goes to
+ *          window q / Ls, row q % Ls, heads [rank*Hl, rank*Hl + Hl).
+ * Words not routed are left untouched. */
+tm_status tm_peer_route_host(int32_t mode, const void* src, void* dst, int32_t batch,
+                             int64_t shard_tokens, int64_t tokens, int64_t window_tokens,
+                             int32_t heads_per_rank, int32_t world_size, int32_t rank,
+                             int32_t head_dim, int32_t elem_bytes);
 
 /* Introspection for tests / bench: number of device kernels the last
  * tm_chunk_attention launched on this ctx, and the attention kernel

@@ -19,8 +19,8 @@ OUT = os.path.join(PKG, "libtm.so")
 BUILD = os.path.join(CSRC, "build")
 ROOT = os.path.dirname(PKG)
 
-SOURCES = ["api.cpp", "comm.cpp", "fmha_sm100.cu", "fmha_fp32.cu", "elementwise.cu"]
-HEADERS = ["ptx.cuh", "internal.h", "comm.h", "ulysses_map.h"]
+SOURCES = ["api.cpp", "comm.cpp", "fmha_sm100.cu", "fmha_fp32.cu", "elementwise.cu", "peer.cu"]
+HEADERS = ["ptx.cuh", "internal.h", "comm.h", "ulysses_map.h", "peer.cuh", "peer_map.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -10,8 +10,10 @@
 // (cache miss / order).
 #include "../../include/tm.h"
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -22,6 +24,7 @@
 
 #include "comm.h"
 #include "internal.h"
+#include "peer_map.h"
 #include "ulysses_map.h"
 
 using namespace tmk;
@@ -62,6 +65,16 @@ tm_status validate(const tm_config* c) {
                     c->heads, c->world_size);
     if (!(c->softmax_scale >= 0.f) || !std::isfinite(c->softmax_scale))
         return fail(TM_ERR_INVALID_ARG, "softmax_scale must be finite and >= 0");
+    if (c->transport != TM_TRANSPORT_NCCL && c->transport != TM_TRANSPORT_PEER)
+        return fail(TM_ERR_INVALID_ARG, "transport %d not in {TM_TRANSPORT_NCCL, TM_TRANSPORT_PEER}",
+                    c->transport);
+    if (c->transport == TM_TRANSPORT_PEER) {
+        if (c->dtype != TM_BF16)
+            return fail(TM_ERR_UNSUPPORTED, "TM_TRANSPORT_PEER is bf16 only (the fp32 validation "
+                                            "mode uses the NCCL transport)");
+        if (c->world_size > kMaxPeers)
+            return fail(TM_ERR_UNSUPPORTED, "TM_TRANSPORT_PEER needs world_size <= %d", kMaxPeers);
+    }
     return TM_OK;
 }
 
@@ -74,7 +87,10 @@ bool force_ulysses() {
 }
 
 struct Layout {
-    bool exchange;                   // Ulysses path (P > 1, or forced)
+    bool exchange;                   // NCCL Ulysses path (P > 1, or forced)
+    bool peer;                       // peer-memory Ulysses path (TM_TRANSPORT_PEER, any P)
+    int64_t Lw;                      // peer window rows max(Lc, Lr)
+    size_t win_off, win_bytes, win_tensor_bytes, win_o_bytes;
     int esize, Hl, P;
     int64_t Lr, Lc, Lr_s, Lc_s;     // full and per-rank shard token counts
     size_t ref_bytes, slot_bytes, region_bytes, cache_bytes;
@@ -97,8 +113,16 @@ Layout layout_of(const tm_config* c) {
     L.cache_bytes = L.region_bytes * size_t(c->num_layers) * size_t(c->num_steps);
     L.flag_bytes = kAlign;
     L.scratch_bytes = c->dtype == TM_BF16 ? align_up(fmha_sm100_scratch_bytes(c->head_dim)) : 0;
-    L.exchange = L.P > 1 || force_ulysses();
-    if (L.exchange) {
+    L.peer = c->transport == TM_TRANSPORT_PEER;
+    L.exchange = !L.peer && (L.P > 1 || force_ulysses());
+    if (L.peer) {
+        L.Lw = std::max(L.Lc, L.Lr);
+        L.win_tensor_bytes = align_up(size_t(c->batch) * L.Lw * row);
+        L.win_o_bytes = align_up(size_t(c->batch) * L.Lc_s * size_t(c->heads) * c->head_dim * L.esize);
+        L.win_off = L.flag_bytes + L.scratch_bytes;
+        L.win_bytes = 4096 + 3 * L.win_tensor_bytes + L.win_o_bytes;
+        L.ws_bytes = L.win_off + L.win_bytes;
+    } else if (L.exchange) {
         const size_t full_row = size_t(c->heads) * c->head_dim * L.esize;
         const size_t qkv = 3 * align_up(size_t(c->batch) * L.Lc_s * full_row);
         const size_t kv = 2 * align_up(size_t(c->batch) * L.Lr_s * full_row);
@@ -126,6 +150,18 @@ struct tm_ctx {
     void* comm = nullptr;
     int launches = 0;
     bool debug = false;
+    // peer transport
+    bool connected = false;
+    uint8_t* win[kMaxPeers] = {};      // every rank's window, mapped in this process
+    std::vector<void*> ipc_opened;     // cudaIpcOpenMemHandle bases to close
+    uint32_t e_arr[3] = {0, 0, 0};     // arrivals expected per source (Q, K, V)
+    uint32_t e_done = 0;               // done signals expected per source
+    // phased operation in flight: kind 0 none, 1 chunk, 2 reference
+    int op_kind = 0;
+    uint32_t op_done = 0;
+    int op_layer = 0, op_step = 0;
+    int64_t op_chunk = 0;
+    const void* op_ptr[4] = {};
     unsigned long long* trace = nullptr;   // TM_TRACE=<file>: kernel timeline of CTA 0
     std::string trace_path;
 
@@ -143,6 +179,12 @@ struct tm_ctx {
     uint8_t* recv() const { return send() + lay.xfer_bytes; }
     uint8_t* qh() const { return recv() + lay.xfer_bytes; }
     uint8_t* oh() const { return qh() + lay.head_bytes; }
+    // peer window of rank r (own: r == cfg.rank)
+    PeerCounters* ctr(int r) const { return reinterpret_cast<PeerCounters*>(win[r]); }
+    uint8_t* wq(int r) const { return win[r] + 4096; }
+    uint8_t* wk(int r) const { return wq(r) + lay.win_tensor_bytes; }
+    uint8_t* wv(int r) const { return wk(r) + lay.win_tensor_bytes; }
+    uint8_t* wo(int r) const { return wv(r) + lay.win_tensor_bytes; }
 };
 
 namespace {
@@ -206,11 +248,104 @@ tm_status ulysses_in(tm_ctx* c, int ntensors, const void* const* src, void* cons
     return TM_OK;
 }
 
+// ------------------------------------------------------------ peer transport
+
+bool peer_separate_push() {   // A/B and debugging: push in its own kernel, not fused
+    const char* e = getenv("TM_PEER_SEPARATE_PUSH");
+    return e && *e && strcmp(e, "0") != 0;
+}
+
+// The push of this rank's sequence shard(s) [B][Ls][H][d] into the owners' windows.
+PeerPush make_push(const tm_ctx* c, const void* q, const void* k, const void* v, int64_t Ls,
+                   int64_t L) {
+    const Layout& Ly = c->lay;
+    PeerPush pp;
+    pp.src[0] = q;
+    pp.src[1] = k;
+    pp.src[2] = v;
+    for (int p = 0; p < Ly.P; ++p) {
+        pp.dst[0][p] = c->wq(p);
+        pp.dst[1][p] = c->wk(p);
+        pp.dst[2][p] = c->wv(p);
+        pp.ctr[p] = c->ctr(p);
+    }
+    pp.own = c->ctr(c->cfg.rank);
+    pp.B = c->cfg.batch;
+    pp.P = Ly.P;
+    pp.rank = c->cfg.rank;
+    pp.W = Ly.Hl * c->cfg.head_dim * Ly.esize / 16;
+    pp.Ls = Ls;
+    pp.L = L;
+    pp.Lw = Ly.Lw;
+    return pp;
+}
+
+// Phase bookkeeping of one collective operation (see TM_PHASE_* in tm.h).
+tm_status begin_phases(tm_ctx* c, int kind, uint32_t phases, int layer, int step, int64_t chunk,
+                       const void* a0, const void* a1, const void* a2, const void* a3, bool* first) {
+    if (phases == 0 || phases > TM_PHASE_ALL || phases == (TM_PHASE_SEND | TM_PHASE_RECV))
+        return fail(TM_ERR_INVALID_ARG, "phases 0x%x: a non-empty run of SEND, ATTEND, RECV", phases);
+    if (!c->lay.peer && phases != TM_PHASE_ALL)
+        return fail(TM_ERR_UNSUPPORTED, "phased calls need TM_TRANSPORT_PEER");
+    const uint32_t lowest = phases & (~phases + 1);
+    if (c->op_kind == 0) {
+        if (lowest != TM_PHASE_SEND)
+            return fail(TM_ERR_STREAM_ORDER, "an operation starts with TM_PHASE_SEND");
+        *first = true;
+        return TM_OK;
+    }
+    const void* a[4] = {a0, a1, a2, a3};
+    bool same = c->op_kind == kind && c->op_layer == layer && c->op_step == step &&
+                c->op_chunk == chunk;
+    for (int i = 0; i < 4; ++i) same = same && a[i] == c->op_ptr[i];
+    if (!same)
+        return fail(TM_ERR_STREAM_ORDER, "a phased operation is in flight: finish it (same "
+                                         "arguments) before starting another");
+    if (lowest != c->op_done + 1)
+        return fail(TM_ERR_STREAM_ORDER, "phase 0x%x out of order (done 0x%x)", phases, c->op_done);
+    *first = false;
+    return TM_OK;
+}
+
+void note_phases(tm_ctx* c, int kind, uint32_t phases, int layer, int step, int64_t chunk,
+                 const void* a0, const void* a1, const void* a2, const void* a3) {
+    if (c->op_kind == 0) {
+        c->op_kind = kind;
+        c->op_layer = layer;
+        c->op_step = step;
+        c->op_chunk = chunk;
+        c->op_ptr[0] = a0;
+        c->op_ptr[1] = a1;
+        c->op_ptr[2] = a2;
+        c->op_ptr[3] = a3;
+        c->op_done = 0;
+    }
+    c->op_done |= phases;
+    if (c->op_done == TM_PHASE_ALL) {
+        c->op_kind = 0;
+        c->op_done = 0;
+    }
+}
+
+using PFN_getAddressRange = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+
+PFN_getAddressRange address_range_fn() {
+    static PFN_getAddressRange fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return PFN_getAddressRange(nullptr);
+        return reinterpret_cast<PFN_getAddressRange>(f);
+    }();
+    return fn;
+}
+
 }  // namespace
 
 extern "C" {
 
-int32_t tm_version(void) { return 100; }
+int32_t tm_version(void) { return 101; }
 
 const char* tm_last_error(void) { return g_err.c_str(); }
 
@@ -283,6 +418,10 @@ tm_status tm_attn_init(const tm_config* cfg, const uint8_t* nccl_id, void* cache
     if (const char* tp = getenv("TM_TRACE")) {
         if (*tp && cudaMalloc(&c->trace, 13 * 4096 * 8) == cudaSuccess) c->trace_path = tp;
     }
+    if (L.peer) {
+        c->win[cfg->rank] = c->ws + L.win_off;
+        c->connected = L.P == 1;       // a one-rank group is its own peer
+    }
     if (L.exchange) {
         const char* e = comm_init(&c->comm, cfg->world_size, cfg->rank, nccl_id);
         if (e) {
@@ -297,6 +436,7 @@ tm_status tm_attn_init(const tm_config* cfg, const uint8_t* nccl_id, void* cache
 tm_status tm_attn_destroy(tm_ctx* ctx) {
     if (!ctx) return fail(TM_ERR_INVALID_ARG, "null ctx");
     if (ctx->comm) comm_destroy(ctx->comm);
+    for (void* p : ctx->ipc_opened) cudaIpcCloseMemHandle(p);
     if (ctx->trace) cudaFree(ctx->trace);
     delete ctx;
     return TM_OK;
@@ -331,18 +471,68 @@ tm_status tm_kvcache_slot_ptr(tm_ctx* ctx, int32_t layer, int32_t step, int64_t 
 
 tm_status tm_kvcache_put_reference(tm_ctx* ctx, int32_t layer, int32_t step, const void* k,
                                    const void* v, void* stream) {
+    return tm_kvcache_put_reference_phases(ctx, layer, step, k, v, TM_PHASE_ALL, stream);
+}
+
+tm_status tm_kvcache_put_reference_phases(tm_ctx* ctx, int32_t layer, int32_t step, const void* k,
+                                          const void* v, uint32_t phases, void* stream) {
     if (!ctx || !k || !v) return fail(TM_ERR_INVALID_ARG, "null argument");
     tm_status st = check_layer_step(ctx, layer, step, true);
     if (st) return st;
+    bool first = false;
+    st = begin_phases(ctx, 2, phases, layer, step, 0, k, v, nullptr, nullptr, &first);
+    if (st) return st;
     const int s0 = step < 0 ? 0 : step, s1 = step < 0 ? ctx->cfg.num_steps : step + 1;
-    for (int s = s0; s < s1; ++s)
-        if (ctx->last[ctx->idx(layer, s)] >= 1)
-            return fail(TM_ERR_REF_IMMUTABLE,
-                        "reference of (layer %d, step %d) is immutable after chunk 1 until "
-                        "tm_stream_reset (S:287)", layer, s);
+    if (first)
+        for (int s = s0; s < s1; ++s)
+            if (ctx->last[ctx->idx(layer, s)] >= 1)
+                return fail(TM_ERR_REF_IMMUTABLE,
+                            "reference of (layer %d, step %d) is immutable after chunk 1 until "
+                            "tm_stream_reset (S:287)", layer, s);
     cudaStream_t cs = static_cast<cudaStream_t>(stream);
     const Layout& Ly = ctx->lay;
     ctx->launches = 0;
+    if (Ly.peer) {
+        // a1 over peer memory: push the reference shard into the owners' K/V
+        // windows, copy the received window into the cache, then a barrier.
+        if (!ctx->connected) return fail(TM_ERR_STREAM_ORDER, "peer group not connected (tm_peer_connect)");
+        const int r = ctx->cfg.rank;
+        const int row_bytes = Ly.Hl * ctx->cfg.head_dim * Ly.esize;
+        if (phases & TM_PHASE_SEND) {
+            const PeerPush pp = make_push(ctx, nullptr, k, v, Ly.Lr_s, Ly.Lr);
+            st = cuda_check(launch_peer_push(pp, cs, &ctx->launches), "peer push (reference)");
+            if (st) return st;
+            ++ctx->e_arr[1];
+            ++ctx->e_arr[2];
+        }
+        if (phases & TM_PHASE_ATTEND) {
+            PeerCounters* ctrs[kMaxPeers];
+            for (int p = 0; p < Ly.P; ++p) ctrs[p] = ctx->ctr(p);
+            ++ctx->e_done;
+            st = cuda_check(launch_peer_ref_store(ctrs, ctx->ctr(r), ctx->e_arr[1], Ly.P, r, ctx->wk(r),
+                                                  ctx->wv(r), ctx->kref(layer, s0), ctx->vref(layer, s0),
+                                                  ctx->cfg.batch, Ly.Lw, Ly.Lr, row_bytes, cs,
+                                                  &ctx->launches),
+                            "peer reference store");
+            if (st) return st;
+            for (int s = s0 + 1; s < s1; ++s) {
+                st = cuda_check(cudaMemcpyAsync(ctx->kref(layer, s), ctx->kref(layer, s0),
+                                                2 * Ly.ref_bytes, cudaMemcpyDeviceToDevice, cs),
+                                "reference alias copy");
+                if (st) return st;
+            }
+        }
+        if (phases & TM_PHASE_RECV) {
+            st = cuda_check(launch_peer_wait_done(ctx->ctr(r), ctx->e_done, Ly.P, cs, &ctx->launches),
+                            "peer barrier");
+            if (st) return st;
+        }
+        note_phases(ctx, 2, phases, layer, step, 0, k, v, nullptr, nullptr);
+        if (phases & TM_PHASE_RECV)
+            for (int s = s0; s < s1; ++s) ctx->ref_ok[ctx->idx(layer, s)] = 1;
+        return TM_OK;
+    }
+    note_phases(ctx, 2, phases, layer, step, 0, k, v, nullptr, nullptr);
     if (!Ly.exchange) {
         const size_t bytes = size_t(ctx->cfg.batch) * Ly.Lr * Ly.Hl * ctx->cfg.head_dim * Ly.esize;
         for (int s = s0; s < s1; ++s) {
@@ -371,6 +561,12 @@ tm_status tm_kvcache_put_reference(tm_ctx* ctx, int32_t layer, int32_t step, con
 
 tm_status tm_chunk_attention(tm_ctx* ctx, int32_t layer, int32_t step, int64_t chunk,
                              const void* q, const void* k, const void* v, void* o, void* stream) {
+    return tm_chunk_attention_phases(ctx, layer, step, chunk, q, k, v, o, TM_PHASE_ALL, stream);
+}
+
+tm_status tm_chunk_attention_phases(tm_ctx* ctx, int32_t layer, int32_t step, int64_t chunk,
+                                    const void* q, const void* k, const void* v, void* o,
+                                    uint32_t phases, void* stream) {
     if (!ctx || !q || !k || !v || !o) return fail(TM_ERR_INVALID_ARG, "null argument");
     tm_status st = check_layer_step(ctx, layer, step, false);
     if (st) return st;
@@ -378,19 +574,94 @@ tm_status tm_chunk_attention(tm_ctx* ctx, int32_t layer, int32_t step, int64_t c
                                (long long)chunk);
     if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o))
         return fail(TM_ERR_INVALID_ARG, "q, k, v, o must be 16-byte aligned");
+    bool first = false;
+    st = begin_phases(ctx, 1, phases, layer, step, chunk, q, k, v, o, &first);
+    if (st) return st;
     const size_t li = ctx->idx(layer, step);
-    if (!ctx->ref_ok[li])
-        return fail(TM_ERR_STREAM_ORDER, "cache miss: no reference for (layer %d, step %d) (S:296)",
-                    layer, step);
-    const int64_t last = ctx->last[li];
-    if (chunk != last + 1 && chunk != last)
-        return fail(TM_ERR_STREAM_ORDER,
-                    "chunk %lld at (layer %d, step %d) out of order (last %lld; S:296)",
-                    (long long)chunk, layer, step, (long long)last);
+    if (first) {
+        if (!ctx->ref_ok[li])
+            return fail(TM_ERR_STREAM_ORDER, "cache miss: no reference for (layer %d, step %d) (S:296)",
+                        layer, step);
+        const int64_t last = ctx->last[li];
+        if (chunk != last + 1 && chunk != last)
+            return fail(TM_ERR_STREAM_ORDER,
+                        "chunk %lld at (layer %d, step %d) out of order (last %lld; S:296)",
+                        (long long)chunk, layer, step, (long long)last);
+    }
     const tm_config& cf = ctx->cfg;
     const Layout& Ly = ctx->lay;
     cudaStream_t cs = static_cast<cudaStream_t>(stream);
     ctx->launches = 0;
+    if (Ly.peer) {
+        if (!ctx->connected) return fail(TM_ERR_STREAM_ORDER, "peer group not connected (tm_peer_connect)");
+        const int r = cf.rank;
+        const bool fused = (phases & TM_PHASE_SEND) && (phases & TM_PHASE_ATTEND) && !peer_separate_push();
+        const PeerPush pp = make_push(ctx, q, k, v, Ly.Lc_s, Ly.Lc);
+        if (phases & TM_PHASE_SEND) {
+            if (!fused) {
+                st = cuda_check(launch_peer_push(pp, cs, &ctx->launches), "peer push");
+                if (st) return st;
+            }
+            for (int T = 0; T < 3; ++T) ++ctx->e_arr[T];
+        }
+        if (phases & TM_PHASE_ATTEND) {
+            // a2 + a3 + a4 + a5 + a6 in one kernel: Q and c_t's K/V come from this
+            // rank's window (pushed by their sequence owners, fused when SEND is
+            // part of this call), c_t is appended to slot chunk&1 from the smem
+            // ring, and O rows are stored into their token owners' windows.
+            AttnProblem pr;
+            pr.q = ctx->wq(r);
+            pr.q_bstride = Ly.Lw;
+            pr.o = ctx->wo(r);
+            pr.Lq = Ly.Lc;
+            pr.B = cf.batch;
+            pr.H = Ly.Hl;
+            pr.d = cf.head_dim;
+            pr.scale = ctx->scale;
+            pr.seg[pr.nseg++] = Segment{ctx->kref(layer, step), ctx->vref(layer, step), Ly.Lr};
+            if (chunk >= 2)
+                pr.seg[pr.nseg++] = Segment{ctx->kslot(layer, step, chunk - 1),
+                                            ctx->vslot(layer, step, chunk - 1), Ly.Lc};
+            pr.seg[pr.nseg++] = Segment{ctx->wk(r), ctx->wv(r), Ly.Lc, Ly.Lw};
+            pr.store_k = ctx->kslot(layer, step, chunk);
+            pr.store_v = ctx->vslot(layer, step, chunk);
+            PeerAttnArgs pa;
+            pa.own = ctx->ctr(r);
+            for (int T = 0; T < 3; ++T) pa.epoch[T] = ctx->e_arr[T];
+            pa.wait_seg = pr.nseg - 1;
+            pa.src_rows = Ly.Lc_s;
+            pa.push = fused;
+            pa.pp = pp;
+            for (int p = 0; p < Ly.P; ++p) {
+                pa.o_dst[p] = ctx->wo(p);
+                pa.done_ctr[p] = ctx->ctr(p);
+            }
+            pa.o_rows = Ly.Lc_s;
+            pa.o_H = cf.heads;
+            pa.o_h0 = r * Ly.Hl;
+            pa.signal_done = true;
+            pa.P = Ly.P;
+            pa.rank = r;
+            pr.peer = &pa;
+            ++ctx->e_done;
+            st = cuda_check(launch_fmha_sm100(pr, ctx->scratch(), cs, &ctx->launches),
+                            "attention kernel launch (peer)");
+            if (st) return st;
+        }
+        if (phases & TM_PHASE_RECV) {
+            st = cuda_check(launch_peer_recv_o(ctx->ctr(r), ctx->e_done, Ly.P, ctx->wo(r), o, cf.batch,
+                                               Ly.Lc_s, Ly.Lc, r, cf.heads * cf.head_dim * Ly.esize,
+                                               cs, &ctx->launches),
+                            "peer receive");
+            if (st) return st;
+        }
+        note_phases(ctx, 1, phases, layer, step, chunk, q, k, v, o);
+        if (!(phases & TM_PHASE_RECV)) return TM_OK;
+        ctx->last[li] = chunk;
+        return debug_check(ctx, o, int64_t(cf.batch) * Ly.Lc_s * cf.heads * cf.head_dim, 1, cs,
+                           "tm_chunk_attention");
+    }
+    note_phases(ctx, 1, phases, layer, step, chunk, q, k, v, o);
 
     void* kslot = ctx->kslot(layer, step, chunk);
     void* vslot = ctx->vslot(layer, step, chunk);
@@ -485,7 +756,7 @@ tm_status tm_chunk_attention(tm_ctx* ctx, int32_t layer, int32_t step, int64_t c
 tm_status tm_window_attention(tm_ctx* ctx, const void* q, const void* k, const void* v, void* o,
                               const int64_t* chunk_len, int32_t n_chunks, void* stream) {
     if (!ctx || !q || !k || !v || !o || !chunk_len) return fail(TM_ERR_INVALID_ARG, "null argument");
-    if (ctx->lay.exchange)
+    if (ctx->lay.exchange || ctx->lay.P > 1)
         return fail(TM_ERR_UNSUPPORTED, "tm_window_attention needs a world_size == 1 context");
     if (n_chunks <= 0) return fail(TM_ERR_SHAPE, "n_chunks = %d <= 0", n_chunks);
     if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o))
@@ -547,7 +818,7 @@ tm_status tm_audio_cross_attention(tm_ctx* ctx, const void* q, const void* k_aud
                                    void* scratch, size_t scratch_bytes, void* stream) {
     if (!ctx || !q || !k_audio || !v_audio || !o || !scratch)
         return fail(TM_ERR_INVALID_ARG, "null argument");
-    if (ctx->lay.exchange)
+    if (ctx->lay.exchange || ctx->lay.P > 1)
         return fail(TM_ERR_UNSUPPORTED, "tm_audio_cross_attention needs a world_size == 1 context");
     if (frames <= 0 || tokens_per_frame <= 0 || audio_tokens_per_frame <= 0)
         return fail(TM_ERR_SHAPE, "non-positive frames / tokens");
@@ -660,6 +931,50 @@ tm_status tm_ulysses_shuffle_host(int32_t mode, const void* src, void* dst, int3
     return TM_OK;
 }
 
+tm_status tm_peer_route_host(int32_t mode, const void* src, void* dst, int32_t batch,
+                             int64_t shard_tokens, int64_t tokens, int64_t window_tokens,
+                             int32_t heads_per_rank, int32_t world_size, int32_t rank,
+                             int32_t head_dim, int32_t elem_bytes) {
+    if (!src || !dst) return fail(TM_ERR_INVALID_ARG, "null buffer");
+    if (mode != 0 && mode != 1) return fail(TM_ERR_INVALID_ARG, "mode %d not in {0, 1}", mode);
+    if (batch <= 0 || shard_tokens <= 0 || tokens <= 0 || heads_per_rank <= 0 || world_size <= 0 ||
+        rank < 0 || rank >= world_size || head_dim <= 0 || elem_bytes <= 0 ||
+        (int64_t(head_dim) * elem_bytes) % 16 || tokens > shard_tokens * world_size ||
+        window_tokens < tokens)
+        return fail(TM_ERR_SHAPE, "invalid peer route shape");
+    struct W16 { uint64_t a, b; };
+    const W16* in = static_cast<const W16*>(src);
+    W16* out = static_cast<W16*>(dst);
+    const int dw = head_dim * elem_bytes / 16;                       // words per (token, head)
+    const int H = heads_per_rank * world_size;
+    if (mode == 0) {
+        const uint32_t W = uint32_t(heads_per_rank * dw);
+        const int64_t win = int64_t(batch) * window_tokens * W;       // words per window
+        const uint64_t n = uint64_t(batch) * shard_tokens * world_size * W;
+        if (n >= (uint64_t(1) << 31)) return fail(TM_ERR_SHAPE, "shard too large");
+        for (uint32_t i = 0; i < uint32_t(n); ++i) {
+            uint32_t p;
+            int64_t off;
+            if (peer_push_route(i, W, uint32_t(world_size), uint32_t(shard_tokens), tokens,
+                                window_tokens, rank, p, off))
+                out[p * win + off] = in[i];
+        }
+    } else {
+        const int64_t owin = int64_t(batch) * shard_tokens * H * dw;  // words per O window
+        for (int64_t b = 0; b < batch; ++b)
+            for (int64_t q = 0; q < tokens; ++q)
+                for (int h = 0; h < heads_per_rank; ++h) {
+                    int owner = 0;
+                    const int64_t row = peer_out_route(b, q, h, shard_tokens, shard_tokens, H,
+                                                       rank * heads_per_rank, owner);
+                    for (int w = 0; w < dw; ++w)
+                        out[owner * owin + row * dw + w] =
+                            in[((b * tokens + q) * heads_per_rank + h) * dw + w];
+                }
+    }
+    return TM_OK;
+}
+
 tm_status tm_flow_sampler_step(tm_ctx* ctx, float* x, const void* v, int32_t v_dtype, int64_t n,
                                float t_cur, float t_next, const float* eps, uint64_t seed,
                                uint64_t offset, void* x_bf16_out, void* stream) {
@@ -679,6 +994,84 @@ tm_status tm_flow_sampler_step(tm_ctx* ctx, float* x, const void* v, int32_t v_d
                               "sampler launch");
     if (st || !ctx) return st;
     return debug_check(ctx, x, n, 0, cs, "tm_flow_sampler_step");
+}
+
+tm_status tm_peer_export(tm_ctx* ctx, uint8_t* handle) {
+    if (!ctx || !handle) return fail(TM_ERR_INVALID_ARG, "null argument");
+    if (!ctx->lay.peer) return fail(TM_ERR_INVALID_ARG, "not a TM_TRANSPORT_PEER context");
+    auto range = address_range_fn();
+    if (!range) return fail(TM_ERR_CUDA, "cuMemGetAddressRange unavailable");
+    uint8_t* w = ctx->win[ctx->cfg.rank];
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (range(&base, &size, reinterpret_cast<CUdeviceptr>(w)) != CUDA_SUCCESS)
+        return fail(TM_ERR_CUDA, "cuMemGetAddressRange failed for the workspace");
+    cudaIpcMemHandle_t h;
+    tm_status st = cuda_check(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)),
+                              "cudaIpcGetMemHandle (workspace must come from cudaMalloc)");
+    if (st) return st;
+    static_assert(sizeof(h) == 64, "IPC handle size");
+    const uint64_t off = uint64_t(reinterpret_cast<uintptr_t>(w) - uintptr_t(base));
+    memcpy(handle, &h, 64);
+    memcpy(handle + 64, &off, 8);
+    return TM_OK;
+}
+
+tm_status tm_peer_connect(tm_ctx* ctx, const uint8_t* handles) {
+    if (!ctx || !handles) return fail(TM_ERR_INVALID_ARG, "null argument");
+    if (!ctx->lay.peer) return fail(TM_ERR_INVALID_ARG, "not a TM_TRANSPORT_PEER context");
+    if (ctx->connected) return fail(TM_ERR_STREAM_ORDER, "already connected");
+    for (int p = 0; p < ctx->lay.P; ++p) {
+        if (p == ctx->cfg.rank) continue;
+        cudaIpcMemHandle_t h;
+        uint64_t off = 0;
+        memcpy(&h, handles + size_t(p) * TM_PEER_HANDLE_BYTES, 64);
+        memcpy(&off, handles + size_t(p) * TM_PEER_HANDLE_BYTES + 64, 8);
+        void* base = nullptr;
+        tm_status st = cuda_check(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess),
+                                  "cudaIpcOpenMemHandle (peer window)");
+        if (st) {
+            for (void* b : ctx->ipc_opened) cudaIpcCloseMemHandle(b);
+            ctx->ipc_opened.clear();
+            return st;
+        }
+        ctx->ipc_opened.push_back(base);
+        ctx->win[p] = static_cast<uint8_t*>(base) + off;
+    }
+    ctx->connected = true;
+    return TM_OK;
+}
+
+tm_status tm_peer_connect_local(tm_ctx* const* ctxs, int32_t n) {
+    if (!ctxs || n <= 0 || n > kMaxPeers) return fail(TM_ERR_INVALID_ARG, "need 1..%d contexts", kMaxPeers);
+    for (int i = 0; i < n; ++i) {
+        const tm_ctx* c = ctxs[i];
+        if (!c || !c->lay.peer || c->cfg.world_size != n || c->cfg.rank != i)
+            return fail(TM_ERR_INVALID_ARG, "ctxs[%d] must be a TM_TRANSPORT_PEER context of rank %d "
+                                            "in a group of %d", i, i, n);
+        if (c->connected && n > 1) return fail(TM_ERR_STREAM_ORDER, "ctxs[%d] already connected", i);
+    }
+    for (int i = 0; i < n; ++i) {
+        for (int p = 0; p < n; ++p) ctxs[i]->win[p] = ctxs[p]->win[p];
+        ctxs[i]->connected = true;
+    }
+    return TM_OK;
+}
+
+tm_status tm_peer_check(tm_ctx* ctx) {
+    if (!ctx) return fail(TM_ERR_INVALID_ARG, "null ctx");
+    if (!ctx->lay.peer) return TM_OK;
+    tm_status st = cuda_check(cudaDeviceSynchronize(), "synchronize");
+    if (st) return st;
+    uint32_t err = 0;
+    uint32_t* e = &ctx->ctr(ctx->cfg.rank)->err;
+    st = cuda_check(cudaMemcpy(&err, e, 4, cudaMemcpyDeviceToHost), "peer flag readback");
+    if (st) return st;
+    if (err) {
+        cudaMemset(e, 0, 4);
+        return fail(TM_ERR_CUDA, "a peer wait timed out (a rank did not send its part)");
+    }
+    return TM_OK;
 }
 
 int32_t tm_last_launch_count(const tm_ctx* ctx) { return ctx ? ctx->launches : -1; }

@@ -49,6 +49,7 @@
 #include <mutex>
 
 #include "internal.h"
+#include "peer.cuh"
 #include "ptx.cuh"
 
 namespace tmk {
@@ -80,9 +81,20 @@ struct __align__(64) FmhaParams {
     int nseg;
     int n_tiles;                      // KV tiles of a whole unit
     int Lq, H, B;
-    int64_t o_bstride;                // tokens between batch elements of o
     float scale_log2;                 // softmax scale * log2(e)
-    uint16_t* o;                      // bf16 bits [B][Lq][H][d]
+    // Output rows (a6 scatter): query row q is stored to o_dst[q / o_rows], row
+    // q % o_rows, heads [o_h0, o_h0 + H) of o_H; P = 1: o_dst[0] = o, o_rows = Lq.
+    uint16_t* o_dst[kMaxPeers];       // bf16 bits [B][o_rows][o_H][d] each
+    int64_t o_bstride;                // rows between batch elements of an o_dst
+    int o_rows, o_H, o_h0;
+    // Peer transport: waits on the own counters before Q tiles (T=0)
+    // and before tiles of segment wait_seg (K: T=1, V: T=2); fused push of
+    // this rank's shard at kernel start; done signal at kernel end.
+    int peer, push, signal_done, wait_seg, src_rows, P, rank;
+    uint32_t epoch[3];
+    PeerCounters* own;
+    PeerCounters* done_ctr[kMaxPeers];
+    PeerPush pp;
     // persistent schedule
     int n_qpairs;                     // Q-tile pairs per (b, h)
     int whole_items;                  // R * C: items that are whole units
@@ -160,6 +172,33 @@ __device__ __forceinline__ void load_order(int q, int nkv, int& jj, int& kv) {
 // (or the piece of that unit whose KV range holds it).
 __device__ __forceinline__ bool stores_tile(const FmhaParams& p, const Item& it, int seg, int row) {
     return seg == p.store_seg && (row / kBN) % p.n_qpairs == it.qp;
+}
+
+// Destination of output row q of head h (row a6: the owner's O window when the
+// path is Ulysses-sharded over peer memory, else o itself); null for pad rows.
+template <int D>
+__device__ __forceinline__ uint16_t* out_row(const FmhaParams& p, int b, int q, int h) {
+    if (q >= p.Lq) return nullptr;
+    int own;
+    const int64_t row = peer_out_route(b, q, h, p.o_rows, p.o_bstride, p.o_H, p.o_h0, own);
+    return p.o_dst[own] + row * D;
+}
+
+// Peer transport: before the producer's first TMA read of window rows
+// [r0, r0 + n) of tensor T, wait until every source rank owning them has
+// landed its push (once per source per launch; `ok` caches satisfied ones).
+__device__ __forceinline__ void peer_ready(const FmhaParams& p, uint32_t& ok, int T, int r0, int n) {
+    if (n <= 0) return;
+    const int s0 = r0 / p.src_rows, s1 = (r0 + n - 1) / p.src_rows;
+    bool waited = false;
+    for (int s = s0; s <= s1; ++s) {
+        const uint32_t bit = 1u << (T * kMaxPeers + s);
+        if (ok & bit) continue;
+        peer_wait_ge(&p.own->arr[T][s], p.epoch[T], &p.own->err);
+        ok |= bit;
+        waited = true;
+    }
+    if (waited) fence_proxy_async_global();   // generic-proxy acquire -> TMA (async proxy) reads
 }
 
 __device__ __forceinline__ float max3(float a, float b, float c) {
@@ -246,6 +285,17 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
 
+    if (p.push) {
+        // a2 fused: all 384 threads push this rank's shard of Q, then K, then V
+        // into the owners' windows (NVLink stores), each tensor signalled as
+        // soon as the grid has stored it, so owners start on Q (and on the
+        // cached c_0 / c_{t-1} segments) while K/V of c_t are still in flight.
+        for (int T = 0; T < 3; ++T) {
+            peer_push_share(p.pp, T, threadIdx.x, kThreads);
+            peer_signal(p.pp.ctr, p.pp.own, p.pp.P, p.pp.rank, T);
+        }
+    }
+
     if (threadIdx.x == 0) {
         for (int i = 0; i < 2; ++i) {
             mbar_init(&q_full[i], 1);
@@ -285,9 +335,14 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
             int tn = 0;
             uint32_t kv_it = 0, n_item = 0;
             uint32_t pending_store = 0, store_par = 0;   // per slot: pending bit / phase parity bit
+            uint32_t ok = 0;                               // peer (tensor, source) pairs already landed
             Item it;
             for (int w = blockIdx.x; get_item(p, w, it); w += gridDim.x, ++n_item) {
                 for (int i = 0; i < 2; ++i) {
+                    if (p.peer) {
+                        const int r0 = it.qp * 2 * kBM + i * kBM;
+                        peer_ready(p, ok, 0, r0, min(kBM, p.Lq - r0));
+                    }
                     mbar_wait(&q_empty[i], (n_item & 1) ^ 1);
                     mbar_arrive_expect_tx(&q_full[i], kTileBytes);
                     for (int hf = 0; hf < D / 64; ++hf)
@@ -312,6 +367,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                         trace_ev(p, 0, tn, 5);
                     }
                     if (stores_tile(p, it, seg, row)) pending_store |= 1u << s;
+                    if (p.peer && seg == p.wait_seg) peer_ready(p, ok, 1 + kv, row, valid);
                     trace_ev(p, 0, tn, 1 + kv);
                     const CUtensorMap* m = kv ? &p.tv[seg] : &p.tk[seg];
                     mbar_arrive_expect_tx(&kv_full[s], kTileBytes);
@@ -565,7 +621,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
             const int q = it.qp * 2 * kBM + row_in_pair;
             if (!it.piece) {
                 const float inv_l = 1.f / l;
-                uint16_t* dst = p.o + ((int64_t(it.b) * p.o_bstride + q) * p.H + it.h) * D;
+                uint16_t* dst = out_row<D>(p, it.b, q, it.h);
 #pragma unroll
                 for (int c = 0; c < D; c += 32) {
                     uint32_t o[32];
@@ -576,7 +632,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                     for (int e = 0; e < 16; ++e)
                         wv[e] = pack_bf16x2(__uint_as_float(o[2 * e]) * inv_l,
                                             __uint_as_float(o[2 * e + 1]) * inv_l);
-                    if (q < p.Lq) {
+                    if (dst) {
                         uint4* d4 = reinterpret_cast<uint4*>(dst + c);
 #pragma unroll
                         for (int e = 0; e < 4; ++e)
@@ -626,7 +682,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                                 __ldcg(bs + 256 * D + 256 + row_in_pair);
                     }
                     const float inv = 1.f / wsum;
-                    uint16_t* dst = p.o + ((int64_t(it.b) * p.o_bstride + q) * p.H + it.h) * D;
+                    uint16_t* dst = out_row<D>(p, it.b, q, it.h);
 #pragma unroll 1
                     for (int c4 = 0; c4 < D / 4; c4 += 2) {
                         float4 a = make_float4(0.f, 0.f, 0.f, 0.f), bq = a;
@@ -638,7 +694,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                             a.x += ws * x.x; a.y += ws * x.y; a.z += ws * x.z; a.w += ws * x.w;
                             bq.x += ws * y.x; bq.y += ws * y.y; bq.z += ws * y.z; bq.w += ws * y.w;
                         }
-                        if (q < p.Lq)
+                        if (dst)
                             *reinterpret_cast<uint4*>(dst + 4 * c4) =
                                 make_uint4(pack_bf16x2(a.x * inv, a.y * inv), pack_bf16x2(a.z * inv, a.w * inv),
                                            pack_bf16x2(bq.x * inv, bq.y * inv), pack_bf16x2(bq.z * inv, bq.w * inv));
@@ -654,6 +710,9 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
         tc_fence_after();
         tmem_dealloc(tmem, 512);
     }
+    // a6 fused: this rank's O rows are in the owners' windows once every CTA
+    // is here; the last CTA bumps done[rank] at each owner.
+    if (p.signal_done) peer_signal(p.done_ctr, p.own, p.P, p.rank, 3);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -775,8 +834,34 @@ cudaError_t launch_fmha_sm100(const AttnProblem& pr, void* scratch, cudaStream_t
     p.H = pr.H;
     p.B = pr.B;
     p.scale_log2 = pr.scale * 1.4426950408889634f;
-    p.o = static_cast<uint16_t*>(pr.o);
+    p.o_dst[0] = static_cast<uint16_t*>(pr.o);
     p.o_bstride = pr.q_bstride > 0 ? pr.q_bstride : pr.Lq;
+    p.o_rows = int(pr.Lq);
+    p.o_H = pr.H;
+    p.o_h0 = 0;
+    p.wait_seg = -1;
+    if (const PeerAttnArgs* pa = pr.peer) {
+        if (pa->P < 1 || pa->P > kMaxPeers) return cudaErrorInvalidValue;
+        for (int r = 0; r < pa->P; ++r) p.o_dst[r] = static_cast<uint16_t*>(pa->o_dst[r]);
+        p.o_rows = int(pa->o_rows);
+        p.o_bstride = pa->o_rows;
+        p.o_H = pa->o_H;
+        p.o_h0 = pa->o_h0;
+        p.peer = pa->own != nullptr && pa->wait_seg >= 0;
+        p.wait_seg = pa->wait_seg;
+        p.src_rows = int(pa->src_rows);
+        for (int t = 0; t < 3; ++t) p.epoch[t] = pa->epoch[t];
+        p.own = pa->own;
+        p.push = pa->push;
+        p.pp = pa->pp;
+        p.signal_done = pa->signal_done;
+        for (int r = 0; r < pa->P; ++r) p.done_ctr[r] = pa->done_ctr[r];
+        p.P = pa->P;
+        p.rank = pa->rank;
+        if (p.peer && p.src_rows <= 0) return cudaErrorInvalidValue;
+        if (p.push && int64_t(p.pp.B) * p.pp.Ls * p.pp.P * p.pp.W >= (int64_t(1) << 31))
+            return cudaErrorInvalidValue;
+    }
     const int qtiles = int((pr.Lq + kBM - 1) / kBM);
     p.n_qpairs = (qtiles + 1) / 2;
     // Persistent schedule: R whole rounds over C CTAs, then the T tail units

@@ -8,6 +8,49 @@ namespace tmk {
 
 constexpr int kMaxSegments = 5;   // {c_0, c_{t-1}, c_t}; f4 audio windows need up to 5
 constexpr int kMaxPersistentCtas = 160;   // persistent grid cap (B200: 148 SMs)
+constexpr int kMaxPeers = 8;      // peer transport: one NVSwitch node
+
+// ---------------------------------------------------------------- peer transport
+// The Ulysses exchange over NVLink peer memory instead of NCCL: each
+// rank's workspace holds a WINDOW that every rank of the group maps (CUDA IPC,
+// or plain pointers for ranks sharing a process).  Window layout:
+//   PeerCounters (4 KiB) | Q [B][Lc][Hl][d] | K [B][Lw][Hl][d] | V [B][Lw][Hl][d] | O [B][Ls][H][d]
+// (Lw = max(Lc, Lr); Ls = shard tokens).  Senders STORE into the owners'
+// windows and bump the owners' monotone counters with release semantics;
+// receivers acquire-poll their own counters against a host-tracked epoch.
+struct PeerCounters {
+    uint32_t arr[3][kMaxPeers];   // tensor T (0 Q, 1 K, 2 V) from source rank s: pushes landed
+    uint32_t done[kMaxPeers];     // source rank s finished writing this rank's O rows / copy barrier
+    uint32_t ticket[4];           // local last-CTA tickets (push T = 0..2, done = 3); zero between launches
+    uint32_t err;                 // nonzero: a device-side wait timed out (see tm_peer_check)
+};
+static_assert(sizeof(PeerCounters) <= 4096, "counter block");
+
+// One rank's push of up to three sequence-shard tensors to the head owners.
+struct PeerPush {
+    const void* src[3] = {nullptr, nullptr, nullptr};   // local [B][Ls][H][d]; null = not pushed
+    void* dst[3][kMaxPeers] = {};                       // peer p's window of tensor T [B][Lw][Hl][d]
+    PeerCounters* ctr[kMaxPeers] = {};                  // peer p's counters (ctr[rank] = own)
+    PeerCounters* own = nullptr;                        // own counters (tickets, err)
+    int B = 1, P = 1, rank = 0, W = 0;                  // W: 16-B words per (token, head block)
+    int64_t Ls = 0, L = 0, Lw = 0;                      // shard tokens, valid tokens, window rows
+};
+
+// Peer side of one attention launch (row a5 between a2 and a6).
+struct PeerAttnArgs {
+    PeerCounters* own = nullptr;      // waits: Q (T=0) before each Q tile, K/V (T=1,2) before
+    uint32_t epoch[3] = {0, 0, 0};    //   each tile of the window segment `wait_seg`
+    int wait_seg = -1;
+    int64_t src_rows = 0;             // window row r came from source rank r / src_rows
+    bool push = false;                // fused: this kernel pushes `pp` before attending
+    PeerPush pp;
+    void* o_dst[kMaxPeers] = {};      // owner p's O window [B][Ls][H][d]
+    int64_t o_rows = 0;               // output row q goes to owner q / o_rows, row q % o_rows
+    int o_H = 0, o_h0 = 0;            // heads of a row in the O window; this rank's first head
+    bool signal_done = false;         // bump every owner's done[rank] when all CTAs finished
+    PeerCounters* done_ctr[kMaxPeers] = {};
+    int P = 1, rank = 0;
+};
 
 // One contiguous K/V segment in token-major layout [B][len][H][d].
 struct Segment {
@@ -31,6 +74,7 @@ struct AttnProblem {
     // written to these [B][len][H][d] buffers (the cache slot) by the kernel.
     void* store_k = nullptr;
     void* store_v = nullptr;
+    const PeerAttnArgs* peer = nullptr;   // peer transport (sm100 path only)
 };
 
 // Launchers; return cudaSuccess or the launch error.  `launches` is
@@ -67,5 +111,23 @@ cudaError_t launch_pack_heads_to_peers(const void* src, void* dst, int B, int64_
                                        int* launches);
 cudaError_t launch_unpack_peers_to_seq(const void* src, void* dst, int B, int64_t Ls, int H,
                                        int P, int d, int esize, cudaStream_t s, int* launches);
+
+// Peer transport kernels (peer.cu).
+// push: every rank's shard tensors -> owners' windows, then arr[T][rank] += 1 at each owner.
+cudaError_t launch_peer_push(const PeerPush& pp, cudaStream_t s, int* launches);
+// recv_o: wait done[s] >= epoch for all s, then copy the O window [B][Ls][H][d] to o
+// (rows of global token >= L zeroed: shard padding).
+cudaError_t launch_peer_recv_o(PeerCounters* own, uint32_t epoch, int P, const void* owin, void* o,
+                               int B, int64_t Ls, int64_t L, int rank, int row_bytes,
+                               cudaStream_t s, int* launches);
+// ref_store: wait arr[1..2][s] >= epoch for all s, copy K/V windows ([B][Lw][Hl][d], rows
+// < Lr) into the cache reference region ([B][Lr][Hl][d]), then done[rank] += 1 at every peer.
+cudaError_t launch_peer_ref_store(PeerCounters* const* ctr, PeerCounters* own, uint32_t epoch,
+                                  int P, int rank, const void* kwin, const void* vwin, void* kref,
+                                  void* vref, int B, int64_t Lw, int64_t Lr, int row_bytes,
+                                  cudaStream_t s, int* launches);
+// wait: done[s] >= epoch for all s (a barrier after ref_store).
+cudaError_t launch_peer_wait_done(PeerCounters* own, uint32_t epoch, int P, cudaStream_t s,
+                                  int* launches);
 
 }  // namespace tmk

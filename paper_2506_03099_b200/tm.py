@@ -19,6 +19,9 @@ STATUS = {0: "TM_OK", 1: "TM_ERR_INVALID_ARG", 2: "TM_ERR_SHAPE", 3: "TM_ERR_DEG
           4: "TM_ERR_STREAM_ORDER", 5: "TM_ERR_REF_IMMUTABLE", 6: "TM_ERR_NONFINITE",
           7: "TM_ERR_UNSUPPORTED", 8: "TM_ERR_CUDA", 9: "TM_ERR_NCCL"}
 TM_BF16, TM_FP32 = 0, 1
+TM_TRANSPORT_NCCL, TM_TRANSPORT_PEER = 0, 1
+TM_PHASE_SEND, TM_PHASE_ATTEND, TM_PHASE_RECV, TM_PHASE_ALL = 1, 2, 4, 7
+TM_PEER_HANDLE_BYTES = 72
 
 
 class TMError(RuntimeError):
@@ -33,13 +36,15 @@ class tm_config(ctypes.Structure):
                 ("num_layers", ctypes.c_int32), ("num_steps", ctypes.c_int32),
                 ("batch", ctypes.c_int32), ("dtype", ctypes.c_int32),
                 ("softmax_scale", ctypes.c_float), ("world_size", ctypes.c_int32),
-                ("rank", ctypes.c_int32), ("device", ctypes.c_int32)]
+                ("rank", ctypes.c_int32), ("device", ctypes.c_int32),
+                ("transport", ctypes.c_int32)]
 
 
 def make_config(heads, head_dim, ref_tokens, chunk_tokens, num_layers=1, num_steps=1, batch=1,
-                dtype=TM_BF16, softmax_scale=0.0, world_size=1, rank=0, device=0) -> tm_config:
+                dtype=TM_BF16, softmax_scale=0.0, world_size=1, rank=0, device=0,
+                transport=TM_TRANSPORT_NCCL) -> tm_config:
     return tm_config(heads, head_dim, ref_tokens, chunk_tokens, num_layers, num_steps, batch,
-                     dtype, softmax_scale, world_size, rank, device)
+                     dtype, softmax_scale, world_size, rank, device, transport)
 
 
 def _load():
@@ -61,6 +66,13 @@ def _load():
         "tm_stream_reset": ([V], i32),
         "tm_kvcache_put_reference": ([V, i32, i32, V, V, V], i32),
         "tm_chunk_attention": ([V, i32, i32, i64, V, V, V, V, V], i32),
+        "tm_chunk_attention_phases": ([V, i32, i32, i64, V, V, V, V, ctypes.c_uint32, V], i32),
+        "tm_kvcache_put_reference_phases": ([V, i32, i32, V, V, ctypes.c_uint32, V], i32),
+        "tm_peer_export": ([V, ctypes.c_char_p], i32),
+        "tm_peer_connect": ([V, ctypes.c_char_p], i32),
+        "tm_peer_connect_local": ([P(V), i32], i32),
+        "tm_peer_check": ([V], i32),
+        "tm_peer_route_host": ([i32, V, V, i32, i64, i64, i64, i32, i32, i32, i32, i32], i32),
         "tm_kvcache_slot_ptr": ([V, i32, i32, i64, P(V), P(V)], i32),
         "tm_kvcache_ref_ptr": ([V, i32, i32, P(V), P(V)], i32),
         "tm_flow_euler_step": ([V, V, V, i32, i64, ctypes.c_float, V], i32),
@@ -87,7 +99,9 @@ EXPORTED = ("tm_version", "tm_last_error", "tm_kvcache_bytes", "tm_workspace_byt
             "tm_kvcache_put_reference", "tm_chunk_attention", "tm_kvcache_slot_ptr",
             "tm_kvcache_ref_ptr", "tm_flow_euler_step", "tm_ulysses_shuffle_host",
             "tm_window_attention", "tm_flow_sampler_step", "tm_audio_scratch_bytes",
-            "tm_audio_cross_attention",
+            "tm_audio_cross_attention", "tm_chunk_attention_phases",
+            "tm_kvcache_put_reference_phases", "tm_peer_export", "tm_peer_connect",
+            "tm_peer_connect_local", "tm_peer_check", "tm_peer_route_host",
             "tm_last_launch_count",
             "tm_kernel_variant")
 
@@ -159,6 +173,37 @@ def tm_chunk_attention(ctx, layer, step, chunk, q, k, v, o, stream=None) -> None
                                   _stream(stream)))
 
 
+def tm_chunk_attention_phases(ctx, layer, step, chunk, q, k, v, o, phases, stream=None) -> None:
+    _check(lib.tm_chunk_attention_phases(ctx, layer, step, chunk, _ptr(q), _ptr(k), _ptr(v),
+                                         _ptr(o), phases, _stream(stream)))
+
+
+def tm_kvcache_put_reference_phases(ctx, layer, step, k, v, phases, stream=None) -> None:
+    _check(lib.tm_kvcache_put_reference_phases(ctx, layer, step, _ptr(k), _ptr(v), phases,
+                                               _stream(stream)))
+
+
+def tm_peer_export(ctx) -> bytes:
+    buf = ctypes.create_string_buffer(TM_PEER_HANDLE_BYTES)
+    _check(lib.tm_peer_export(ctx, buf))
+    return buf.raw
+
+
+def tm_peer_connect(ctx, handles) -> None:
+    """handles: the world_size exported handles, in rank order."""
+    blob = b"".join(handles)
+    _check(lib.tm_peer_connect(ctx, blob))
+
+
+def tm_peer_connect_local(ctxs) -> None:
+    arr = (ctypes.c_void_p * len(ctxs))(*ctxs)
+    _check(lib.tm_peer_connect_local(arr, len(ctxs)))
+
+
+def tm_peer_check(ctx) -> None:
+    _check(lib.tm_peer_check(ctx))
+
+
 def tm_kvcache_slot_ptr(ctx, layer, step, chunk):
     k, v = ctypes.c_void_p(), ctypes.c_void_p()
     _check(lib.tm_kvcache_slot_ptr(ctx, layer, step, chunk, ctypes.byref(k), ctypes.byref(v)))
@@ -207,6 +252,14 @@ def tm_ulysses_shuffle_host(mode, src, dst, batch, shard_tokens, tokens, heads_p
                                        tokens, heads_per_rank, world_size, head_dim, elem_bytes))
 
 
+def tm_peer_route_host(mode, src, dst, batch, shard_tokens, tokens, window_tokens, heads_per_rank,
+                       world_size, rank, head_dim, elem_bytes) -> None:
+    """src/dst: contiguous numpy arrays (host memory)."""
+    _check(lib.tm_peer_route_host(mode, src.ctypes.data, dst.ctypes.data, batch, shard_tokens,
+                                  tokens, window_tokens, heads_per_rank, world_size, rank,
+                                  head_dim, elem_bytes))
+
+
 def tm_last_launch_count(ctx) -> int:
     return lib.tm_last_launch_count(ctx)
 
@@ -224,10 +277,10 @@ class ChunkAttention:
 
     def __init__(self, heads, head_dim, ref_tokens, chunk_tokens, num_layers=1, num_steps=1,
                  batch=1, dtype=TM_BF16, softmax_scale=0.0, world_size=1, rank=0, device=0,
-                 nccl_id=None):
+                 nccl_id=None, transport=TM_TRANSPORT_NCCL):
         import torch
         self.cfg = make_config(heads, head_dim, ref_tokens, chunk_tokens, num_layers, num_steps,
-                               batch, dtype, softmax_scale, world_size, rank, device)
+                               batch, dtype, softmax_scale, world_size, rank, device, transport)
         self.cache_bytes = tm_kvcache_bytes(self.cfg)
         self.ws_bytes = tm_workspace_bytes(self.cfg)
         if self.cache_bytes == 0 or self.ws_bytes == 0:
@@ -262,6 +315,35 @@ class ChunkAttention:
     def attend(self, layer, step, chunk, q, k, v, o, stream=None):
         tm_chunk_attention(self.ctx, layer, step, chunk, q, k, v, o, stream)
         return o
+
+    def attend_phases(self, layer, step, chunk, q, k, v, o, phases, stream=None):
+        tm_chunk_attention_phases(self.ctx, layer, step, chunk, q, k, v, o, phases, stream)
+        return o
+
+    def put_reference_phases(self, layer, step, k, v, phases, stream=None):
+        tm_kvcache_put_reference_phases(self.ctx, layer, step, k, v, phases, stream)
+
+    # -- peer transport group setup (TM_TRANSPORT_PEER)
+    def export_handle(self) -> bytes:
+        return tm_peer_export(self.ctx)
+
+    def connect(self, handles):
+        tm_peer_connect(self.ctx, handles)
+
+    def connect_dist(self, group=None):
+        """All-gather the window handles over torch.distributed and map the peers'."""
+        import torch.distributed as dist
+        mine = self.export_handle()
+        allh = [None] * dist.get_world_size(group)
+        dist.all_gather_object(allh, mine, group=group)
+        self.connect(allh)
+
+    @staticmethod
+    def connect_local(cas):
+        tm_peer_connect_local([c.ctx for c in cas])
+
+    def check(self):
+        tm_peer_check(self.ctx)
 
     def slot_ptr(self, layer, step, chunk):
         return tm_kvcache_slot_ptr(self.ctx, layer, step, chunk)

@@ -29,7 +29,7 @@ def test_library_exports_every_declared_symbol():
 
 
 def test_version():
-    assert tm.tm_version() == 100
+    assert tm.tm_version() == 101
 
 
 def wan512(**kw):
@@ -61,14 +61,16 @@ def test_cache_bytes_720_and_alignment():
 @pytest.mark.parametrize("bad", [
     dict(head_dim=96), dict(head_dim=0), dict(heads=0), dict(ref_tokens=0), dict(chunk_tokens=-1),
     dict(world_size=3), dict(world_size=2, rank=2), dict(dtype=5), dict(num_steps=0),
-    dict(batch=0), dict(softmax_scale=-1.0)])
+    dict(batch=0), dict(softmax_scale=-1.0), dict(transport=2),
+    dict(transport=tm.TM_TRANSPORT_PEER, dtype=tm.TM_FP32),
+    dict(transport=tm.TM_TRANSPORT_PEER, heads=40, world_size=10)])
 def test_invalid_configs_are_rejected(bad):
     c = wan512(**bad)
     assert tm.tm_kvcache_bytes(c) == 0
     assert tm.tm_workspace_bytes(c) == 0
     with pytest.raises(tm.TMError) as e:
         tm.tm_attn_init(c, None, 1024, 1 << 40, 1024, 1 << 20)
-    assert e.value.status in (1, 2)
+    assert e.value.status in (1, 2, 7)
 
 
 def test_workspace_sizes():
@@ -107,3 +109,22 @@ def test_cache_bytes_table1_variants():
     c = tm.make_config(40, 128, 1024, 7168, 40, 4)
     per_tok = 40 * 128 * 2
     assert tm.tm_kvcache_bytes(c) == 160 * (2 * 1024 * per_tok + 4 * 7168 * per_tok)
+
+
+def test_peer_workspace_layout():
+    """TM_TRANSPORT_PEER: the workspace ends in the peer window: 4 KiB of
+    counters, Q/K/V windows [B][max(Lc,Lr)][H/P][d] and the O window
+    [B][ceil(Lc/P)][H][d], each 1024-B aligned; no NCCL staging."""
+    al = lambda x: (x + 1023) // 1024 * 1024
+    scratch = 1024 + al(160 * (256 * 128 + 512) * 4 + 160 * 4)
+    for P in (1, 2, 8):
+        c = wan512(world_size=P, transport=tm.TM_TRANSPORT_PEER)
+        win = 4096 + 3 * al(3072 * (40 // P) * 128 * 2) + al(-(-3072 // P) * 40 * 128 * 2)
+        assert tm.tm_workspace_bytes(c) == scratch + win
+    c = tm.make_config(40, 128, 2025, 6075, 40, 2, world_size=8, transport=tm.TM_TRANSPORT_PEER)
+    win = 4096 + 3 * al(6075 * 5 * 128 * 2) + al(760 * 40 * 128 * 2)
+    assert tm.tm_workspace_bytes(c) == scratch + win
+    # Lr > Lc: the K/V windows also carry the reference push
+    c = tm.make_config(4, 64, 500, 100, 1, 1, world_size=2, transport=tm.TM_TRANSPORT_PEER)
+    scratch64 = 1024 + al(160 * (256 * 64 + 512) * 4 + 160 * 4)
+    assert tm.tm_workspace_bytes(c) == scratch64 + 4096 + 3 * al(500 * 2 * 64 * 2) + al(50 * 4 * 64 * 2)

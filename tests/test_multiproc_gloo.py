@@ -129,3 +129,105 @@ def test_shuffle_host_roundtrip_and_padding():
     assert (blk2[P - 1, :, L - (P - 1) * Ls:] == 0).all()   # the padded tail rows
     with pytest.raises(tm.TMError):
         tm.tm_ulysses_shuffle_host(0, x, blk, B, Ls, L, Hl, P, 3, 4)   # 12-byte rows
+
+
+# ------------------------------------------------------------------ peer transport (TM_TRANSPORT_PEER)
+
+def _peer_worker(rank, world, port, H, d, Lr, Lc, errq):
+    """The peer transport's routing at world size 2 over gloo: each rank
+    routes its sequence shard into P window images with the library's own
+    index map (tm_peer_route_host mode 0 = the device push), the images go to
+    their owners (all_to_all) and are overlaid; the oracle runs on the
+    owned heads; the output rows are routed to their token owners (mode 1 =
+    the attention epilogue's scatter) and overlaid again.  Every rank's O
+    shard must equal the unsharded oracle rows exactly."""
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        rng = np.random.default_rng(2506030991)
+        q, k, v = (rng.standard_normal((Lc, H, d)).astype(np.float32) for _ in range(3))
+        kr, vr = (rng.standard_normal((Lr, H, d)).astype(np.float32) for _ in range(2))
+        P, Hl = world, H // world
+        Ls, Lrs = -(-Lc // P), -(-Lr // P)
+        Lw = max(Lc, Lr)
+
+        def shard(x, L, S):
+            out = np.full((S, H, d), np.nan, dtype=np.float32)    # padding must never be read
+            lo, hi = rank * S, min(rank * S + S, L)
+            if hi > lo:
+                out[: hi - lo] = x[lo:hi]
+            return out
+
+        def push(x, L, S):
+            img = np.zeros((P, 1, Lw, Hl, d), dtype=np.float32)
+            tm.tm_peer_route_host(0, shard(x, L, S), img, 1, S, L, Lw, Hl, P, rank, d, 4)
+            return _a2a(img).sum(axis=0)[0]          # disjoint rows from each source
+
+        qw, kw, vw = (push(x, Lc, Ls) for x in (q, k, v))
+        hs = slice(rank * Hl, rank * Hl + Hl)
+        for got, full in ((qw, q), (kw, k), (vw, v)):
+            assert (got[:Lc] == full[:, hs]).all(), "window layout mismatch"
+        krw, vrw = (push(x, Lr, Lrs)[:Lr] for x in (kr, vr))
+        assert (krw == kr[:, hs]).all() and (vrw == vr[:, hs]).all()
+        for prev in (None, (kw[:Lc], vw[:Lc])):
+            oh = oracle.stream_attention(qw[:Lc], krw, vrw, None if prev is None else prev[0],
+                                         None if prev is None else prev[1], kw[:Lc], vw[:Lc])
+            img = np.zeros((P, 1, Ls, H, d), dtype=np.float32)
+            tm.tm_peer_route_host(1, np.ascontiguousarray(oh.astype(np.float32)[None]), img, 1, Ls,
+                                  Lc, Lw, Hl, P, rank, d, 4)
+            o_shard = _a2a(img).sum(axis=0)[0]     # disjoint head blocks from each source
+            ref = oracle.stream_attention(q, kr, vr, None if prev is None else k,
+                                          None if prev is None else v, k, v)
+            lo, hi = rank * Ls, min(rank * Ls + Ls, Lc)
+            assert np.abs(o_shard[: hi - lo] - ref[lo:hi].astype(np.float32)).max() == 0.0
+            assert (o_shard[hi - lo:] == 0).all()
+        dist.barrier()
+        dist.destroy_process_group()
+    except BaseException as e:  # report to the parent
+        errq.put(f"rank {rank}: {type(e).__name__}: {e}")
+        raise
+
+
+@pytest.mark.parametrize("H,d,Lr,Lc", [(4, 8, 5, 7), (2, 4, 9, 4), (6, 16, 17, 33)])
+def test_peer_routes_world2_gloo(H, d, Lr, Lc):
+    oracle.build()
+    ctx = mp.get_context("spawn")
+    errq = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_peer_worker, args=(r, 2, port, H, d, Lr, Lc, errq))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+    errs = []
+    while not errq.empty():
+        errs.append(errq.get())
+    assert all(p.exitcode == 0 for p in procs), errs
+
+
+def test_peer_route_host_single_process():
+    """mode 0 over every source rank rebuilds each owner's head slice exactly
+    (P=3, ragged L, padding never routed); mode 1 over every source fills
+    each owner's O window exactly once."""
+    rng = np.random.default_rng(3)
+    B, P, Hl, d, L = 2, 3, 2, 8, 10
+    Ls, H, Lw = -(-L // P), P * Hl, 12
+    full = rng.standard_normal((B, L, H, d)).astype(np.float32)
+    win = np.zeros((P, B, Lw, Hl, d), dtype=np.float32)
+    for r in range(P):
+        sh = np.full((B, Ls, H, d), np.nan, dtype=np.float32)
+        n = min(Ls, L - r * Ls)
+        sh[:, :n] = full[:, r * Ls: r * Ls + n]
+        tm.tm_peer_route_host(0, sh, win, B, Ls, L, Lw, Hl, P, r, d, 4)
+    for p in range(P):
+        assert (win[p][:, :L] == full[:, :, p * Hl:(p + 1) * Hl]).all()
+        assert (win[p][:, L:] == 0).all()
+    out = np.full((P, B, Ls, H, d), -1.0, dtype=np.float32)
+    for r in range(P):
+        tm.tm_peer_route_host(1, np.ascontiguousarray(full[:, :, r * Hl:(r + 1) * Hl]), out, B, Ls,
+                              L, Lw, Hl, P, r, d, 4)
+    flat = out.transpose(1, 0, 2, 3, 4).reshape(B, P * Ls, H, d)
+    assert (flat[:, :L] == full).all()
+    assert (flat[:, L:] == -1.0).all()          # pad rows are the receive kernel's job
