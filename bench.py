@@ -305,6 +305,10 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-extras", action="store_true",
                     help="skip the SURVEY Sec 8(f) rows (f1 window, f2 sampler, f4 audio)")
+    ap.add_argument("--transport", default=None, choices=["peer", "nccl"],
+                    help="Ulysses exchange for N>1 (default peer: fused NVLink peer-memory "
+                         "push/scatter; nccl: pack + ncclAlltoAll + unpack).  At N=1 the "
+                         "default is the direct path; --transport peer runs a 1-rank group.")
     ap.add_argument("--stream-chunks", type=int, default=4,
                     help="BJ.configs[3] streaming measurement over this many chunks (0: off)")
     args = ap.parse_args()
@@ -332,13 +336,22 @@ def main():
     P = world
     Lc_s, Lr_s = -(-Lc // P), -(-Lr // P)
     NL = args.layers
+    transport = args.transport or ("peer" if P > 1 else "nccl")
+    tcode = tm.TM_TRANSPORT_PEER if transport == "peer" else tm.TM_TRANSPORT_NCCL
     nccl_id = None
-    if P > 1:
+    if P > 1 and transport == "nccl":
         obj = [tm.tm_get_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
-    ca = tm.ChunkAttention(H, d, Lr, Lc, num_layers=NL, num_steps=1, world_size=P, rank=rank,
-                           device=local, nccl_id=nccl_id)
+
+    def make_ctx(layers, steps):
+        cx = tm.ChunkAttention(H, d, Lr, Lc, num_layers=layers, num_steps=steps, world_size=P,
+                               rank=rank, device=local, nccl_id=nccl_id, transport=tcode)
+        if transport == "peer" and P > 1:
+            cx.connect_dist()          # CUDA IPC handles of the windows, all-gathered
+        return cx
+
+    ca = make_ctx(NL, 1)
     stream = torch.cuda.current_stream()
     g = torch.Generator(device="cuda").manual_seed(2506030990 + 1000 + rank)
     bf = torch.bfloat16
@@ -402,14 +415,24 @@ def main():
     gpu_launches = launches[0]
 
     # ---------------------------------------------------------------- attention kernel alone
-    # K/V pre-placed in the cache slot (zero-copy append) so each call is one
-    # attention-kernel launch; per-call CUDA events on the launching stream.
+    # P = 1: K/V pre-placed in the cache slot (zero-copy append) so each call is
+    # one attention-kernel launch.  P > 1: the whole call (peer: the fused
+    # push + attention + scatter kernel and the receive kernel; nccl: pack,
+    # all-to-all, unpack, attention, pack, all-to-all, unpack).  Per-call CUDA
+    # events on the launching stream.
     kev = []
+    zc = P == 1 and transport == "nccl"
+
+    def kv_for(i, layer):
+        if zc:
+            return ca.slot_ptr(layer, 0, chunk[layer])
+        return sets[i % NB][1], sets[i % NB][2]
+
     barrier()
     for i in range(3):          # fill the launch queue so no event pair spans a host gap
         layer = i % NL
         chunk[layer] += 1
-        kp, vp = ca.slot_ptr(layer, 0, chunk[layer])
+        kp, vp = kv_for(i, layer)
         ca.attend(layer, 0, chunk[layer], sets[i % NB][0], kp, vp, outs[i % NB], stream)
     w2 = time.time()
     for i in range(args.steps):
@@ -417,7 +440,7 @@ def main():
         layer = i % NL
         chunk[layer] += 1
         q = sets[i % NB][0]
-        kp, vp = ca.slot_ptr(layer, 0, chunk[layer])
+        kp, vp = kv_for(i, layer)
         a.record(stream)
         ca.attend(layer, 0, chunk[layer], q, kp, vp, outs[i % NB], stream)
         b.record(stream)
@@ -498,8 +521,7 @@ def main():
         # every (layer, step) of a WAN-2.1-14B DiT (40 blocks x 2 NFE), the
         # reference cached once per (layer, step), one Euler update per step.
         NLs, NS = 40, 2
-        sc = tm.ChunkAttention(H, d, Lr, Lc, num_layers=NLs, num_steps=NS, world_size=P,
-                               rank=rank, device=local, nccl_id=nccl_id)
+        sc = make_ctx(NLs, NS)
         for layer in range(NLs):
             for st in range(NS):
                 sc.put_reference(layer, st, kref, vref, stream)
@@ -533,7 +555,7 @@ def main():
     ms_step = ms_total / args.steps
     value = fl * args.steps / (ms_total * 1e-3) / 1e12
     peak, peak_sus, peak_src = measured_peaks()
-    achieved = fl / (k_ms * 1e-3) / 1e12
+    achieved = fl / P / (k_ms * 1e-3) / 1e12      # per GPU (each rank does 1/P of the heads)
     prof = os.path.join(ROOT, "profiles", "ncu_fmha_traffic.json")
     traffic = None
     try:
@@ -559,6 +581,7 @@ def main():
                        "chunk_tokens": Lc, "chunk_index": ">=2", "keys_attended": Lr + 2 * Lc,
                        "gflop_per_chunk_attention": fl / 1e9, "euler_elements": c["latent"],
                        "parallelism": f"ulysses-heads{P}" if P > 1 else "single-gpu",
+                       "transport": transport if (P > 1 or transport == "peer") else "none",
                        "l2": "inputs larger than L2 (8 layer caches x 4 input sets rotated)"},
             "ms_per_chunk_attention": k_ms,
             "ms_per_chunk_attention_median": k_med,
@@ -566,8 +589,10 @@ def main():
             "frac_of_bf16_peak": achieved / peak,
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak,
                          "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "tm_fmha_sm100 (tcgen05)", "peak_source": f"{peak_src} bf16 burst",
-                         "flop_per_launch": fl, "achieved_median_launch": fl / (k_med * 1e-3) / 1e12,
+                         "kernel": "tm_fmha_sm100 (tcgen05)" if zc else
+                                   f"whole call ({transport} transport: exchange + attention)",
+                         "peak_source": f"{peak_src} bf16 burst",
+                         "flop_per_launch": fl, "achieved_median_launch": fl / P / (k_med * 1e-3) / 1e12,
                          "algorithmic_bytes_per_launch": algo_bytes(c)},
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -97,11 +97,11 @@ struct __align__(64) FmhaParams {
     PeerPush pp;
     // persistent schedule
     int n_qpairs;                     // Q-tile pairs per (b, h)
-    int whole_items;                  // R * C: items that are whole units
-    int tail_pieces;                  // T * S
-    int splits;                       // S
-    float* part;                      // split partials: per piece [d/4][256] float4 + m[256] + l[256]
-    int* counters;                    // per tail unit, zero between launches
+    int rounds;                       // R: whole units per CTA (unit c + k*C, k < R)
+    int sk_units;                     // T = U - R*C tail units, spread stream-K style ...
+    int sk_ctas;                      // ... over the first G' CTAs (contiguous tile ranges)
+    float* part;                      // piece partials: per slot [d/4][256] float4 + m[256] + l[256]
+    int* counters;                    // per split unit (indexed by its first CTA), zero between launches
     unsigned long long* trace;        // debug timeline (TM_TRACE=1), CTA 0 only; may be null
 };
 
@@ -120,27 +120,51 @@ __device__ __forceinline__ void trace_ev(const FmhaParams& p, int role, int& n, 
 }
 
 struct Item {
-    int b, h, qp, lo, hi, piece, tail_unit, split;
+    int b, h, qp, lo, hi, piece;
+    int cfirst, npieces, pidx;        // split units: first CTA, piece count, this piece's index
 };
 
-__device__ __forceinline__ bool get_item(const FmhaParams& p, int w, Item& it) {
+// Tail (stream-K) CTA holding tile x of the flattened tail space of W tiles
+// split into G contiguous ranges [floor(c*W/G), floor((c+1)*W/G)).
+__device__ __forceinline__ int sk_cta_of(long long x, long long W, int G) {
+    return int(((x + 1) * G - 1) / W);
+}
+// Piece k of a split unit whose first CTA is cf is held by CTA cf + k.  Piece
+// 0 is CTA cf's LAST item and merges; piece k >= 1 is CTA cf+k's FIRST item and
+// leaves its partial in slot cf + k (one partial slot per CTA suffices).
+
+// Item k of this CTA: first its R whole units c, c+C, ...; then its range of
+// the tail's tiles (stream-K: each of the first G' CTAs takes an equal
+// contiguous range of the T tail units' KV tiles, so the last wave is
+// balanced to within a tile; a unit cut by range ends becomes pieces merged
+// by whichever piece finishes last).
+__device__ __forceinline__ bool get_item(const FmhaParams& p, int k, Item& it) {
     int unit;
-    if (w < p.whole_items) {
-        unit = w;
+    const int c = blockIdx.x;
+    it.cfirst = 0;
+    it.npieces = 1;
+    it.pidx = 0;
+    if (k < p.rounds) {
+        unit = c + k * int(gridDim.x);
         it.lo = 0;
         it.hi = p.n_tiles;
         it.piece = 0;
-        it.tail_unit = 0;
-        it.split = 0;
     } else {
-        const int pw = w - p.whole_items;
-        if (pw >= p.tail_pieces) return false;
-        it.tail_unit = pw / p.splits;
-        it.split = pw % p.splits;
-        unit = p.whole_items + it.tail_unit;
-        it.lo = int((long long)it.split * p.n_tiles / p.splits);
-        it.hi = int((long long)(it.split + 1) * p.n_tiles / p.splits);
-        it.piece = p.splits > 1;
+        if (c >= p.sk_ctas) return false;
+        const long long n = p.n_tiles, W = (long long)p.sk_units * n, G = p.sk_ctas;
+        const long long start = c * W / G, end = (c + 1) * W / G;
+        const long long u = start / n + (k - p.rounds);
+        const long long ub = u * n;
+        if (start >= end || ub >= end) return false;
+        it.lo = int((start > ub ? start : ub) - ub);
+        it.hi = int((end < ub + n ? end : ub + n) - ub);
+        it.piece = it.lo > 0 || it.hi < n;
+        if (it.piece) {
+            it.cfirst = sk_cta_of(ub, W, p.sk_ctas);
+            it.npieces = sk_cta_of(ub + n - 1, W, p.sk_ctas) - it.cfirst + 1;
+            it.pidx = c - it.cfirst;
+        }
+        unit = p.rounds * int(gridDim.x) + int(u);
     }
     it.qp = unit % p.n_qpairs;
     const int bh = unit / p.n_qpairs;
@@ -280,7 +304,6 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
     uint64_t* s_free = o_done + 2;           // [1]  S buffer loaded into registers
     uint64_t* store_done = s_free + 1;       // [kStages] append-store finished reading a slot
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(store_done + kStages);
-    int* merge_flag = reinterpret_cast<int*>(tmem_holder + 1);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -337,7 +360,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
             uint32_t pending_store = 0, store_par = 0;   // per slot: pending bit / phase parity bit
             uint32_t ok = 0;                               // peer (tensor, source) pairs already landed
             Item it;
-            for (int w = blockIdx.x; get_item(p, w, it); w += gridDim.x, ++n_item) {
+            for (int w = 0; get_item(p, w, it); ++w, ++n_item) {
                 for (int i = 0; i < 2; ++i) {
                     if (p.peer) {
                         const int r0 = it.qp * 2 * kBM + i * kBM;
@@ -388,7 +411,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
             int tn = 0;
             uint32_t g = 0;
             Item it;
-            for (int w = blockIdx.x; get_item(p, w, it); w += gridDim.x)
+            for (int w = 0; get_item(p, w, it); ++w)
                 for (int j = it.lo; j < it.hi; ++j, ++g)
                     for (int i = 0; i < 2; ++i) {
                         mbar_wait(&s_full[i], g & 1);
@@ -402,7 +425,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
             uint32_t kv_it = 0;
             int tn = 0;
             Item it;
-            for (int w = blockIdx.x; get_item(p, w, it); w += gridDim.x) {
+            for (int w = 0; get_item(p, w, it); ++w) {
                 const int nkv = it.hi - it.lo;
                 for (int q = 0; q < 2 * nkv; ++q, ++kv_it) {
                     int jj, kv;
@@ -444,7 +467,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
         uint32_t kv_it = 0, g = 0, n_item = 0, s_count = 0;
         int tn = 0;
         Item it;
-        for (int w = blockIdx.x; get_item(p, w, it); w += gridDim.x, ++n_item) {
+        for (int w = 0; get_item(p, w, it); ++w, ++n_item) {
             const int nkv = it.hi - it.lo;
             if (warp == 9) {
                 for (int j = 0; j < nkv; ++j) {
@@ -502,7 +525,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
         int tn = 0;
         const bool tr = (lane == 0);   // every softmax warp records (equal trace overhead)
         Item it;
-        for (int w = blockIdx.x; get_item(p, w, it); w += gridDim.x, ++n_item) {
+        for (int w = 0; get_item(p, w, it); ++w, ++n_item) {
             float m_run = -INFINITY, l = 0.f;
             for (int j = it.lo; j < it.hi; ++j, ++g) {
                 int seg, row, valid;
@@ -641,10 +664,12 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                 }
                 tc_fence_before();
                 mbar_arrive(&o_empty[i]);
-            } else {
-                // split piece: unnormalised O, running max m (log2 units) and l
+            } else if (it.pidx > 0) {
+                // piece k >= 1 of a split unit (this CTA's first item): unnormalised
+                // O, running max m (log2 units) and l to this CTA's partial slot,
+                // then count it in for the unit's merger (piece 0).
                 constexpr int kPieceFloats = 256 * D + 512;
-                float* base = p.part + size_t(it.tail_unit * p.splits + it.split) * kPieceFloats;
+                float* base = p.part + size_t(blockIdx.x) * kPieceFloats;
                 float4* po = reinterpret_cast<float4*>(base);
 #pragma unroll
                 for (int c = 0; c < D; c += 32) {
@@ -663,44 +688,73 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                 base[256 * D + 256 + row_in_pair] = l;
                 __threadfence();
                 softmax_bar();
-                if (threadIdx.x == 0)
-                    *merge_flag = atomicAdd(&p.counters[it.tail_unit], 1) == p.splits - 1;
-                softmax_bar();
-                const int do_merge = *merge_flag;
-                softmax_bar();          // everyone has read the flag before it is reused
-                if (do_merge) {
-                    // last piece to finish: merge all S pieces in piece order.
-                    __threadfence();
-                    const float* b0 = p.part + size_t(it.tail_unit * p.splits) * kPieceFloats;
-                    float mstar = -INFINITY;
-                    for (int s = 0; s < p.splits; ++s)
-                        mstar = fmaxf(mstar, __ldcg(b0 + size_t(s) * kPieceFloats + 256 * D + row_in_pair));
-                    float wsum = 0.f;
-                    for (int s = 0; s < p.splits; ++s) {
-                        const float* bs = b0 + size_t(s) * kPieceFloats;
-                        wsum += ex2(__ldcg(bs + 256 * D + row_in_pair) - mstar) *
-                                __ldcg(bs + 256 * D + 256 + row_in_pair);
-                    }
-                    const float inv = 1.f / wsum;
-                    uint16_t* dst = out_row<D>(p, it.b, q, it.h);
-#pragma unroll 1
-                    for (int c4 = 0; c4 < D / 4; c4 += 2) {
-                        float4 a = make_float4(0.f, 0.f, 0.f, 0.f), bq = a;
-                        for (int s = 0; s < p.splits; ++s) {
-                            const float* bs = b0 + size_t(s) * kPieceFloats;
-                            const float ws = ex2(__ldcg(bs + 256 * D + row_in_pair) - mstar);
-                            const float4 x = __ldcg(reinterpret_cast<const float4*>(bs) + c4 * 256 + row_in_pair);
-                            const float4 y = __ldcg(reinterpret_cast<const float4*>(bs) + (c4 + 1) * 256 + row_in_pair);
-                            a.x += ws * x.x; a.y += ws * x.y; a.z += ws * x.z; a.w += ws * x.w;
-                            bq.x += ws * y.x; bq.y += ws * y.y; bq.z += ws * y.z; bq.w += ws * y.w;
-                        }
-                        if (dst)
-                            *reinterpret_cast<uint4*>(dst + 4 * c4) =
-                                make_uint4(pack_bf16x2(a.x * inv, a.y * inv), pack_bf16x2(a.z * inv, a.w * inv),
-                                           pack_bf16x2(bq.x * inv, bq.y * inv), pack_bf16x2(bq.z * inv, bq.w * inv));
-                    }
-                    if (threadIdx.x == 0) p.counters[it.tail_unit] = 0;   // ready for the next launch
+                if (threadIdx.x == 0) atomicAdd(&p.counters[it.cfirst], 1);
+            } else {
+                // piece 0 of a split unit = this CTA's LAST item (its range ends
+                // inside the unit), so O_i stays in TMEM: wait until the other
+                // pieces (first items of the next CTAs, long finished) are in,
+                // then merge them into the TMEM accumulator in piece order
+                // (deterministic) and store the output.  No partial of its own.
+                constexpr int kPieceFloats = 256 * D + 512;
+                if (threadIdx.x == 0) {
+                    volatile int* ctr = p.counters + it.cfirst;
+                    const long long t0 = clock64();
+                    while (*ctr != it.npieces - 1)
+                        if (clock64() - t0 > (1ll << 33)) __trap();
+                    *ctr = 0;                               // ready for the next launch
                 }
+                __threadfence();
+                softmax_bar();
+                auto piece_base = [&](int k) {
+                    return p.part + size_t(it.cfirst + k) * kPieceFloats;
+                };
+                float mstar = m_run;
+                for (int k = 1; k < it.npieces; ++k)
+                    mstar = fmaxf(mstar, __ldcg(piece_base(k) + 256 * D + row_in_pair));
+                const float w0 = ex2(m_run - mstar);
+                float wsum = w0 * l;
+                for (int k = 1; k < it.npieces; ++k) {
+                    const float* bs = piece_base(k);
+                    wsum += ex2(__ldcg(bs + 256 * D + row_in_pair) - mstar) *
+                            __ldcg(bs + 256 * D + 256 + row_in_pair);
+                }
+                const float inv = 1.f / wsum;
+                uint16_t* dst = out_row<D>(p, it.b, q, it.h);
+#pragma unroll 1
+                for (int c = 0; c < D; c += 32) {
+                    uint32_t o[32];
+                    tmem_ld32(tOi + c, o);
+                    tmem_wait_ld();
+                    float acc[32];
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) acc[e] = __uint_as_float(o[e]) * w0;
+                    for (int k = 1; k < it.npieces; ++k) {
+                        const float* bs = piece_base(k);
+                        const float wk = ex2(__ldcg(bs + 256 * D + row_in_pair) - mstar);
+                        float4 x[8];
+#pragma unroll
+                        for (int e = 0; e < 8; ++e)
+                            x[e] = __ldcg(reinterpret_cast<const float4*>(bs) + ((c >> 2) + e) * 256 + row_in_pair);
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) {
+                            acc[4 * e] += wk * x[e].x;
+                            acc[4 * e + 1] += wk * x[e].y;
+                            acc[4 * e + 2] += wk * x[e].z;
+                            acc[4 * e + 3] += wk * x[e].w;
+                        }
+                    }
+                    if (dst) {
+                        uint4* d4 = reinterpret_cast<uint4*>(dst + c);
+#pragma unroll
+                        for (int e = 0; e < 4; ++e)
+                            d4[e] = make_uint4(pack_bf16x2(acc[8 * e] * inv, acc[8 * e + 1] * inv),
+                                               pack_bf16x2(acc[8 * e + 2] * inv, acc[8 * e + 3] * inv),
+                                               pack_bf16x2(acc[8 * e + 4] * inv, acc[8 * e + 5] * inv),
+                                               pack_bf16x2(acc[8 * e + 6] * inv, acc[8 * e + 7] * inv));
+                    }
+                }
+                tc_fence_before();
+                mbar_arrive(&o_empty[i]);
             }
         }
     }
@@ -864,26 +918,38 @@ cudaError_t launch_fmha_sm100(const AttnProblem& pr, void* scratch, cudaStream_t
     }
     const int qtiles = int((pr.Lq + kBM - 1) / kBM);
     p.n_qpairs = (qtiles + 1) / 2;
-    // Persistent schedule: R whole rounds over C CTAs, then the T tail units
-    // split S ways along the KV axis (S*T <= C).
+    // Persistent schedule: R whole rounds over C CTAs, then the T tail units'
+    // T*n KV tiles in equal contiguous ranges over G' CTAs (stream-K), pieces
+    // of at least kMinPiece tiles.  P = 2, 4, 8 head shards leave T >= C/2
+    // (240, 120, 60 units of 56 tiles at WAN-512), where whole-unit or
+    // even-split tails idle ~19% of the machine in the last wave.
+    // TM_SCHED_SPLIT=1 (A/B only): G' = T * floor(C / T), the earlier even split.
+    constexpr int kMinPiece = 4;
     const int C = sm_count() < kMaxPersistentCtas ? sm_count() : kMaxPersistentCtas;
     const int U = pr.B * pr.H * p.n_qpairs;
     const int R = U / C;
     const int T = U - R * C;
-    int S = 1;
+    int G = 0;
     if (T > 0) {
-        S = C / T;
-        if (S > tiles) S = tiles;
-        if (S < 1) S = 1;
+        static const bool split_sched = [] {
+            const char* e = getenv("TM_SCHED_SPLIT");
+            return e && *e && strcmp(e, "0") != 0;
+        }();
+        const long long by_len = (long long)T * tiles / kMinPiece;
+        G = C;
+        if (split_sched) G = T * (C / T > tiles ? tiles : C / T);
+        if (G > by_len) G = int(by_len);
+        if (G < T) G = T;                 // every tail unit at least whole (short units)
+        if (G > C) G = C;
     }
-    p.whole_items = R * C;
-    p.tail_pieces = T * S;
-    p.splits = S;
+    p.rounds = R;
+    p.sk_units = T;
+    p.sk_ctas = G;
     p.trace = trace;
     p.part = static_cast<float*>(scratch);
     p.counters = reinterpret_cast<int*>(static_cast<uint8_t*>(scratch) +
                                         size_t(kMaxPersistentCtas) * (256 * size_t(pr.d) + 512) * 4);
-    const int grid = R > 0 ? C : T * S;
+    const int grid = R > 0 ? C : G;
     cudaError_t e = pr.d == 128 ? launch_d<128>(p, grid, stream) : launch_d<64>(p, grid, stream);
     if (e == cudaSuccess && launches) ++*launches;
     return e;

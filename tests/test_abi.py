@@ -74,7 +74,7 @@ def test_invalid_configs_are_rejected(bad):
 
 
 def test_workspace_sizes():
-    # bf16: debug flag + split-KV scratch for <= 160 persistent CTAs (partials + counters)
+    # bf16: debug flag + split-KV scratch: 1 partial slot per persistent CTA (<= 160) + counters
     scratch = 160 * (256 * 128 + 512) * 4 + 160 * 4
     assert tm.tm_workspace_bytes(wan512()) == 1024 + (scratch + 1023) // 1024 * 1024
     assert tm.tm_workspace_bytes(wan512(dtype=tm.TM_FP32)) == 1024
