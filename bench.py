@@ -325,11 +325,21 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # Test hook (not a benchmark mode): TM_BENCH_ONE_DEVICE=1 puts every rank on
+    # cuda:0 with a gloo process group, so the N>1 flow (peer windows over CUDA
+    # IPC, barriers, max over ranks) can be exercised on a one-GPU box; the
+    # time-sliced numbers it prints are meaningless.
+    one_dev = os.environ.get("TM_BENCH_ONE_DEVICE") == "1"
+    if one_dev:
+        local = 0
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_dev:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2506_03099_b200 import tm
 
     H, d, Lr, Lc = c["H"], c["d"], c["Lr"], c["Lc"]
@@ -394,7 +404,7 @@ def main():
     def max_over_ranks(x):
         if P == 1:
             return x
-        t = torch.tensor([x], device="cuda", dtype=torch.float64)
+        t = torch.tensor([x], device="cpu" if one_dev else "cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 

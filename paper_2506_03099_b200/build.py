@@ -42,7 +42,8 @@ def _nccl_default() -> str:
 
 
 def _flags():
-    extra = ["-DTM_TRACE_ENABLED"] if os.environ.get("TM_TRACE_BUILD") == "1" else []
+    tb = os.environ.get("TM_TRACE_BUILD")
+    extra = {"1": ["-DTM_TRACE_ENABLED"], "spans": ["-DTM_SPANS_ENABLED"]}.get(tb, [])
     # TM_EXTRA_DEFINES="A=1 B": tuning variants for tools/ A/B builds only
     extra += ["-D" + d for d in os.environ.get("TM_EXTRA_DEFINES", "").split()]
     return extra + ARCH + ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC",

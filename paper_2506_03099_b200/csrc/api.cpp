@@ -416,7 +416,7 @@ tm_status tm_attn_init(const tm_config* cfg, const uint8_t* nccl_id, void* cache
     const char* dbg = getenv("TM_DEBUG");
     c->debug = dbg && *dbg && strcmp(dbg, "0") != 0;
     if (const char* tp = getenv("TM_TRACE")) {
-        if (*tp && cudaMalloc(&c->trace, 13 * 4096 * 8) == cudaSuccess) c->trace_path = tp;
+        if (*tp && cudaMalloc(&c->trace, kTraceWords * 8) == cudaSuccess) c->trace_path = tp;
     }
     if (L.peer) {
         c->win[cfg->rank] = c->ws + L.win_off;
@@ -718,13 +718,13 @@ tm_status tm_chunk_attention_phases(tm_ctx* ctx, int32_t layer, int32_t step, in
         pr.seg[pr.nseg++] = Segment{kslot, vslot, Ly.Lc};
     }
 
-    if (ctx->trace) cudaMemsetAsync(ctx->trace, 0, 13 * 4096 * 8, cs);
+    if (ctx->trace) cudaMemsetAsync(ctx->trace, 0, kTraceWords * 8, cs);
     cudaError_t e = cf.dtype == TM_BF16 ? launch_fmha_sm100(pr, ctx->scratch(), cs, &ctx->launches, ctx->trace)
                                         : launch_fmha_fp32(pr, cs, &ctx->launches);
     st = cuda_check(e, "attention kernel launch");
     if (st) return st;
     if (ctx->trace) {   // debug only: dump CTA 0's timeline (synchronises)
-        std::vector<unsigned long long> h(13 * 4096);
+        std::vector<unsigned long long> h(kTraceWords);
         cudaMemcpyAsync(h.data(), ctx->trace, h.size() * 8, cudaMemcpyDeviceToHost, cs);
         cudaStreamSynchronize(cs);
         if (FILE* f = fopen(ctx->trace_path.c_str(), "ab")) {

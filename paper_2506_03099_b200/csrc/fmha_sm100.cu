@@ -119,6 +119,19 @@ __device__ __forceinline__ void trace_ev(const FmhaParams& p, int role, int& n, 
 #endif
 }
 
+// Per-CTA span stamps (globaltimer ns) after the role timelines; debug build only.
+__device__ __forceinline__ void trace_span(const FmhaParams& p, int j, long long val = -1) {
+#if defined(TM_TRACE_ENABLED) || defined(TM_SPANS_ENABLED)
+    if (p.trace != nullptr) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        p.trace[13 * kTraceCap + blockIdx.x * 8 + j] = val >= 0 ? (unsigned long long)val : t;
+    }
+#else
+    (void)p; (void)j; (void)val;
+#endif
+}
+
 struct Item {
     int b, h, qp, lo, hi, piece;
     int cfirst, npieces, pidx;        // split units: first CTA, piece count, this piece's index
@@ -308,6 +321,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
 
+    if (threadIdx.x == 0) trace_span(p, 0);
     if (p.push) {
         // a2 fused: all 384 threads push this rank's shard of Q, then K, then V
         // into the owners' windows (NVLink stores), each tensor signalled as
@@ -526,6 +540,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
         const bool tr = (lane == 0);   // every softmax warp records (equal trace overhead)
         Item it;
         for (int w = 0; get_item(p, w, it); ++w, ++n_item) {
+            if (threadIdx.x == 0 && n_item == 1) trace_span(p, 2);   // first item's epilogue done
             float m_run = -INFINITY, l = 0.f;
             for (int j = it.lo; j < it.hi; ++j, ++g) {
                 int seg, row, valid;
@@ -533,6 +548,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                 uint32_t r[kBN];
                 mbar_wait(&s_full[i], g & 1);
                 if (tr) trace_ev(p, 5 + warp, tn, 20);
+                if (threadIdx.x == 0 && g == 0) trace_span(p, 1);
                 tc_fence_after();
 #pragma unroll
                 for (int c = 0; c < kBN; c += 32) tmem_ld32(tS + c, r + c);
@@ -696,6 +712,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                 // then merge them into the TMEM accumulator in piece order
                 // (deterministic) and store the output.  No partial of its own.
                 constexpr int kPieceFloats = 256 * D + 512;
+                if (threadIdx.x == 0) trace_span(p, 4);
                 if (threadIdx.x == 0) {
                     volatile int* ctr = p.counters + it.cfirst;
                     const long long t0 = clock64();
@@ -705,6 +722,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                 }
                 __threadfence();
                 softmax_bar();
+                if (threadIdx.x == 0) trace_span(p, 5);
                 auto piece_base = [&](int k) {
                     return p.part + size_t(it.cfirst + k) * kPieceFloats;
                 };
@@ -757,9 +775,14 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                 mbar_arrive(&o_empty[i]);
             }
         }
+        if (threadIdx.x == 0) {
+            trace_span(p, 6, g);
+            trace_span(p, 7, n_item);
+        }
     }
     tc_fence_before();
     __syncthreads();
+    if (threadIdx.x == 0) trace_span(p, 3);
     if (warp == 9) {
         tc_fence_after();
         tmem_dealloc(tmem, 512);

@@ -9,6 +9,10 @@ namespace tmk {
 constexpr int kMaxSegments = 5;   // {c_0, c_{t-1}, c_t}; f4 audio windows need up to 5
 constexpr int kMaxPersistentCtas = 160;   // persistent grid cap (B200: 148 SMs)
 constexpr int kMaxPeers = 8;      // peer transport: one NVSwitch node
+// Debug trace buffer (TM_TRACE build): 13 roles x 4096 clock64 events of CTA 0,
+// then 8 words per CTA: globaltimer at entry, first S seen, second item start,
+// exit, merge wait begin / end; tiles and items of the CTA.
+constexpr int kTraceWords = 13 * 4096 + 8 * kMaxPersistentCtas;
 
 // ---------------------------------------------------------------- peer transport
 // The Ulysses exchange over NVLink peer memory instead of NCCL: each

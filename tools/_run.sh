@@ -1,0 +1,4 @@
+export TM_BENCH_ONE_DEVICE=1
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --steps 4 --warmup 3 --stream-chunks 2 --no-e2e > gpurun_out/bench2proc.log 2>&1
+echo "rc=$?"
+tail -c 1500 gpurun_out/bench2proc.log

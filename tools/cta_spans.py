@@ -1,0 +1,63 @@
+#!/usr/bin/env python
+"""Per-CTA spans of one chunk-attention launch (TM_TRACE build: globaltimer at
+CTA entry, first S seen by the softmax, second item start, exit).  Shows the
+fixed per-launch costs (prologue latency, tail spread) at a given head count:
+    SWEEP_H=5 python tools/cta_spans.py      (one rank's heads at P = 8)
+Rebuilds libtm.so with -DTM_SPANS_ENABLED; rebuild normally afterwards."""
+import os
+import statistics
+import subprocess
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+PATH = "/tmp/tm_spans.bin"
+if os.path.exists(PATH):
+    os.unlink(PATH)
+os.environ["TM_TRACE"] = PATH
+os.environ["TM_TRACE_BUILD"] = "spans"      # per-CTA stamps only (no role timeline)
+subprocess.check_call([sys.executable, "-m", "paper_2506_03099_b200.build"], cwd=ROOT,
+                      stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+import torch  # noqa: E402
+
+from paper_2506_03099_b200 import tm  # noqa: E402
+
+cfg = os.environ.get("SWEEP_CFG", "512")
+H, d, Lr, Lc = (40, 128, 1024, 3072) if cfg == "512" else (40, 128, 2025, 6075)
+H = int(os.environ.get("SWEEP_H", H))
+ca = tm.ChunkAttention(H, d, Lr, Lc, 1, 1)
+g = torch.Generator(device="cuda").manual_seed(1)
+mk = lambda L: torch.randn(L, H, d, device="cuda", dtype=torch.bfloat16, generator=g)
+ca.put_reference(0, 0, mk(Lr), mk(Lr))
+for t in range(1, 6):
+    q, k, v = mk(Lc), mk(Lc), mk(Lc)
+    o = torch.empty_like(q)
+    ca.attend(0, 0, t, q, k, v, o)
+torch.cuda.synchronize()
+W = 13 * 4096 + 8 * 160
+allw = np.fromfile(PATH, dtype=np.uint64).reshape(-1, W)[-1][13 * 4096:].reshape(160, 8)
+allw = allw[allw[:, 0] != 0].astype(np.int64)
+raw = allw[:, :6]
+t0 = raw[:, 0].min()
+rel = np.where(raw != 0, (raw - t0) / 1000.0, np.nan)          # us
+print(f"cfg={cfg} H={H}: {len(raw)} CTAs, kernel span {rel[:, 3].max():.1f} us")
+for j, name in enumerate(["entry", "first S", "item 2 start", "exit", "merge wait", "merge go"]):
+    col = rel[:, j][raw[:, j] != 0]
+    if len(col):
+        print(f"  {name:13s} min {col.min():7.1f}  median {statistics.median(col):7.1f}  max {col.max():7.1f} us")
+busy = rel[:, 3] - rel[:, 0]
+print(f"  CTA busy     min {busy.min():7.1f}  median {statistics.median(busy):7.1f}  max {busy.max():7.1f} us")
+wait = rel[:, 5] - rel[:, 4]
+ok = ~np.isnan(wait)
+if ok.any():
+    print(f"  merge wait   n {ok.sum()}  median {np.median(wait[ok]):6.1f}  max {wait[ok].max():6.1f} us")
+tiles, items = allw[:, 6], allw[:, 7]
+print(f"  tiles/CTA min {tiles.min()} max {tiles.max()}; items/CTA {sorted(set(items.tolist()))}")
+order = np.argsort(rel[:, 3])
+print("  slowest 8 CTAs: (cta, tiles, items, exit us, merge wait us)")
+for c in order[-8:]:
+    print(f"    {c:4d} {tiles[c]:4d} {items[c]:3d} {rel[c, 3]:7.1f} {wait[c] if ok[c] else float('nan'):6.1f}")
+rate = tiles / (rel[:, 3] - rel[:, 1])
+print(f"  tiles/us per CTA: min {rate.min():.3f} median {np.median(rate):.3f} max {rate.max():.3f}")
