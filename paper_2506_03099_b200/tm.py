@@ -268,6 +268,43 @@ def tm_kernel_variant(ctx) -> str:
     return lib.tm_kernel_variant(ctx).decode()
 
 
+_cudart_lib = None
+
+
+def _cudart():
+    global _cudart_lib
+    if _cudart_lib is None:
+        _cudart_lib = ctypes.CDLL("libcudart.so.12")
+        _cudart_lib.cudaMalloc.argtypes = [ctypes.POINTER(ctypes.c_void_p), ctypes.c_size_t]
+        _cudart_lib.cudaFree.argtypes = [ctypes.c_void_p]
+        _cudart_lib.cudaMemset.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t]
+        _cudart_lib.cudaSetDevice.argtypes = [ctypes.c_int]
+        _cudart_lib.cudaDeviceSynchronize.argtypes = []
+    return _cudart_lib
+
+
+def _cuda_malloc(nbytes, device):
+    """Zeroed plain cudaMalloc block (IPC-exportable), or None if cudart is unavailable."""
+    try:
+        rt = _cudart()
+    except OSError:
+        return None
+    rt.cudaSetDevice(device)
+    p = ctypes.c_void_p()
+    if rt.cudaMalloc(ctypes.byref(p), nbytes) != 0:
+        raise TMError(8, f"cudaMalloc of {nbytes} bytes for the peer workspace failed")
+    rt.cudaMemset(p, 0, nbytes)
+    rt.cudaDeviceSynchronize()
+    return p.value
+
+
+def _cuda_free(ptr):
+    try:
+        _cudart().cudaFree(ptr)
+    except OSError:
+        pass
+
+
 class ChunkAttention:
     """Owns a tm_ctx plus torch-allocated cache and workspace (plumbing only).
 
@@ -289,9 +326,19 @@ class ChunkAttention:
         # torch's caching allocator returns >= 512-B aligned blocks; over-allocate
         # by 1 KiB and offset to honour the cache's 1024-B alignment.
         self._cache = torch.empty(self.cache_bytes + 1024, dtype=torch.uint8, device=dev)
-        self._ws = torch.zeros(self.ws_bytes + 1024, dtype=torch.uint8, device=dev)
+        self._ws_raw = None
+        if transport == TM_TRANSPORT_PEER and world_size > 1:
+            # The peer window (in the workspace) is shared through CUDA IPC, which
+            # needs a cudaMalloc allocation: a torch block may come from VMM
+            # (expandable segments), which IPC cannot export.
+            self._ws_raw = _cuda_malloc(self.ws_bytes + 1024, device)
+        if self._ws_raw is None:
+            self._ws = torch.zeros(self.ws_bytes + 1024, dtype=torch.uint8, device=dev)
+            ws_base = self._ws.data_ptr()
+        else:
+            ws_base = self._ws_raw
         self.cache_ptr = (self._cache.data_ptr() + 1023) // 1024 * 1024
-        self.ws_ptr = (self._ws.data_ptr() + 1023) // 1024 * 1024
+        self.ws_ptr = (ws_base + 1023) // 1024 * 1024
         self.ctx = tm_attn_init(self.cfg, nccl_id, self.cache_ptr, self.cache_bytes,
                                 self.ws_ptr, self.ws_bytes)
 
@@ -299,6 +346,9 @@ class ChunkAttention:
         if getattr(self, "ctx", None):
             tm_attn_destroy(self.ctx)
             self.ctx = None
+        if getattr(self, "_ws_raw", None):
+            _cuda_free(self._ws_raw)
+            self._ws_raw = None
 
     def __del__(self):
         try:
