@@ -69,6 +69,9 @@ constexpr int kHalfBytes = 128 * 128;   // one 64-column (128 B) half of a 128-r
 constexpr uint32_t kColS = 0, kColP = 128, kColO = 256;
 // Lazy running-max threshold (log2 units): weights stay <= 2^8 between rescales.
 constexpr float kLazyLog2 = 8.f;
+// Fused peer push: the producer releases K/V after this many tile loads at the
+// latest (about 3 tiles of compute after Q arrived; the pushes have drained).
+constexpr int kKvReleaseLoads = 6;
 
 struct __align__(64) FmhaParams {
     CUtensorMap tq;                   // Q [B][Lq][H][d]
@@ -323,14 +326,24 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
 
     if (threadIdx.x == 0) trace_span(p, 0);
     if (p.push) {
-        // a2 fused: all 384 threads push this rank's shard of Q, then K, then V
-        // into the owners' windows (NVLink stores), each tensor signalled as
-        // soon as the grid has stored it, so owners start on Q (and on the
-        // cached c_0 / c_{t-1} segments) while K/V of c_t are still in flight.
-        for (int T = 0; T < 3; ++T) {
-            peer_push_share(p.pp, T, threadIdx.x, kThreads);
-            peer_signal(p.pp.ctr, p.pp.own, p.pp.P, p.pp.rank, T);
+        // a2 fused.  All 384 threads store this rank's shard of Q into the owners'
+        // windows (NVLink stores).  Then warp 10 alone releases Q (a system-scope
+        // fence waits until the CTA's stores have landed; the grid's last CTA
+        // bumps arr[0][rank] at every owner) while the other 11 warps store K
+        // and V.  K/V are released later by the producer (peer_kv_release), once
+        // their stores have long drained, so no role waits for NVLink: owners
+        // start on Q and the cached c_0 / c_{t-1} segments while c_t is in flight.
+        peer_push_share(p.pp, 0, threadIdx.x, kThreads);
+        __syncthreads();
+        if (warp == 10) {
+            if (lane == 0) peer_release(p.pp.ctr, p.pp.own, p.pp.P, p.pp.rank, 0);
+            __syncwarp();
+        } else {
+            const int t = threadIdx.x < 320 ? threadIdx.x : threadIdx.x - 32;
+            peer_push_share(p.pp, 1, t, kThreads - 32);
+            peer_push_share(p.pp, 2, t, kThreads - 32);
         }
+        __syncthreads();
     }
 
     if (threadIdx.x == 0) {
@@ -373,6 +386,8 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
             uint32_t kv_it = 0, n_item = 0;
             uint32_t pending_store = 0, store_par = 0;   // per slot: pending bit / phase parity bit
             uint32_t ok = 0;                               // peer (tensor, source) pairs already landed
+            bool kv_released = !p.push;                    // fused push: K/V not yet released
+            int n_loads = 0;
             Item it;
             for (int w = 0; get_item(p, w, it); ++w, ++n_item) {
                 for (int i = 0; i < 2; ++i) {
@@ -404,6 +419,13 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                         trace_ev(p, 0, tn, 5);
                     }
                     if (stores_tile(p, it, seg, row)) pending_store |= 1u << s;
+                    // Release this CTA's K/V pushes before the first wait on K/V
+                    // (own rank included) or after a few loads, whichever first:
+                    // by then the stores have drained and the fence is cheap.
+                    if (!kv_released && (seg == p.wait_seg || ++n_loads > kKvReleaseLoads)) {
+                        peer_release(p.pp.ctr, p.pp.own, p.pp.P, p.pp.rank, 1);
+                        kv_released = true;
+                    }
                     if (p.peer && seg == p.wait_seg) peer_ready(p, ok, 1 + kv, row, valid);
                     trace_ev(p, 0, tn, 1 + kv);
                     const CUtensorMap* m = kv ? &p.tv[seg] : &p.tk[seg];
@@ -413,6 +435,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                                     hf * 64, it.h, row, it.b);
                 }
             }
+            if (!kv_released) peer_release(p.pp.ctr, p.pp.own, p.pp.P, p.pp.rank, 1);
         }
       } else if (warp == 10) {
 #ifdef TM_TRACE_ENABLED
@@ -948,7 +971,8 @@ cudaError_t launch_fmha_sm100(const AttnProblem& pr, void* scratch, cudaStream_t
     // even-split tails idle ~19% of the machine in the last wave.
     // TM_SCHED_SPLIT=1 (A/B only): G' = T * floor(C / T), the earlier even split.
     constexpr int kMinPiece = 4;
-    const int C = sm_count() < kMaxPersistentCtas ? sm_count() : kMaxPersistentCtas;
+    int C = sm_count() < kMaxPersistentCtas ? sm_count() : kMaxPersistentCtas;
+    if (pr.max_ctas > 0 && pr.max_ctas < C) C = pr.max_ctas;
     const int U = pr.B * pr.H * p.n_qpairs;
     const int R = U / C;
     const int T = U - R * C;

@@ -79,6 +79,7 @@ struct AttnProblem {
     void* store_k = nullptr;
     void* store_v = nullptr;
     const PeerAttnArgs* peer = nullptr;   // peer transport (sm100 path only)
+    int max_ctas = 0;                     // persistent grid cap (0: one CTA per SM)
 };
 
 // Launchers; return cudaSuccess or the launch error.  `launches` is
@@ -118,7 +119,8 @@ cudaError_t launch_unpack_peers_to_seq(const void* src, void* dst, int B, int64_
 
 // Peer transport kernels (peer.cu).
 // push: every rank's shard tensors -> owners' windows, then arr[T][rank] += 1 at each owner.
-cudaError_t launch_peer_push(const PeerPush& pp, cudaStream_t s, int* launches);
+// `ctas` = grid size (0: one CTA per SM).
+cudaError_t launch_peer_push(const PeerPush& pp, cudaStream_t s, int* launches, int ctas = 0);
 // recv_o: wait done[s] >= epoch for all s, then copy the O window [B][Ls][H][d] to o
 // (rows of global token >= L zeroed: shard padding).
 cudaError_t launch_peer_recv_o(PeerCounters* own, uint32_t epoch, int P, const void* owin, void* o,

@@ -94,10 +94,10 @@ __global__ void peer_wait_kernel(PeerCounters* own, uint32_t epoch, int P) {
 
 }  // namespace
 
-cudaError_t launch_peer_push(const PeerPush& pp, cudaStream_t s, int* launches) {
+cudaError_t launch_peer_push(const PeerPush& pp, cudaStream_t s, int* launches, int ctas) {
     if (pp.P < 1 || pp.P > kMaxPeers || pp.W <= 0) return cudaErrorInvalidValue;
     if (int64_t(pp.B) * pp.Ls * pp.P * pp.W >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
-    peer_push_kernel<<<sm_count_peer(), kThreads, 0, s>>>(pp);
+    peer_push_kernel<<<ctas > 0 ? ctas : sm_count_peer(), kThreads, 0, s>>>(pp);
     if (launches) ++*launches;
     return cudaGetLastError();
 }

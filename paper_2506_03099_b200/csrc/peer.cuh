@@ -80,6 +80,28 @@ __device__ __forceinline__ void peer_signal(PeerCounters* const* ctr, PeerCounte
     }
 }
 
+// Single-thread release for the whole CTA: the caller's CTA-wide barrier
+// (bar.sync) already orders every thread's window stores before this thread,
+// so its system-scope fence covers them (cumulativity); then the grid's last
+// CTA bumps arr[T][rank] at every owner (`which` = 1 releases K and V).
+__device__ __forceinline__ void peer_release(PeerCounters* const* ctr, PeerCounters* own, int P,
+                                             int rank, int which) {
+    fence_acq_rel_sys();
+    const uint32_t prev = atomicAdd(&own->ticket[which], 1u);
+    if (prev == gridDim.x - 1) {
+        own->ticket[which] = 0;
+        fence_acq_rel_sys();
+        for (int p = 0; p < P; ++p) {
+            if (which == 0) {
+                red_release_sys_add(&ctr[p]->arr[0][rank], 1u);
+            } else {
+                red_release_sys_add(&ctr[p]->arr[1][rank], 1u);
+                red_release_sys_add(&ctr[p]->arr[2][rank], 1u);
+            }
+        }
+    }
+}
+
 // This CTA's share of pushing tensor T of `pp`: the local shard [B][Ls][H][d]
 // is read linearly as 16-B words; the words of head block p of token t go to
 // rank p's window row rank*Ls + t (tokens >= L are shard padding, dropped).
