@@ -46,7 +46,10 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <tuple>
+#include <vector>
 
 #include "internal.h"
 #include "peer.cuh"
@@ -102,7 +105,8 @@ struct __align__(64) FmhaParams {
     int n_qpairs;                     // Q-tile pairs per (b, h)
     int rounds;                       // R: whole units per CTA (unit c + k*C, k < R)
     int sk_units;                     // T = U - R*C tail units, spread stream-K style ...
-    int sk_ctas;                      // ... over the first G' CTAs (contiguous tile ranges)
+    int sk_ctas;                      // ... over the first G' CTAs (contiguous tile ranges):
+    int sk_bound[kMaxPersistentCtas + 1];   // CTA c takes tail tiles [sk_bound[c], sk_bound[c+1])
     float* part;                      // piece partials: per slot [d/4][256] float4 + m[256] + l[256]
     int* counters;                    // per split unit (indexed by its first CTA), zero between launches
     unsigned long long* trace;        // debug timeline (TM_TRACE=1), CTA 0 only; may be null
@@ -140,20 +144,26 @@ struct Item {
     int cfirst, npieces, pidx;        // split units: first CTA, piece count, this piece's index
 };
 
-// Tail (stream-K) CTA holding tile x of the flattened tail space of W tiles
-// split into G contiguous ranges [floor(c*W/G), floor((c+1)*W/G)).
-__device__ __forceinline__ int sk_cta_of(long long x, long long W, int G) {
-    return int(((x + 1) * G - 1) / W);
+// Tail (stream-K) CTA holding tile x of the flattened tail space: the c with
+// sk_bound[c] <= x < sk_bound[c+1] (ranges are non-empty; binary search).
+__device__ __forceinline__ int sk_cta_of(const FmhaParams& p, int x) {
+    int lo = 0, hi = p.sk_ctas - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (p.sk_bound[mid] <= x) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
 }
 // Piece k of a split unit whose first CTA is cf is held by CTA cf + k.  Piece
 // 0 is CTA cf's LAST item and merges; piece k >= 1 is CTA cf+k's FIRST item and
 // leaves its partial in slot cf + k (one partial slot per CTA suffices).
 
 // Item k of this CTA: first its R whole units c, c+C, ...; then its range of
-// the tail's tiles (stream-K: each of the first G' CTAs takes an equal
-// contiguous range of the T tail units' KV tiles, so the last wave is
-// balanced to within a tile; a unit cut by range ends becomes pieces merged
-// by whichever piece finishes last).
+// the tail's tiles (stream-K: each of the first G' CTAs takes a contiguous
+// range of the T tail units' KV tiles, sized on the host so that tiles plus a
+// per-item cost are equal (fmha_sm100 launcher); a unit cut by range ends
+// becomes pieces, merged by piece 0).
 __device__ __forceinline__ bool get_item(const FmhaParams& p, int k, Item& it) {
     int unit;
     const int c = blockIdx.x;
@@ -167,17 +177,17 @@ __device__ __forceinline__ bool get_item(const FmhaParams& p, int k, Item& it) {
         it.piece = 0;
     } else {
         if (c >= p.sk_ctas) return false;
-        const long long n = p.n_tiles, W = (long long)p.sk_units * n, G = p.sk_ctas;
-        const long long start = c * W / G, end = (c + 1) * W / G;
-        const long long u = start / n + (k - p.rounds);
-        const long long ub = u * n;
+        const int n = p.n_tiles;
+        const int start = p.sk_bound[c], end = p.sk_bound[c + 1];
+        const int u = start / n + (k - p.rounds);
+        const int ub = u * n;
         if (start >= end || ub >= end) return false;
-        it.lo = int((start > ub ? start : ub) - ub);
-        it.hi = int((end < ub + n ? end : ub + n) - ub);
+        it.lo = (start > ub ? start : ub) - ub;
+        it.hi = (end < ub + n ? end : ub + n) - ub;
         it.piece = it.lo > 0 || it.hi < n;
         if (it.piece) {
-            it.cfirst = sk_cta_of(ub, W, p.sk_ctas);
-            it.npieces = sk_cta_of(ub + n - 1, W, p.sk_ctas) - it.cfirst + 1;
+            it.cfirst = sk_cta_of(p, ub);
+            it.npieces = sk_cta_of(p, ub + n - 1) - it.cfirst + 1;
             it.pidx = c - it.cfirst;
         }
         unit = p.rounds * int(gridDim.x) + int(u);
@@ -800,7 +810,9 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
         }
         if (threadIdx.x == 0) {
             trace_span(p, 6, g);
-            trace_span(p, 7, n_item);
+            uint32_t smid;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            trace_span(p, 7, n_item | (long long)smid << 16);
         }
     }
     tc_fence_before();
@@ -900,6 +912,69 @@ cudaError_t launch_d(const FmhaParams& p, int grid, cudaStream_t stream) {
 
 }  // namespace
 
+// Host: cut the tail's W = T*n tiles into at most C contiguous ranges whose
+// cost -- tiles plus kItemCost per item after a range's first -- is as equal
+// as possible (a CTA that switches to another unit pays its epilogue / partial
+// write, the next Q load and pipeline refill, and as the unit's merger the
+// partial reads: ~6 tiles' time measured, profiles/r1_v8_cta_spans.txt).  A
+// greedy fill under budget B, the smallest B (bisection) that needs <= C
+// ranges.  Pieces shorter than kMinPiece are not started at a range's end.
+// TM_SCHED_SPLIT=1 (A/B only): plain equal ranges.  Returns G'.
+int tail_bounds(int T, int n, int C, int min_piece, int* bound) {
+    static const float item_cost = [] {
+        const char* e = getenv("TM_SCHED_ITEM_COST");
+        return e ? float(atof(e)) : 3.f;
+    }();
+    static const bool split_sched = [] {
+        const char* e = getenv("TM_SCHED_SPLIT");
+        return e && *e && strcmp(e, "0") != 0;
+    }();
+    const int W = T * n;
+    int G = C;
+    if (G > W / min_piece) G = W / min_piece;
+    if (G < T) G = T;
+    if (G > C) G = C;
+    if (split_sched || item_cost <= 0.f) {
+        for (int c = 0; c <= G; ++c) bound[c] = int((long long)c * W / G);
+        return G;
+    }
+    auto fill = [&](float B, int* out) -> int {   // ranges used, or C+1 if more are needed
+        int x = 0, g = 0;
+        if (out) out[0] = 0;
+        while (x < W) {
+            if (g == C) return C + 1;
+            const int start = x;
+            float cost = 0.f;
+            while (x < W) {
+                const int ue = (x / n + 1) * n;
+                const float extra = x > start ? item_cost : 0.f;
+                const float avail = B - cost - extra;
+                int take = int(avail);
+                if (take > ue - x) take = ue - x;
+                if (x > start && take < min_piece && take < ue - x) break;
+                if (take <= 0) {
+                    if (x == start) take = 1;    // always progress
+                    else break;
+                }
+                cost += take + extra;
+                x += take;
+                if (x < ue) break;               // budget ends inside this unit
+            }
+            ++g;
+            if (out) out[g] = x;
+        }
+        return g;
+    };
+    float lo = float(W) / C, hi = float(W) / C + item_cost * 4 + n;
+    while (fill(hi, nullptr) > C) hi *= 2;
+    for (int it = 0; it < 40; ++it) {
+        const float mid = 0.5f * (lo + hi);
+        if (fill(mid, nullptr) <= C) hi = mid;
+        else lo = mid;
+    }
+    return fill(hi, bound);
+}
+
 size_t fmha_sm100_scratch_bytes(int d) {
     return size_t(kMaxPersistentCtas) * (256 * size_t(d) + 512) * 4 + kMaxPersistentCtas * 4;
 }
@@ -965,11 +1040,9 @@ cudaError_t launch_fmha_sm100(const AttnProblem& pr, void* scratch, cudaStream_t
     const int qtiles = int((pr.Lq + kBM - 1) / kBM);
     p.n_qpairs = (qtiles + 1) / 2;
     // Persistent schedule: R whole rounds over C CTAs, then the T tail units'
-    // T*n KV tiles in equal contiguous ranges over G' CTAs (stream-K), pieces
-    // of at least kMinPiece tiles.  P = 2, 4, 8 head shards leave T >= C/2
-    // (240, 120, 60 units of 56 tiles at WAN-512), where whole-unit or
-    // even-split tails idle ~19% of the machine in the last wave.
-    // TM_SCHED_SPLIT=1 (A/B only): G' = T * floor(C / T), the earlier even split.
+    // T*n KV tiles in contiguous ranges over G' CTAs (stream-K).  P = 2, 4, 8
+    // head shards leave T >= C/2 (240, 120, 60 units of 56 tiles at WAN-512),
+    // where whole-unit or even-split tails idle ~19% of the machine.
     constexpr int kMinPiece = 4;
     int C = sm_count() < kMaxPersistentCtas ? sm_count() : kMaxPersistentCtas;
     if (pr.max_ctas > 0 && pr.max_ctas < C) C = pr.max_ctas;
@@ -978,16 +1051,20 @@ cudaError_t launch_fmha_sm100(const AttnProblem& pr, void* scratch, cudaStream_t
     const int T = U - R * C;
     int G = 0;
     if (T > 0) {
-        static const bool split_sched = [] {
-            const char* e = getenv("TM_SCHED_SPLIT");
-            return e && *e && strcmp(e, "0") != 0;
-        }();
-        const long long by_len = (long long)T * tiles / kMinPiece;
-        G = C;
-        if (split_sched) G = T * (C / T > tiles ? tiles : C / T);
-        if (G > by_len) G = int(by_len);
-        if (G < T) G = T;                 // every tail unit at least whole (short units)
-        if (G > C) G = C;
+        if ((long long)T * tiles >= (1ll << 30)) return cudaErrorInvalidValue;
+        // the bounds depend only on (T, n, C): computed once, then cached
+        static std::mutex mu;
+        static std::map<std::tuple<int, int, int>, std::vector<int>> cache;
+        std::lock_guard<std::mutex> lock(mu);
+        std::vector<int>& b = cache[std::make_tuple(T, tiles, C)];
+        if (b.empty()) {
+            b.assign(kMaxPersistentCtas + 1, 0);
+            const int g = tail_bounds(T, tiles, C, kMinPiece, b.data());
+            b.resize(g + 1);
+        }
+        G = int(b.size()) - 1;
+        if (G <= 0) return cudaErrorInvalidValue;
+        for (int c = 0; c <= G; ++c) p.sk_bound[c] = b[c];
     }
     p.rounds = R;
     p.sk_units = T;

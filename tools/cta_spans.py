@@ -53,11 +53,43 @@ wait = rel[:, 5] - rel[:, 4]
 ok = ~np.isnan(wait)
 if ok.any():
     print(f"  merge wait   n {ok.sum()}  median {np.median(wait[ok]):6.1f}  max {wait[ok].max():6.1f} us")
-tiles, items = allw[:, 6], allw[:, 7]
+tiles, items, smid = allw[:, 6], allw[:, 7] & 0xFFFF, allw[:, 7] >> 16
 print(f"  tiles/CTA min {tiles.min()} max {tiles.max()}; items/CTA {sorted(set(items.tolist()))}")
 order = np.argsort(rel[:, 3])
-print("  slowest 8 CTAs: (cta, tiles, items, exit us, merge wait us)")
+print("  slowest 8 CTAs: (cta, smid, tiles, items, exit us, merge wait us)")
 for c in order[-8:]:
-    print(f"    {c:4d} {tiles[c]:4d} {items[c]:3d} {rel[c, 3]:7.1f} {wait[c] if ok[c] else float('nan'):6.1f}")
+    print(f"    {c:4d} {smid[c]:4d} {tiles[c]:4d} {items[c]:3d} {rel[c, 3]:7.1f} {wait[c] if ok[c] else float('nan'):6.1f}")
+rate_all = tiles / (rel[:, 3] - rel[:, 1])
+print("  rate by smid (tiles/us), 148 values in smid order:")
+by = sorted(zip(smid.tolist(), rate_all.tolist()))
+print("   " + " ".join(f"{r:.3f}" for _, r in by))
 rate = tiles / (rel[:, 3] - rel[:, 1])
 print(f"  tiles/us per CTA: min {rate.min():.3f} median {np.median(rate):.3f} max {rate.max():.3f}")
+
+# Per-CTA table (host replica of the stream-K item math) -> gpurun_out/spans_<H>.json
+import json  # noqa: E402
+n_tiles = sum(-(-L // 128) for L in (Lr, Lc, Lc))
+qpairs = -(-(-(-Lc // 128)) // 2)
+U = H * qpairs
+C = len(allw)
+R, T = U // C, U % C
+G = 0
+if T:
+    G = min(C, max(T, T * n_tiles // 4))
+W = T * n_tiles
+rows = []
+for c in range(C):
+    items = [("whole", n_tiles)] * R
+    if T and c < G:
+        s, e = c * W // G, (c + 1) * W // G
+        u = s // n_tiles
+        while u * n_tiles < e:
+            lo, hi = max(s, u * n_tiles) - u * n_tiles, min(e, (u + 1) * n_tiles) - u * n_tiles
+            items.append((f"u{u}[{lo},{hi})", hi - lo))
+            u += 1
+    rows.append({"cta": c, "smid": int(smid[c]), "exit": float(rel[c, 3]), "first_s": float(rel[c, 1]),
+                 "item2": float(rel[c, 2]) if raw[c, 2] else None, "rate": float(rate_all[c]),
+                 "items": items})
+os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+with open(os.path.join(ROOT, "gpurun_out", f"spans_{cfg}_{H}.json"), "w") as f:
+    json.dump(rows, f)
