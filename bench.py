@@ -309,7 +309,7 @@ def main():
                     help="Ulysses exchange for N>1 (default peer: fused NVLink peer-memory "
                          "push/scatter; nccl: pack + ncclAlltoAll + unpack).  At N=1 the "
                          "default is the direct path; --transport peer runs a 1-rank group.")
-    ap.add_argument("--stream-chunks", type=int, default=4,
+    ap.add_argument("--stream-chunks", type=int, default=64,
                     help="BJ.configs[3] streaming measurement over this many chunks (0: off)")
     args = ap.parse_args()
     if args.warmup < 3:
@@ -457,6 +457,8 @@ def main():
         kev.append((a, b))
     barrier()
     w3 = time.time()
+    if transport == "peer":
+        ca.check()      # raises if any device-side peer wait timed out (results would be garbage)
     clocks.stop()
     clk = clocks.summary(window=(w0, w1))
     kclk = clocks.summary(window=(w2, w3))
@@ -550,6 +552,8 @@ def main():
         sb.record(stream)
         barrier()
         s_ms = max_over_ranks(sa.elapsed_time(sb)) / (args.stream_chunks - 1)
+        if transport == "peer":
+            sc.check()
         streaming = {"config": f"BJ.configs[3] shape: {NLs} layers x {NS} steps per chunk, "
                                f"chunks 2..{args.stream_chunks} timed (steady state, t>=2)",
                      "ms_per_chunk": s_ms,

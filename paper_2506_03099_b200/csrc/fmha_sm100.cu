@@ -400,21 +400,25 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
             int n_loads = 0;
             Item it;
             for (int w = 0; get_item(p, w, it); ++w, ++n_item) {
-                for (int i = 0; i < 2; ++i) {
-                    if (p.peer) {
-                        const int r0 = it.qp * 2 * kBM + i * kBM;
-                        peer_ready(p, ok, 0, r0, min(kBM, p.Lq - r0));
-                    }
-                    mbar_wait(&q_empty[i], (n_item & 1) ^ 1);
-                    mbar_arrive_expect_tx(&q_full[i], kTileBytes);
-                    for (int hf = 0; hf < D / 64; ++hf)
-                        tma_load_4d(sQ + i * kTileBytes + hf * kHalfBytes, &p.tq, &q_full[i],
-                                    hf * 64, it.h, it.qp * 2 * kBM + i * kBM, it.b);
-                }
-                // Load order K_lo, K_lo+1, V_lo, K_lo+2, V_lo+1, ..., V_hi-1: K runs one
-                // tile ahead of V, matching the MMA's use (S(j+1) before PV(j)).
+                // Load order Q_0, K_lo, Q_1, K_lo+1, V_lo, K_lo+2, V_lo+1, ..., V_hi-1:
+                // S_0(lo) needs only Q_0 and K_lo, and K runs one tile ahead of V,
+                // matching the MMA's use (S(j+1) before PV(j)).
                 const int nkv = it.hi - it.lo;
-                for (int q = 0; q < 2 * nkv; ++q, ++kv_it) {
+                for (int step = 0; step < 2 * nkv + 2; ++step) {
+                    if (step == 0 || step == 2) {
+                        const int i = step >> 1;
+                        if (p.peer) {
+                            const int r0 = it.qp * 2 * kBM + i * kBM;
+                            peer_ready(p, ok, 0, r0, min(kBM, p.Lq - r0));
+                        }
+                        mbar_wait(&q_empty[i], (n_item & 1) ^ 1);
+                        mbar_arrive_expect_tx(&q_full[i], kTileBytes);
+                        for (int hf = 0; hf < D / 64; ++hf)
+                            tma_load_4d(sQ + i * kTileBytes + hf * kHalfBytes, &p.tq, &q_full[i],
+                                        hf * 64, it.h, it.qp * 2 * kBM + i * kBM, it.b);
+                        continue;
+                    }
+                    const int q = step == 1 ? 0 : step - 2;
                     int jj, kv;
                     load_order(q, nkv, jj, kv);
                     int seg, row, valid;
@@ -443,6 +447,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                     for (int hf = 0; hf < D / 64; ++hf)
                         tma_load_4d(sKV + s * kTileBytes + hf * kHalfBytes, m, &kv_full[s],
                                     hf * 64, it.h, row, it.b);
+                    ++kv_it;
                 }
             }
             if (!kv_released) peer_release(p.pp.ctr, p.pp.own, p.pp.P, p.pp.rank, 1);
