@@ -27,6 +27,11 @@ int num_sms() {
     return n;
 }
 
+cudaError_t finish(cudaError_t e, int* launches) {
+    if (e == cudaSuccess && launches) ++*launches;
+    return e;
+}
+
 unsigned grid_for(int64_t work_items, int threads, int per_sm = 8) {
     const int64_t want = (work_items + threads - 1) / threads;
     const int64_t cap = int64_t(num_sms()) * per_sm;
@@ -40,6 +45,7 @@ template <bool kBf16>
 __global__ void __launch_bounds__(256) euler_kernel(float* __restrict__ x,
                                                     const void* __restrict__ vv, int64_t n,
                                                     float dt) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");   // PDL: after the previous grid
     const int64_t n8 = n / 8;
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
     for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n8; i += stride) {
@@ -242,11 +248,11 @@ cudaError_t launch_euler(float* x, const void* v, int v_is_bf16, int64_t n, floa
     if (n <= 0) return cudaSuccess;
     const unsigned grid = grid_for((n + 7) / 8, 256, 16);
     if (v_is_bf16)
-        euler_kernel<true><<<grid, 256, 0, s>>>(x, v, n, dt);
+        return finish(launch_pdl(euler_kernel<true>, dim3(grid), dim3(256), 0, s, x, v, n, dt),
+                      launches);
     else
-        euler_kernel<false><<<grid, 256, 0, s>>>(x, v, n, dt);
-    if (launches) ++*launches;
-    return cudaGetLastError();
+        return finish(launch_pdl(euler_kernel<false>, dim3(grid), dim3(256), 0, s, x, v, n, dt),
+                      launches);
 }
 
 cudaError_t launch_sampler(float* x, const void* v, int v_is_bf16, const float* eps, int64_t n,

@@ -335,26 +335,6 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
     const int lane = threadIdx.x & 31;
 
     if (threadIdx.x == 0) trace_span(p, 0);
-    if (p.push) {
-        // a2 fused.  All 384 threads store this rank's shard of Q into the owners'
-        // windows (NVLink stores).  Then warp 10 alone releases Q (a system-scope
-        // fence waits until the CTA's stores have landed; the grid's last CTA
-        // bumps arr[0][rank] at every owner) while the other 11 warps store K
-        // and V.  K/V are released later by the producer (peer_kv_release), once
-        // their stores have long drained, so no role waits for NVLink: owners
-        // start on Q and the cached c_0 / c_{t-1} segments while c_t is in flight.
-        peer_push_share(p.pp, 0, threadIdx.x, kThreads);
-        __syncthreads();
-        if (warp == 10) {
-            if (lane == 0) peer_release(p.pp.ctr, p.pp.own, p.pp.P, p.pp.rank, 0);
-            __syncwarp();
-        } else {
-            const int t = threadIdx.x < 320 ? threadIdx.x : threadIdx.x - 32;
-            peer_push_share(p.pp, 1, t, kThreads - 32);
-            peer_push_share(p.pp, 2, t, kThreads - 32);
-        }
-        __syncthreads();
-    }
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < 2; ++i) {
@@ -386,6 +366,30 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_holder;
+    // Programmatic dependent launch: everything above (barriers, TMEM, tensor-map
+    // prefetch) overlaps the previous kernel's tail; no global data is touched
+    // before the previous grid has completed.  (No-op without the attribute.)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (p.push) {
+        // a2 fused.  All 384 threads store this rank's shard of Q into the owners'
+        // windows (NVLink stores).  Then warp 10 alone releases Q (a system-scope
+        // fence waits until the CTA's stores have landed; the grid's last CTA
+        // bumps arr[0][rank] at every owner) while the other 11 warps store K
+        // and V.  K/V are released later by the producer (peer_release), once
+        // their stores have long drained, so no role waits for NVLink: owners
+        // start on Q and the cached c_0 / c_{t-1} segments while c_t is in flight.
+        peer_push_share(p.pp, 0, threadIdx.x, kThreads);
+        __syncthreads();
+        if (warp == 10) {
+            if (lane == 0) peer_release(p.pp.ctr, p.pp.own, p.pp.P, p.pp.rank, 0);
+            __syncwarp();
+        } else {
+            const int t = threadIdx.x < 320 ? threadIdx.x : threadIdx.x - 32;
+            peer_push_share(p.pp, 1, t, kThreads - 32);
+            peer_push_share(p.pp, 2, t, kThreads - 32);
+        }
+        __syncthreads();
+    }
 
     if (warp >= 8) {
       asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsOther));
@@ -888,8 +892,8 @@ cudaError_t launch_t(const FmhaParams& p, int grid, cudaStream_t stream) {
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    fmha_sm100_kernel<D, kPolyMask><<<grid, kThreads, smem_bytes<D>(), stream>>>(p);
-    return cudaGetLastError();
+    return launch_pdl(fmha_sm100_kernel<D, kPolyMask>, dim3(grid), dim3(kThreads), smem_bytes<D>(),
+                      stream, p);
 }
 
 // Which of every 16 exp2 pairs run as the FMA-pipe polynomial (bit e set) --
@@ -978,6 +982,14 @@ int tail_bounds(int T, int n, int C, int min_piece, int* bound) {
         else lo = mid;
     }
     return fill(hi, bound);
+}
+
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("TM_PDL");
+        return !(e && strcmp(e, "0") == 0);
+    }();
+    return on;
 }
 
 size_t fmha_sm100_scratch_bytes(int d) {

@@ -2,6 +2,9 @@
 // kernel launchers.  Not part of the public ABI (include/tm.h is).
 #pragma once
 #include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <utility>
 #include <cuda_runtime.h>
 
 namespace tmk {
@@ -81,6 +84,28 @@ struct AttnProblem {
     const PeerAttnArgs* peer = nullptr;   // peer transport (sm100 path only)
     int max_ctas = 0;                     // persistent grid cap (0: one CTA per SM)
 };
+
+// Launch with programmatic dependent launch allowed (the kernel executes
+// griddepcontrol.wait before touching global data, so its prologue overlaps the
+// previous kernel's tail).  TM_PDL=0 disables the attribute (A/B).
+bool pdl_enabled();
+#ifdef __CUDACC__
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t s, Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+#endif
 
 // Launchers; return cudaSuccess or the launch error.  `launches` is
 // incremented by the number of kernels enqueued.

@@ -54,6 +54,7 @@ __global__ void __launch_bounds__(kThreads) peer_recv_o_kernel(PeerCounters* own
                                                                int P, const uint4* owin, uint4* o,
                                                                int B, int64_t Ls, int64_t L,
                                                                int rank, int W) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");   // PDL: after the attention grid
     cta_wait_all(own, 3, epoch, P);
     const int64_t n = int64_t(B) * Ls * W;
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
@@ -106,11 +107,11 @@ cudaError_t launch_peer_recv_o(PeerCounters* own, uint32_t epoch, int P, const v
                                int B, int64_t Ls, int64_t L, int rank, int row_bytes,
                                cudaStream_t s, int* launches) {
     if (row_bytes % 16) return cudaErrorInvalidValue;
-    peer_recv_o_kernel<<<sm_count_peer(), kThreads, 0, s>>>(
-        own, epoch, P, static_cast<const uint4*>(owin), static_cast<uint4*>(o), B, Ls, L, rank,
-        row_bytes / 16);
-    if (launches) ++*launches;
-    return cudaGetLastError();
+    const cudaError_t e = launch_pdl(peer_recv_o_kernel, dim3(sm_count_peer()), dim3(kThreads), 0, s,
+                                     own, epoch, P, static_cast<const uint4*>(owin),
+                                     static_cast<uint4*>(o), B, Ls, L, rank, row_bytes / 16);
+    if (e == cudaSuccess && launches) ++*launches;
+    return e;
 }
 
 cudaError_t launch_peer_ref_store(PeerCounters* const* ctr, PeerCounters* own, uint32_t epoch,
