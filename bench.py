@@ -378,14 +378,18 @@ def main():
     chunk = [0] * NL
     launches = [0]
 
-    def step(i, zero_copy=False):
+    def step(i, zero_copy=False, ev=None):
         layer = i % NL
         chunk[layer] += 1
         q, k, v = sets[i % NB]
         o = outs[i % NB]
         if zero_copy:
             k, v = ca.slot_ptr(layer, 0, chunk[layer])
+        if ev is not None:
+            ev[0].record(stream)
         ca.attend(layer, 0, chunk[layer], q, k, v, o, stream)
+        if ev is not None:
+            ev[1].record(stream)
         n = ca.launches
         ca.euler(xlat, vlat, tm.TM_BF16, 0.5, stream)
         launches[0] += n + ca.launches
@@ -415,13 +419,23 @@ def main():
     barrier()
     w0 = time.time()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # Events around every 4th attention call inside the timed region give the
+    # dominant kernel's live duration (roofline.achieved).  Not every call: an
+    # event pair costs ~6 us per step (it also stops the next launch's prologue
+    # from overlapping the previous kernel).
+    EV_EVERY = 4
+    lev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(0, args.steps, EV_EVERY)]
     e0.record(stream)
     for i in range(args.steps):
-        step(i)
+        step(i, ev=lev[i // EV_EVERY] if i % EV_EVERY == 0 else None)
     e1.record(stream)
     barrier()
     w1 = time.time()
     ms_total = max_over_ranks(e0.elapsed_time(e1))
+    live = [a.elapsed_time(b) for a, b in lev]
+    live_ms = max_over_ranks(statistics.mean(live))
+    live_med = max_over_ranks(statistics.median(live))
     gpu_launches = launches[0]
 
     # ---------------------------------------------------------------- attention kernel alone
@@ -569,7 +583,9 @@ def main():
     ms_step = ms_total / args.steps
     value = fl * args.steps / (ms_total * 1e-3) / 1e12
     peak, peak_sus, peak_src = measured_peaks()
-    achieved = fl / P / (k_ms * 1e-3) / 1e12      # per GPU (each rank does 1/P of the heads)
+    # per GPU (each rank does 1/P of the heads); live = inside the timed region
+    achieved = fl / P / (live_ms * 1e-3) / 1e12
+    achieved_alone = fl / P / (k_ms * 1e-3) / 1e12
     prof = os.path.join(ROOT, "profiles", "ncu_fmha_traffic.json")
     traffic = None
     try:
@@ -603,10 +619,17 @@ def main():
             "frac_of_bf16_peak": achieved / peak,
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak,
                          "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "tm_fmha_sm100 (tcgen05)" if zc else
+                         "kernel": "tm_fmha_sm100 (tcgen05, fused c_t append)" if P == 1 and
+                                   transport == "nccl" else
                                    f"whole call ({transport} transport: exchange + attention)",
+                         "timing": f"CUDA events around every {EV_EVERY}th of the {args.steps} "
+                                   "attention calls inside the timed region (mean)",
                          "peak_source": f"{peak_src} bf16 burst",
-                         "flop_per_launch": fl, "achieved_median_launch": fl / P / (k_med * 1e-3) / 1e12,
+                         "flop_per_launch": fl / P,
+                         "achieved_median_launch": fl / P / (live_med * 1e-3) / 1e12,
+                         "achieved_kernel_alone": achieved_alone,
+                         "kernel_alone": "zero-copy calls (no append), per-call events, after the "
+                                         "timed region" if zc else "whole calls, per-call events",
                          "algorithmic_bytes_per_launch": algo_bytes(c)},
             "cpu_baseline": cpu,
             "e2e": e2e,
