@@ -347,6 +347,16 @@ def main():
     Lc_s, Lr_s = -(-Lc // P), -(-Lr // P)
     NL = args.layers
     transport = args.transport or ("peer" if P > 1 else "nccl")
+    if transport == "peer" and P > 1 and not one_dev:
+        # the peer windows need NVLink/PCIe peer access between every pair of GPUs
+        ok = all(torch.cuda.can_device_access_peer(local, j) for j in range(P) if j != local)
+        flag = torch.tensor([1 if ok else 0], device="cuda", dtype=torch.int32)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if int(flag.item()) == 0:
+            if rank == 0:
+                print("bench: no peer access between all GPUs; using the NCCL transport",
+                      file=sys.stderr)
+            transport = "nccl"
     tcode = tm.TM_TRANSPORT_PEER if transport == "peer" else tm.TM_TRANSPORT_NCCL
     nccl_id = None
     if P > 1 and transport == "nccl":
