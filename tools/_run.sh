@@ -1,3 +1,2 @@
-for rep in 1 2; do for lib in libtm.so libtm_sumguard.so; do for H in 40 5; do
- TM_LIB_PATH=$PWD/paper_2506_03099_b200/$lib SWEEP_H=$H timeout 120 python tools/sweep.py | sed "s/^/$lib /"
-done; done; done
+python bench.py --no-extras --no-cpu-baseline --stream-chunks 0 2>/dev/null | python -c "
+import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], json.dumps(d['e2e']))"
