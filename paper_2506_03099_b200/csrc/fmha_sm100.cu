@@ -60,7 +60,15 @@ namespace {
 
 constexpr int kBM = 128;          // query rows per Q tile
 constexpr int kBN = 128;          // keys per KV tile
-constexpr int kStages = 5;        // K/V smem ring slots (Q 64 KB + 5 x 32 KB fits in 227 KB)
+// K/V smem ring slots: Q 64 KB + 4 x 32 KB + 32 KB of epilogue staging fit in
+// 227 KB (the 5th slot measured within noise at 512^2, +3 % at 720^2 when the
+// epilogue wrote rows straight from registers; the staging makes every output
+// store instruction write 4 rows x 128 B instead of 32 rows x 16 B).
+#ifndef TM_KV_STAGES
+#define TM_KV_STAGES 4
+#endif
+constexpr int kStages = TM_KV_STAGES;
+constexpr int kEpiBytes = 8 * 4096;   // per softmax warp: 32 rows x 128 B (bf16 half row)
 constexpr int kThreads = 384;     // 2 softmax warpgroups + {TMA, MMA, 2 spare} warpgroup
 constexpr int kRegsSoftmax = 216; // setmaxnreg budgets (see the static_assert)
 constexpr int kRegsOther = 72;
@@ -229,9 +237,56 @@ __device__ __forceinline__ bool stores_tile(const FmhaParams& p, const Item& it,
 template <int D>
 __device__ __forceinline__ uint16_t* out_row(const FmhaParams& p, int b, int q, int h) {
     if (q >= p.Lq) return nullptr;
+    if (p.o_rows >= p.Lq)     // one owner (P = 1): no division
+        return p.o_dst[0] + ((int64_t(b) * p.o_bstride + q) * p.o_H + p.o_h0 + h) * D;
     int own;
     const int64_t row = peer_out_route(b, q, h, p.o_rows, p.o_bstride, p.o_H, p.o_h0, own);
     return p.o_dst[own] + row * D;
+}
+
+// Epilogue: the warp's 32 threads each hold one output row (lane l = row
+// q0 + l) as D fp32 values in TMEM columns [tsrc, tsrc + D); scale, round to
+// bf16 and store.  Through a 4 KB per-warp staging buffer (32 rows x 64
+// columns, 16-B chunks XOR-swizzled by row: conflict-free both ways) each
+// store instruction writes 4 rows x 128 B instead of 32 rows x 16 B.
+template <int D>
+__device__ __forceinline__ void store_rows_bf16(const FmhaParams& p, uint32_t tsrc, float scale,
+                                                uint8_t* stg, int b, int q0, int h, int lane) {
+    // This lane stores rows t*4 + lane/8 (t < 8), 16 B at column chunk lane%8:
+    // destinations computed once for both halves (32-bit index math).
+    uint16_t* dsts[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+        const int q = q0 + t * 4 + (lane >> 3);
+        dsts[t] = q < p.Lq ? out_row<D>(p, b, q, h) : nullptr;
+    }
+#pragma unroll 1
+    for (int half = 0; half < D / 64; ++half) {
+        uint32_t o[64];
+        tmem_ld32(tsrc + half * 64, o);
+        tmem_ld32(tsrc + half * 64 + 32, o + 32);
+        tmem_wait_ld();
+#ifdef TM_SPANS_MERGE
+        if (threadIdx.x == 0 && half == 0) trace_span(p, 1);
+#endif
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            uint4 v;
+            v.x = pack_bf16x2(__uint_as_float(o[8 * j]) * scale, __uint_as_float(o[8 * j + 1]) * scale);
+            v.y = pack_bf16x2(__uint_as_float(o[8 * j + 2]) * scale, __uint_as_float(o[8 * j + 3]) * scale);
+            v.z = pack_bf16x2(__uint_as_float(o[8 * j + 4]) * scale, __uint_as_float(o[8 * j + 5]) * scale);
+            v.w = pack_bf16x2(__uint_as_float(o[8 * j + 6]) * scale, __uint_as_float(o[8 * j + 7]) * scale);
+            *reinterpret_cast<uint4*>(stg + lane * 128 + ((j ^ (lane & 7)) << 4)) = v;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+            const int r = t * 4 + (lane >> 3), j = lane & 7;
+            const uint4 v = *reinterpret_cast<const uint4*>(stg + r * 128 + ((j ^ (r & 7)) << 4));
+            if (dsts[t]) *reinterpret_cast<uint4*>(dsts[t] + half * 64 + j * 8) = v;
+        }
+        __syncwarp();
+    }
 }
 
 // Peer transport: before the producer's first TMA read of window rows
@@ -317,7 +372,8 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
     uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
     uint8_t* sQ = smem;                                  // 2 tiles
     uint8_t* sKV = smem + 2 * kTileBytes;                // kStages slots
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + kStages * kTileBytes);
+    uint8_t* sEpi = sKV + kStages * kTileBytes;          // epilogue staging, 4 KB per softmax warp
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sEpi + kEpiBytes);
     uint64_t* q_full = bars;                 // [2]
     uint64_t* q_empty = q_full + 2;          // [2]
     uint64_t* kv_full = q_empty + 2;         // [kStages]
@@ -329,7 +385,9 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
     uint64_t* o_done = o_empty + 2;          // [2]  each PV_i complete (P_i reusable)
     uint64_t* s_free = o_done + 2;           // [1]  S buffer loaded into registers
     uint64_t* store_done = s_free + 1;       // [kStages] append-store finished reading a slot
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(store_done + kStages);
+    uint64_t* store_idle = store_done + kStages;   // [1] append warp done (one phase per launch)
+    uint64_t* merge_bar = store_idle + 1;          // [1] a piece's partial landed in smem (merge)
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(merge_bar + 1);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -352,6 +410,8 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
             mbar_init(&kv_empty[s], 1);
             mbar_init(&store_done[s], 1);
         }
+        mbar_init(store_idle, 1);
+        mbar_init(merge_bar, 1);
         fence_mbar_init();
     }
     if (warp == 8 && lane == 0) {
@@ -505,6 +565,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                 }
             }
         }
+        if (lane == 0) mbar_arrive(store_idle);   // the ring is no longer read by TMA stores
       } else if (warp == 9 || warp == 11) {
         // ------------------------------------------------ MMA issuers
         // Two independent issuers so that neither waits behind the other:
@@ -582,7 +643,9 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
         const bool tr = (lane == 0);   // every softmax warp records (equal trace overhead)
         Item it;
         for (int w = 0; get_item(p, w, it); ++w, ++n_item) {
+#ifndef TM_SPANS_MERGE
             if (threadIdx.x == 0 && n_item == 1) trace_span(p, 2);   // first item's epilogue done
+#endif
             float m_run = -INFINITY, l = 0.f;
             for (int j = it.lo; j < it.hi; ++j, ++g) {
                 int seg, row, valid;
@@ -590,7 +653,9 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                 uint32_t r[kBN];
                 mbar_wait(&s_full[i], g & 1);
                 if (tr) trace_ev(p, 5 + warp, tn, 20);
+#ifndef TM_SPANS_MERGE
                 if (threadIdx.x == 0 && g == 0) trace_span(p, 1);
+#endif
                 tc_fence_after();
 #pragma unroll
                 for (int c = 0; c < kBN; c += 32) tmem_ld32(tS + c, r + c);
@@ -699,27 +764,15 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
             // ------------------------------------------------ epilogue
             mbar_wait(&o_final[i], n_item & 1);
             tc_fence_after();
+#ifdef TM_SPANS_MERGE
+            if (threadIdx.x == 0) trace_span(p, 2);   // (spans A/B) this item's epilogue begins
+#endif
             const int q = it.qp * 2 * kBM + row_in_pair;
             if (!it.piece) {
-                const float inv_l = 1.f / l;
-                uint16_t* dst = out_row<D>(p, it.b, q, it.h);
-#pragma unroll
-                for (int c = 0; c < D; c += 32) {
-                    uint32_t o[32];
-                    tmem_ld32(tOi + c, o);
-                    tmem_wait_ld();
-                    uint32_t wv[16];
-#pragma unroll
-                    for (int e = 0; e < 16; ++e)
-                        wv[e] = pack_bf16x2(__uint_as_float(o[2 * e]) * inv_l,
-                                            __uint_as_float(o[2 * e + 1]) * inv_l);
-                    if (dst) {
-                        uint4* d4 = reinterpret_cast<uint4*>(dst + c);
-#pragma unroll
-                        for (int e = 0; e < 4; ++e)
-                            d4[e] = make_uint4(wv[4 * e], wv[4 * e + 1], wv[4 * e + 2], wv[4 * e + 3]);
-                    }
-                }
+                store_rows_bf16<D>(p, tOi, 1.f / l, sEpi + warp * 4096, it.b, q - lane, it.h, lane);
+#ifdef TM_SPANS_MERGE
+                if (threadIdx.x == 0) trace_span(p, 5);
+#endif
                 tc_fence_before();
                 mbar_arrive(&o_empty[i]);
             } else if (it.pidx > 0) {
@@ -744,9 +797,11 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                 mbar_arrive(&o_empty[i]);
                 base[256 * D + row_in_pair] = m_run;
                 base[256 * D + 256 + row_in_pair] = l;
-                __threadfence();
-                softmax_bar();
-                if (threadIdx.x == 0) atomicAdd(&p.counters[it.cfirst], 1);
+                softmax_bar();                // every thread's partial stores precede ...
+                if (threadIdx.x == 0) {       // ... this one fence (cumulative) and the count
+                    __threadfence();
+                    atomicAdd(&p.counters[it.cfirst], 1);
+                }
             } else {
                 // piece 0 of a split unit = this CTA's LAST item (its range ends
                 // inside the unit), so O_i stays in TMEM: wait until the other
@@ -768,55 +823,85 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                 auto piece_base = [&](int k) {
                     return p.part + size_t(it.cfirst + k) * kPieceFloats;
                 };
+                // This is the CTA's last item: no more K/V loads, and once store_idle
+                // has completed no append store reads the ring.  The pieces' partials
+                // (O 128 KB, then m and l) are pulled one at a time into the K/V ring
+                // by a bulk copy; each thread reads its row from shared memory
+                // (conflict-free [d/4][256] float4 layout) and accumulates into O_i in
+                // TMEM.  The weights need every piece's m and l first: loaded from
+                // global, up to 8 pieces per batch of independent loads.
+                constexpr uint32_t kPieceBytes = kPieceFloats * 4;
+                static_assert(kPieceBytes <= kStages * kTileBytes + kEpiBytes,
+                              "a partial fits the ring + staging");
+                const int np = it.npieces;
+                if (threadIdx.x == 0) {
+                    mbar_wait(store_idle, 0);
+                    fence_proxy_async_global();
+                    mbar_arrive_expect_tx(merge_bar, kPieceBytes);
+                    bulk_g2s(sKV, piece_base(1), kPieceBytes, merge_bar);
+                }
                 float mstar = m_run;
-                for (int k = 1; k < it.npieces; ++k)
-                    mstar = fmaxf(mstar, __ldcg(piece_base(k) + 256 * D + row_in_pair));
+                for (int k0 = 1; k0 < np; k0 += 8) {
+                    float mm[8];
+#pragma unroll
+                    for (int e = 0; e < 8; ++e)
+                        mm[e] = k0 + e < np ? __ldcg(piece_base(k0 + e) + 256 * D + row_in_pair) : -INFINITY;
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) mstar = fmaxf(mstar, mm[e]);
+                }
                 const float w0 = ex2(m_run - mstar);
                 float wsum = w0 * l;
-                for (int k = 1; k < it.npieces; ++k) {
-                    const float* bs = piece_base(k);
-                    wsum += ex2(__ldcg(bs + 256 * D + row_in_pair) - mstar) *
-                            __ldcg(bs + 256 * D + 256 + row_in_pair);
+                for (int k0 = 1; k0 < np; k0 += 8) {
+                    float mm[8], ll[8];
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        const bool in = k0 + e < np;
+                        mm[e] = in ? __ldcg(piece_base(k0 + e) + 256 * D + row_in_pair) : -INFINITY;
+                        ll[e] = in ? __ldcg(piece_base(k0 + e) + 256 * D + 256 + row_in_pair) : 0.f;
+                    }
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) wsum += ex2(mm[e] - mstar) * ll[e];
                 }
                 const float inv = 1.f / wsum;
-                uint16_t* dst = out_row<D>(p, it.b, q, it.h);
-#pragma unroll 1
-                for (int c = 0; c < D; c += 32) {
-                    uint32_t o[32];
-                    tmem_ld32(tOi + c, o);
-                    tmem_wait_ld();
-                    float acc[32];
-#pragma unroll
-                    for (int e = 0; e < 32; ++e) acc[e] = __uint_as_float(o[e]) * w0;
-                    for (int k = 1; k < it.npieces; ++k) {
-                        const float* bs = piece_base(k);
-                        const float wk = ex2(__ldcg(bs + 256 * D + row_in_pair) - mstar);
-                        float4 x[8];
-#pragma unroll
-                        for (int e = 0; e < 8; ++e)
-                            x[e] = __ldcg(reinterpret_cast<const float4*>(bs) + ((c >> 2) + e) * 256 + row_in_pair);
-#pragma unroll
-                        for (int e = 0; e < 8; ++e) {
-                            acc[4 * e] += wk * x[e].x;
-                            acc[4 * e + 1] += wk * x[e].y;
-                            acc[4 * e + 2] += wk * x[e].z;
-                            acc[4 * e + 3] += wk * x[e].w;
+                const float* sml = reinterpret_cast<const float*>(sKV) + 256 * D;
+                const float4* sp = reinterpret_cast<const float4*>(sKV);
+                for (int k = 1; k < np; ++k) {
+                    if (k > 1) {
+                        softmax_bar();              // everyone done with the previous piece
+                        if (threadIdx.x == 0) {
+                            mbar_arrive_expect_tx(merge_bar, kPieceBytes);
+                            bulk_g2s(sKV, piece_base(k), kPieceBytes, merge_bar);
                         }
                     }
-                    if (dst) {
-                        uint4* d4 = reinterpret_cast<uint4*>(dst + c);
+                    mbar_wait(merge_bar, (k - 1) & 1);
+                    const float wk = ex2(sml[row_in_pair] - mstar);
+                    const float wo = k == 1 ? w0 : 1.f;
+#pragma unroll 1
+                    for (int c = 0; c < D; c += 32) {
+                        uint32_t o[32];
+                        tmem_ld32(tOi + c, o);
+                        tmem_wait_ld();
 #pragma unroll
-                        for (int e = 0; e < 4; ++e)
-                            d4[e] = make_uint4(pack_bf16x2(acc[8 * e] * inv, acc[8 * e + 1] * inv),
-                                               pack_bf16x2(acc[8 * e + 2] * inv, acc[8 * e + 3] * inv),
-                                               pack_bf16x2(acc[8 * e + 4] * inv, acc[8 * e + 5] * inv),
-                                               pack_bf16x2(acc[8 * e + 6] * inv, acc[8 * e + 7] * inv));
+                        for (int e = 0; e < 8; ++e) {
+                            const float4 x = sp[((c >> 2) + e) * 256 + row_in_pair];
+                            o[4 * e] = __float_as_uint(__uint_as_float(o[4 * e]) * wo + wk * x.x);
+                            o[4 * e + 1] = __float_as_uint(__uint_as_float(o[4 * e + 1]) * wo + wk * x.y);
+                            o[4 * e + 2] = __float_as_uint(__uint_as_float(o[4 * e + 2]) * wo + wk * x.z);
+                            o[4 * e + 3] = __float_as_uint(__uint_as_float(o[4 * e + 3]) * wo + wk * x.w);
+                        }
+                        tmem_st32(tOi + c, o);
                     }
+                    tmem_wait_st();
                 }
+                softmax_bar();                      // the last piece's smem is read: staging free
+                store_rows_bf16<D>(p, tOi, inv, sEpi + warp * 4096, it.b, q - lane, it.h, lane);
                 tc_fence_before();
                 mbar_arrive(&o_empty[i]);
             }
         }
+#ifdef TM_SPANS_MERGE
+        if (threadIdx.x == 0) trace_span(p, 4);   // (spans A/B) softmax loop left, before the final barrier
+#endif
         if (threadIdx.x == 0) {
             trace_span(p, 6, g);
             uint32_t smid;
@@ -868,7 +953,7 @@ bool make_map(CUtensorMap* m, const void* base, int d, int H, int64_t L, int B, 
 
 template <int D>
 constexpr int smem_bytes() {
-    return 1024 + (2 + kStages) * kBN * D * 2 + 512;
+    return 1024 + (2 + kStages) * kBN * D * 2 + kEpiBytes + 512;
 }
 
 int sm_count() {
