@@ -461,6 +461,9 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
             uint32_t pending_store = 0, store_par = 0;   // per slot: pending bit / phase parity bit
             uint32_t ok = 0;                               // peer (tensor, source) pairs already landed
             bool kv_released = !p.push;                    // fused push: K/V not yet released
+#ifdef TM_SPANS_PROD
+            long long cyc_empty = 0, cyc_store = 0;
+#endif
             int n_loads = 0;
             Item it;
             for (int w = 0; get_item(p, w, it); ++w, ++n_item) {
@@ -489,9 +492,19 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                     tile_info(p, it.lo + jj, seg, row, valid);
                     const int s = kv_it % kStages;
                     trace_ev(p, 0, tn, 3 + kv);
+#ifdef TM_SPANS_PROD
+                    long long tw0 = clock64();
+#endif
                     mbar_wait(&kv_empty[s], ((kv_it / kStages) & 1) ^ 1);
+#ifdef TM_SPANS_PROD
+                    long long tw1 = clock64();
+                    cyc_empty += tw1 - tw0;
+#endif
                     if ((pending_store >> s) & 1) {       // previous occupant being appended
                         mbar_wait(&store_done[s], (store_par >> s) & 1);
+#ifdef TM_SPANS_PROD
+                        cyc_store += clock64() - tw1;
+#endif
                         store_par ^= 1u << s;
                         pending_store &= ~(1u << s);
                         trace_ev(p, 0, tn, 5);
@@ -515,6 +528,10 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                 }
             }
             if (!kv_released) peer_release(p.pp.ctr, p.pp.own, p.pp.P, p.pp.rank, 1);
+#ifdef TM_SPANS_PROD
+            trace_span(p, 1, cyc_store);
+            trace_span(p, 5, cyc_empty);
+#endif
         }
       } else if (warp == 10) {
 #ifdef TM_TRACE_ENABLED

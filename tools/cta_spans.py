@@ -87,7 +87,7 @@ for c in range(C):
             lo, hi = max(s, u * n_tiles) - u * n_tiles, min(e, (u + 1) * n_tiles) - u * n_tiles
             items.append((f"u{u}[{lo},{hi})", hi - lo))
             u += 1
-    rows.append({"cta": c, "smid": int(smid[c]), "exit": float(rel[c, 3]), "first_s": float(rel[c, 1]),
+    rows.append({"cta": c, "raw": [int(x) for x in allw[c]], "smid": int(smid[c]), "exit": float(rel[c, 3]), "first_s": float(rel[c, 1]),
                  "merge_wait": float(rel[c, 4]) if raw[c, 4] else None,
                  "merge_go": float(rel[c, 5]) if raw[c, 5] else None,
                  "item2": float(rel[c, 2]) if raw[c, 2] else None, "rate": float(rate_all[c]),

@@ -16,7 +16,7 @@ from paper_2506_03099_b200 import tm  # noqa: E402
 cfg = os.environ.get("SWEEP_CFG", "512")
 H, d, Lr, Lc = (40, 128, 1024, 3072) if cfg == "512" else (40, 128, 2025, 6075)
 H = int(os.environ.get("SWEEP_H", H))     # e.g. 20/10/5: one rank's heads at P = 2/4/8
-NL = 8
+NL = int(os.environ.get("SWEEP_NL", 8))   # layer caches rotated (8: operands from HBM)
 ca = tm.ChunkAttention(H, d, Lr, Lc, NL, 1)
 g = torch.Generator(device="cuda").manual_seed(1)
 mk = lambda L: torch.randn(L, H, d, device="cuda", dtype=torch.bfloat16, generator=g)
@@ -28,10 +28,16 @@ for l in range(NL):
 chunk = [0] * NL
 
 
+APPEND = os.environ.get("SWEEP_APPEND") == "1"     # fused c_t append (as in bench's step)
+
+
 def call(i):
     l = i % NL
     chunk[l] += 1
-    kp, vp = ca.slot_ptr(l, 0, chunk[l])
+    if APPEND:
+        kp, vp = ks, vs
+    else:
+        kp, vp = ca.slot_ptr(l, 0, chunk[l])
     ca.attend(l, 0, chunk[l], qs[i % 4], kp, vp, o)
 
 
@@ -56,6 +62,6 @@ torch.cuda.synchronize()
 ms = [a.elapsed_time(b) for a, b in ev]
 fl = 4.0 * Lc * (Lr + 2 * Lc) * d * H
 med = statistics.median(ms)
-print(f"{os.environ.get('TM_POLY', '-'):>3} sched={os.environ.get('TM_SCHED_SPLIT', '0')} "
+print(f"{os.environ.get('TM_POLY', '-'):>3} append={int(APPEND)} "
       f"cfg={cfg} H={H} median {med * 1e3:7.1f} us  "
       f"{fl / med / 1e9:7.1f} TFLOP/s  min {min(ms) * 1e3:7.1f} us")
