@@ -10,14 +10,18 @@
 //
 // Blackwell design.  Work unit = (batch, head, pair of 128-row Q tiles).
 // PERSISTENT grid of min(#SMs, 160) CTAs, one per SM: CTA c runs units c,
-// c+C, ... (whole); the T = U mod C tail units are split along the KV axis
-// into S = C/T pieces so the last wave fills the machine (split-KV tail);
-// the last piece of a unit to finish merges the pieces' (O, m, l) in fixed
-// piece order (deterministic, no floating-point atomics).
+// c+C, ... (whole); the KV tiles of the T = U mod C tail units are then cut
+// into contiguous ranges over the CTAs (stream-K, host-balanced with a
+// per-item cost).  A unit cut by range ends becomes pieces; piece 0 is its
+// CTA's last item, so it keeps O in TMEM, pulls the other pieces' partials
+// (O, m, l) into shared memory by bulk copy and merges them in piece order
+// (deterministic, no floating-point atomics).
 // Warp roles (384 threads; setmaxnreg gives the softmax warpgroups 216 regs):
-//   warp 8      TMA producer: Q_i per unit, K_j / V_j through a 5-slot smem
-//               ring in the order K0, K1, V0, K2, V1, ... (K one tile ahead of
-//               V; cp.async.bulk.tensor, 128B swizzle).
+//   all         (peer transport, P > 1) push this rank's Q, then K/V shards
+//               into the head owners' windows before taking roles.
+//   warp 8      TMA producer: per item Q_0, K_lo, Q_1, then K/V through a
+//               4-slot smem ring in the order K_lo+1, V_lo, K_lo+2, V_lo+1, ...
+//               (K one tile ahead of V; cp.async.bulk.tensor, 128B swizzle).
 //   warp 9      S issuer + TMEM owner: S_i(j) = Q_i K_j^T (SS, M=128 N=128
 //               K=d, fp32) into ONE S buffer shared by both Q tiles, refilled
 //               as soon as the previous S is in registers (s_free).
@@ -35,7 +39,10 @@
 //               MUFU pipe with a share on an FMA-pipe polynomial (kPolyMask),
 //               packed FADD2 row sums, P rounded to bf16 (RNE) and held in
 //               registers until the previous PV_i has consumed P_i; epilogue
-//               O/l -> bf16 (or the unnormalised partial for split pieces).
+//               O/l -> bf16 through a per-warp swizzled smem staging buffer
+//               (coalesced rows; or the unnormalised partial of a piece).
+// Launched with programmatic dependent launch: the prologue overlaps the
+// previous kernel's tail (griddepcontrol.wait before any global access).
 // TMEM: S [0,128) (shared), P0 [128,192) P1 [192,256), O0 [256,256+d) O1 [256+d,256+2d).
 #include <cuda.h>
 #include <cuda_bf16.h>

@@ -70,6 +70,16 @@ def test_ragged_segments(dtype, Lr, Lc):
     assert err <= (FP32_TOL if dtype == "fp32" else BF16_ALARM), err
 
 
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+@pytest.mark.parametrize("H,Lr,Lc", [(1, 7000, 200), (1, 2000, 256), (2, 5000, 130)])
+def test_few_units_long_kv_many_pieces(dtype, H, Lr, Lc):
+    """Few work units with long KV ranges: the stream-K tail cuts one unit into
+    up to 14 pieces over 14 CTAs (1 x 1 x 59 tiles at Lr=7000), so the merger
+    accumulates 13 partials (two batches of weight loads, 13 bulk copies)."""
+    err = run_stream(H, 128, Lr, Lc, dtype, chunks=2)
+    assert err <= (FP32_TOL if dtype == "fp32" else BF16_ALARM), err
+
+
 @pytest.mark.parametrize("dist", ["D1", "D2", "D3", "D6"])
 def test_distributions_bf16(dist):
     err = run_stream(4, 128, 256, 640, "bf16", dist=dist, chunks=3)
