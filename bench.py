@@ -379,6 +379,10 @@ def main():
     sets = [[torch.randn(Lc_s, H, d, device="cuda", dtype=bf, generator=g) for _ in range(3)]
             for _ in range(NB)]
     outs = [torch.empty(Lc_s, H, d, device="cuda", dtype=bf) for _ in range(NB)]
+    if transport == "peer" and P > 1:
+        # zero-copy output: the ranks' epilogues write straight into this rank's
+        # O window, the receive phase only waits (tm_peer_output_ptr)
+        outs = [ca.output_window()[0]] * NB
     xlat = torch.randn(c["latent"], device="cuda", generator=g)
     vlat = torch.randn(c["latent"], device="cuda", generator=g).to(bf)
     kref = torch.randn(Lr_s, H, d, device="cuda", dtype=bf, generator=g)

@@ -234,6 +234,14 @@ tm_status tm_peer_export(tm_ctx* ctx, uint8_t handle[TM_PEER_HANDLE_BYTES]);
 tm_status tm_peer_connect(tm_ctx* ctx, const uint8_t* handles);
 tm_status tm_peer_connect_local(tm_ctx* const* ctxs, int32_t n);
 
+/* TM_TRANSPORT_PEER zero-copy output: the device pointer of this rank's O
+ * window ([B][ceil(Lc/P)][H][d], bf16).  Passing it as `o` to
+ * tm_chunk_attention(_phases) skips the receive copy: the RECV phase only
+ * waits until every rank has stored its rows.  The window is rewritten by the
+ * next call; rows past the end of the sequence (shard padding) are
+ * unspecified (the copying RECV writes zeros there). */
+tm_status tm_peer_output_ptr(tm_ctx* ctx, void** o);
+
 /* Synchronises the device and reports whether a device-side peer wait timed
  * out (10 s without the expected peer signal) since the last check:
  * TM_ERR_CUDA with a message, else TM_OK.  Clears the flag. */

@@ -648,7 +648,12 @@ tm_status tm_chunk_attention_phases(tm_ctx* ctx, int32_t layer, int32_t step, in
                             "attention kernel launch (peer)");
             if (st) return st;
         }
-        if (phases & TM_PHASE_RECV) {
+        if ((phases & TM_PHASE_RECV) && o == ctx->wo(r)) {
+            // zero-copy output (tm_peer_output_ptr): only wait for every rank's rows
+            st = cuda_check(launch_peer_wait_done(ctx->ctr(r), ctx->e_done, Ly.P, cs, &ctx->launches),
+                            "peer receive (zero-copy)");
+            if (st) return st;
+        } else if (phases & TM_PHASE_RECV) {
             st = cuda_check(launch_peer_recv_o(ctx->ctr(r), ctx->e_done, Ly.P, ctx->wo(r), o, cf.batch,
                                                Ly.Lc_s, Ly.Lc, r, cf.heads * cf.head_dim * Ly.esize,
                                                cs, &ctx->launches),
@@ -1055,6 +1060,13 @@ tm_status tm_peer_connect_local(tm_ctx* const* ctxs, int32_t n) {
         for (int p = 0; p < n; ++p) ctxs[i]->win[p] = ctxs[p]->win[p];
         ctxs[i]->connected = true;
     }
+    return TM_OK;
+}
+
+tm_status tm_peer_output_ptr(tm_ctx* ctx, void** o) {
+    if (!ctx || !o) return fail(TM_ERR_INVALID_ARG, "null argument");
+    if (!ctx->lay.peer) return fail(TM_ERR_INVALID_ARG, "not a TM_TRANSPORT_PEER context");
+    *o = ctx->wo(ctx->cfg.rank);
     return TM_OK;
 }
 

@@ -72,6 +72,7 @@ def _load():
         "tm_peer_connect": ([V, ctypes.c_char_p], i32),
         "tm_peer_connect_local": ([P(V), i32], i32),
         "tm_peer_check": ([V], i32),
+        "tm_peer_output_ptr": ([V, P(V)], i32),
         "tm_peer_route_host": ([i32, V, V, i32, i64, i64, i64, i32, i32, i32, i32, i32], i32),
         "tm_kvcache_slot_ptr": ([V, i32, i32, i64, P(V), P(V)], i32),
         "tm_kvcache_ref_ptr": ([V, i32, i32, P(V), P(V)], i32),
@@ -101,7 +102,7 @@ EXPORTED = ("tm_version", "tm_last_error", "tm_kvcache_bytes", "tm_workspace_byt
             "tm_window_attention", "tm_flow_sampler_step", "tm_audio_scratch_bytes",
             "tm_audio_cross_attention", "tm_chunk_attention_phases",
             "tm_kvcache_put_reference_phases", "tm_peer_export", "tm_peer_connect",
-            "tm_peer_connect_local", "tm_peer_check", "tm_peer_route_host",
+            "tm_peer_connect_local", "tm_peer_check", "tm_peer_route_host", "tm_peer_output_ptr",
             "tm_last_launch_count",
             "tm_kernel_variant")
 
@@ -200,6 +201,12 @@ def tm_peer_connect_local(ctxs) -> None:
     _check(lib.tm_peer_connect_local(arr, len(ctxs)))
 
 
+def tm_peer_output_ptr(ctx) -> int:
+    o = ctypes.c_void_p()
+    _check(lib.tm_peer_output_ptr(ctx, ctypes.byref(o)))
+    return o.value
+
+
 def tm_peer_check(ctx) -> None:
     _check(lib.tm_peer_check(ctx))
 
@@ -266,6 +273,18 @@ def tm_last_launch_count(ctx) -> int:
 
 def tm_kernel_variant(ctx) -> str:
     return lib.tm_kernel_variant(ctx).decode()
+
+
+def _wrap_device_ptr(ptr, numel, dtype, device):
+    """A torch tensor aliasing `numel` elements at device pointer `ptr` (no copy)."""
+    import torch
+
+    class _Holder:
+        __cuda_array_interface__ = {
+            "shape": (numel,), "typestr": "<i2", "data": (ptr, False), "version": 3}
+
+    t = torch.as_tensor(_Holder(), device=torch.device("cuda", device))
+    return t.view(dtype)
 
 
 _cudart_lib = None
@@ -394,6 +413,16 @@ class ChunkAttention:
 
     def check(self):
         tm_peer_check(self.ctx)
+
+    def output_window(self):
+        """torch view of this rank's O window (zero-copy output, TM_TRANSPORT_PEER)."""
+        import torch
+        ptr = tm_peer_output_ptr(self.ctx)
+        Ls = -(-self.cfg.chunk_tokens // self.cfg.world_size)
+        shape = (self.cfg.batch, Ls, self.cfg.heads, self.cfg.head_dim)
+        n = shape[0] * shape[1] * shape[2] * shape[3]
+        # wrap the raw device pointer without copying (the ctx owns its lifetime)
+        return _wrap_device_ptr(ptr, n, torch.bfloat16, self.cfg.device).view(shape)
 
     def slot_ptr(self, layer, step, chunk):
         return tm_kvcache_slot_ptr(self.ctx, layer, step, chunk)

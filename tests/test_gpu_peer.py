@@ -322,3 +322,33 @@ def test_peer_two_processes_ipc_fused(tmp_path):
             full = np.concatenate([np.load(tmp_path / f"o_r{s}_t{t}.npy") for s in range(P)])
             assert (full[Lc:] == 0).all()
             assert (full[:Lc, r * Hl:(r + 1) * Hl] == bits(ref[t - 1])).all(), (r, t)
+
+
+def test_peer_zero_copy_output_window():
+    """tm_peer_output_ptr: passing the O window as `o` skips the receive copy;
+    the valid rows equal the copying path's output bit for bit."""
+    P, H, d, Lr, Lc = 2, 8, 128, 300, 333
+    host, dev = make_inputs(H, d, Lr, Lc, 2, syn.seed_for(14, 0))
+    ref = _run_virtual(P, H, d, Lr, Lc, dev)
+    cas = [tm.ChunkAttention(H, d, Lr, Lc, 1, 1, world_size=P, rank=r, transport=PEER)
+           for r in range(P)]
+    tm.ChunkAttention.connect_local(cas)
+    _, kr, vr = dev[0]
+    for ph in (tm.TM_PHASE_SEND, tm.TM_PHASE_ATTEND, tm.TM_PHASE_RECV):
+        for r in range(P):
+            cas[r].put_reference_phases(0, 0, shard(kr, Lr, P, r), shard(vr, Lr, P, r), ph)
+    wins = [c.output_window() for c in cas]
+    Ls = -(-Lc // P)
+    for t in (1, 2):
+        q, k, v = dev[t]
+        for ph in (tm.TM_PHASE_SEND, tm.TM_PHASE_ATTEND, tm.TM_PHASE_RECV):
+            for r in range(P):
+                cas[r].attend_phases(0, 0, t, shard(q, Lc, P, r), shard(k, Lc, P, r),
+                                     shard(v, Lc, P, r), wins[r][0], ph)
+        torch.cuda.synchronize()
+        full = torch.cat([w[0] for w in wins], dim=0)[:Lc]
+        assert cas[0].launches == 1            # the wait kernel only, no copy
+        assert (bits(full.contiguous()) == bits(ref[t - 1])).all(), t
+    for c in cas:
+        c.check()
+        c.close()
