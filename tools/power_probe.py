@@ -43,7 +43,10 @@ a.record()
 for i in range(n):
     l = i % NL
     chunk[l] += 1
-    kp, vp = ca.slot_ptr(l, 0, chunk[l])
+    if os.environ.get("PROBE_APPEND") == "1":      # fused c_t append (bench's step)
+        kp, vp = ks, vs
+    else:
+        kp, vp = ca.slot_ptr(l, 0, chunk[l])
     ca.attend(l, 0, chunk[l], qs[i % 4], kp, vp, o)
 b.record()
 torch.cuda.synchronize()
@@ -55,7 +58,7 @@ rows = [r.split(",") for r in tmp.read().strip().splitlines()]
 load = [r for r in rows if float(r[1]) > 300]
 us = a.elapsed_time(b) * 1e3 / n
 fl = 4.0 * Lc * (Lr + 2 * Lc) * d * H
-print(f"TM_POLY={os.environ.get('TM_POLY', '-')}: {n} calls, {us:.1f} us/call, {fl / us / 1e6:.1f} TFLOP/s")
+print(f"TM_POLY={os.environ.get('TM_POLY', '-')} append={os.environ.get('PROBE_APPEND', '0')}: {n} calls, {us:.1f} us/call, {fl / us / 1e6:.1f} TFLOP/s")
 if load:
     print("under load: sm MHz median", statistics.median(float(r[0]) for r in load),
           " power W median", statistics.median(float(r[1]) for r in load),
