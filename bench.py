@@ -157,6 +157,68 @@ class ClockSampler:
                 "samples": len(sm), "in_timed_window": inside}
 
 
+class NvmlSampler:
+    """In-process NVML polling (~1 ms) of the SM clock and clock-event reasons
+    from a thread, so that even a ~13 ms timed region gets samples (the
+    nvidia-smi poller's 20 ms period can miss it)."""
+
+    BITS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20,
+            "hw_thermal_slowdown": 0x40}
+
+    def __init__(self, device_index):
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.smax = float(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
+            self.ok = True
+        except Exception:
+            pass
+        self.samples = []
+        self.thread = None
+
+    def _reasons(self):
+        nv = self.nv
+        f = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        return int(f(self.h))
+
+    def start(self):
+        import threading
+        if not self.ok:
+            return
+        self.samples = []
+        self.stop_flag = False
+
+        def loop():
+            while not self.stop_flag:
+                try:
+                    self.samples.append((float(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)),
+                                         self._reasons()))
+                except Exception:
+                    pass
+                time.sleep(0.001)
+
+        self.thread = threading.Thread(target=loop, daemon=True)
+        self.thread.start()
+
+    def stop(self):
+        if self.thread:
+            self.stop_flag = True
+            self.thread.join(timeout=2)
+            self.thread = None
+
+    def summary(self):
+        if not self.samples:
+            return None
+        reasons = sorted(nm for nm, bit in self.BITS.items() if any(r & bit for _, r in self.samples))
+        return {"sm_mhz": statistics.median(c for c, _ in self.samples), "sm_max_mhz": self.smax,
+                "reasons": reasons, "samples": len(self.samples), "in_timed_window": True,
+                "source": "NVML, ~1 ms polling thread"}
+
+
 # ----------------------------------------------------------------------------- reference arm
 
 _ORACLE_INPUTS = {}
@@ -429,6 +491,7 @@ def main():
     # ---------------------------------------------------------------- main timed region
     clocks = ClockSampler(local)
     clocks.start()
+    nvml = NvmlSampler(local)
     launches[0] = 0
     barrier()
     w0 = time.time()
@@ -440,11 +503,13 @@ def main():
     EV_EVERY = 4
     lev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(0, args.steps, EV_EVERY)]
+    nvml.start()
     e0.record(stream)
     for i in range(args.steps):
         step(i, ev=lev[i // EV_EVERY] if i % EV_EVERY == 0 else None)
     e1.record(stream)
     barrier()
+    nvml.stop()
     w1 = time.time()
     ms_total = max_over_ranks(e0.elapsed_time(e1))
     live = [a.elapsed_time(b) for a, b in lev]
@@ -488,7 +553,7 @@ def main():
     if transport == "peer":
         ca.check()      # raises if any device-side peer wait timed out (results would be garbage)
     clocks.stop()
-    clk = clocks.summary(window=(w0, w1))
+    clk = nvml.summary() or clocks.summary(window=(w0, w1))
     kclk = clocks.summary(window=(w2, w3))
     k_list = [a.elapsed_time(b) for a, b in kev]
     k_ms = max_over_ranks(statistics.mean(k_list))
