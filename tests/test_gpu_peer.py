@@ -291,13 +291,16 @@ def _ipc_worker(rank, world, port, H, d, Lr, Lc, outdir, errq):
         raise
 
 
-def test_peer_two_processes_ipc_fused(tmp_path):
-    """World size 2 as two processes sharing the device: windows exchanged as
-    CUDA IPC handles over torch.distributed (gloo), every call fused (push in
-    the attention kernel, epilogue scatter, receive).  Each rank's shard of
-    the output equals the direct path's rows bit for bit per head block."""
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_peer_two_processes_ipc_fused(tmp_path, P):
+    """World size 2 (and 4) as processes sharing the device: windows exchanged
+    as CUDA IPC handles over torch.distributed (gloo), every call fused (push
+    in the attention kernel, epilogue scatter, receive).  Each rank's shard of
+    the output equals the direct path's rows bit for bit per head block.  At
+    P = 4 and 8 the shards are 250 and 125 rows, so Q and K/V tiles span two
+    source ranks; P = 8 is the node-size group of the multi-GPU benchmark."""
     import torch.multiprocessing as mp
-    H, d, Lr, Lc, P = 8, 128, 256, 1000, 2
+    H, d, Lr, Lc = 8, 128, 256, 1000
     ctx = mp.get_context("spawn")
     errq = ctx.Queue()
     port = _free_port()
