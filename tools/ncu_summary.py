@@ -75,8 +75,12 @@ def summarise_launches(path):
             agg[k][0] += 1
             agg[k][1] += float(d["Metric Value"]) * scale
     tot = sum(v[1] for v in agg.values())
+    # share among this library's kernels only (tmk::): the launch list also holds
+    # the bench's input generation (torch randn), which is outside the timed step
+    tot_tm = sum(v[1] for k, v in agg.items() if "tmk::" in k) or 1.0
     return [{"kernel": k, "launches": v[0], "total_us": v[1], "mean_us": v[1] / v[0],
-             "share": v[1] / tot} for k, v in sorted(agg.items(), key=lambda x: -x[1][1])]
+             "share": v[1] / tot, "share_of_tm_kernels": (v[1] / tot_tm) if "tmk::" in k else None}
+            for k, v in sorted(agg.items(), key=lambda x: -x[1][1])]
 
 
 def main():
