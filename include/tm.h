@@ -173,6 +173,18 @@ tm_status tm_chunk_attention(tm_ctx* ctx, int32_t layer, int32_t step, int64_t c
                              const void* q, const void* k, const void* v, void* o,
                              void* stream);
 
+/* Chunk 0 generated by the model (SURVEY Sec 8(b) optional mode; P:141 c_0
+ * "containing the ground truth image", "chunk 0 attends itself only"):
+ * o = softmax(q k^T / sqrt(d)) v over the reference tokens only, and k, v are
+ * stored as the reference of (layer, step) (step = -1: every step), as
+ * tm_kvcache_put_reference would.  q, k, v, o: device [B][Lr][H][d].  Same
+ * immutability rule as tm_kvcache_put_reference (TM_ERR_REF_IMMUTABLE after
+ * chunk 1).  world_size 1 direct contexts only (else TM_ERR_UNSUPPORTED).
+ * bf16: one launch (the attention kernel appends K/V into the cache as it
+ * reads them). */
+tm_status tm_reference_attention(tm_ctx* ctx, int32_t layer, int32_t step, const void* q,
+                                 const void* k, const void* v, void* o, void* stream);
+
 /* the full-window form (P:130-143 and Eq 7 over a whole
  * training window, e.g. 21 latent frames = 7 chunks x 3 frames, P:134-136;
  * the DMD student's teacher-forcing pattern): q, k, v, o are device

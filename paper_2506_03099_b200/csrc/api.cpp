@@ -758,6 +758,61 @@ tm_status tm_chunk_attention_phases(tm_ctx* ctx, int32_t layer, int32_t step, in
     return debug_check(ctx, o, n_out, cf.dtype == TM_BF16, cs, "tm_chunk_attention");
 }
 
+tm_status tm_reference_attention(tm_ctx* ctx, int32_t layer, int32_t step, const void* q,
+                                 const void* k, const void* v, void* o, void* stream) {
+    if (!ctx || !q || !k || !v || !o) return fail(TM_ERR_INVALID_ARG, "null argument");
+    if (ctx->lay.exchange || ctx->lay.P > 1 || ctx->lay.peer)
+        return fail(TM_ERR_UNSUPPORTED, "tm_reference_attention needs a world_size == 1 direct context");
+    tm_status st = check_layer_step(ctx, layer, step, true);
+    if (st) return st;
+    if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o))
+        return fail(TM_ERR_INVALID_ARG, "q, k, v, o must be 16-byte aligned");
+    const int s0 = step < 0 ? 0 : step, s1 = step < 0 ? ctx->cfg.num_steps : step + 1;
+    for (int s = s0; s < s1; ++s)
+        if (ctx->last[ctx->idx(layer, s)] >= 1)
+            return fail(TM_ERR_REF_IMMUTABLE,
+                        "reference of (layer %d, step %d) is immutable after chunk 1 until "
+                        "tm_stream_reset (S:287)", layer, s);
+    const tm_config& cf = ctx->cfg;
+    const Layout& Ly = ctx->lay;
+    cudaStream_t cs = static_cast<cudaStream_t>(stream);
+    ctx->launches = 0;
+    // c_0's queries attend c_0 only: one segment, and (bf16) the
+    // kernel appends that segment's K/V into the reference region as it reads it.
+    AttnProblem pr;
+    pr.q = q;
+    pr.o = o;
+    pr.Lq = Ly.Lr;
+    pr.B = cf.batch;
+    pr.H = Ly.Hl;
+    pr.d = cf.head_dim;
+    pr.scale = ctx->scale;
+    pr.seg[pr.nseg++] = Segment{k, v, Ly.Lr};
+    cudaError_t e;
+    if (cf.dtype == TM_BF16) {
+        pr.store_k = ctx->kref(layer, s0);
+        pr.store_v = ctx->vref(layer, s0);
+        e = launch_fmha_sm100(pr, ctx->scratch(), cs, &ctx->launches);
+    } else {
+        const size_t bytes = size_t(cf.batch) * Ly.Lr * Ly.Hl * cf.head_dim * Ly.esize;
+        e = cudaMemcpyAsync(ctx->kref(layer, s0), k, bytes, cudaMemcpyDeviceToDevice, cs);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(ctx->vref(layer, s0), v, bytes, cudaMemcpyDeviceToDevice, cs);
+        if (e == cudaSuccess) e = launch_fmha_fp32(pr, cs, &ctx->launches);
+    }
+    st = cuda_check(e, "reference attention launch");
+    if (st) return st;
+    for (int s = s0 + 1; s < s1; ++s) {
+        st = cuda_check(cudaMemcpyAsync(ctx->kref(layer, s), ctx->kref(layer, s0), 2 * Ly.ref_bytes,
+                                        cudaMemcpyDeviceToDevice, cs),
+                        "reference alias copy");
+        if (st) return st;
+    }
+    for (int s = s0; s < s1; ++s) ctx->ref_ok[ctx->idx(layer, s)] = 1;
+    return debug_check(ctx, o, int64_t(cf.batch) * Ly.Lr * cf.heads * cf.head_dim,
+                       cf.dtype == TM_BF16, cs, "tm_reference_attention");
+}
+
 tm_status tm_window_attention(tm_ctx* ctx, const void* q, const void* k, const void* v, void* o,
                               const int64_t* chunk_len, int32_t n_chunks, void* stream) {
     if (!ctx || !q || !k || !v || !o || !chunk_len) return fail(TM_ERR_INVALID_ARG, "null argument");

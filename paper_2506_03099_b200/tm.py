@@ -79,6 +79,7 @@ def _load():
         "tm_flow_euler_step": ([V, V, V, i32, i64, ctypes.c_float, V], i32),
         "tm_ulysses_shuffle_host": ([i32, V, V, i32, i64, i64, i32, i32, i32, i32], i32),
         "tm_window_attention": ([V, V, V, V, V, P(i64), i32, V], i32),
+        "tm_reference_attention": ([V, i32, i32, V, V, V, V, V], i32),
         "tm_audio_scratch_bytes": ([V, i64, i64], S),
         "tm_audio_cross_attention": ([V, V, V, V, V, i64, i64, i64, V, i64, i32, V, S, V], i32),
         "tm_flow_sampler_step": ([V, V, V, i32, i64, ctypes.c_float, ctypes.c_float, V,
@@ -99,7 +100,7 @@ EXPORTED = ("tm_version", "tm_last_error", "tm_kvcache_bytes", "tm_workspace_byt
             "tm_get_unique_id", "tm_attn_init", "tm_attn_destroy", "tm_stream_reset",
             "tm_kvcache_put_reference", "tm_chunk_attention", "tm_kvcache_slot_ptr",
             "tm_kvcache_ref_ptr", "tm_flow_euler_step", "tm_ulysses_shuffle_host",
-            "tm_window_attention", "tm_flow_sampler_step", "tm_audio_scratch_bytes",
+            "tm_window_attention", "tm_reference_attention", "tm_flow_sampler_step", "tm_audio_scratch_bytes",
             "tm_audio_cross_attention", "tm_chunk_attention_phases",
             "tm_kvcache_put_reference_phases", "tm_peer_export", "tm_peer_connect",
             "tm_peer_connect_local", "tm_peer_check", "tm_peer_route_host", "tm_peer_output_ptr",
@@ -244,6 +245,11 @@ def tm_audio_cross_attention(ctx, q, k_audio, v_audio, o, frames, tokens_per_fra
                                         tokens_per_frame, audio_tokens_per_frame, _ptr(face_ids),
                                         n_face, window, _ptr(scratch), scratch_bytes,
                                         _stream(stream)))
+
+
+def tm_reference_attention(ctx, layer, step, q, k, v, o, stream=None) -> None:
+    _check(lib.tm_reference_attention(ctx, layer, step, _ptr(q), _ptr(k), _ptr(v), _ptr(o),
+                                      _stream(stream)))
 
 
 def tm_window_attention(ctx, q, k, v, o, chunk_lens, stream=None) -> None:
@@ -429,6 +435,11 @@ class ChunkAttention:
 
     def ref_ptr(self, layer, step):
         return tm_kvcache_ref_ptr(self.ctx, layer, step)
+
+    def reference_attend(self, layer, step, q, k, v, o, stream=None):
+        """Chunk 0 generated by the model: o = attention over c_0, and k, v cached."""
+        tm_reference_attention(self.ctx, layer, step, q, k, v, o, stream)
+        return o
 
     def window(self, q, k, v, o, chunk_lens, stream=None):
         tm_window_attention(self.ctx, q, k, v, o, chunk_lens, stream)

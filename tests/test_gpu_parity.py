@@ -393,6 +393,41 @@ def test_table1_four_steps_cache_slots():
     assert err <= BF16_ALARM, err
 
 
+# ------------------------------------------------------------------ chunk 0 generated
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+@pytest.mark.parametrize("Lr", [1, 300, 1024])
+def test_reference_attention_mode(dtype, Lr):
+    """tm_reference_attention: c_0's queries attend c_0 only -- the
+    window oracle with one chunk -- and its K/V become the cached reference,
+    so the following chunks match the streaming oracle fed the same K/V;
+    step = -1 stores it for both steps."""
+    H, d, Lc = 4, 128, 200
+    rng = np.random.default_rng(syn.seed_for(15, 0, extra=Lr))
+    q0, k0, v0 = syn.chunk_qkv(rng, Lr, H, d, dtype, "D0")
+    ca = tm.ChunkAttention(H, d, Lr, Lc, 1, 2, dtype=DT[dtype])
+    o0 = torch.empty_like(to_dev(q0))
+    ca.reference_attend(0, -1, to_dev(q0), to_dev(k0), to_dev(v0), o0)
+    torch.cuda.synchronize()
+    tol = FP32_TOL if dtype == "fp32" else BF16_ALARM
+    ref0 = oracle.window_attention(q0.f64, k0.f64, v0.f64, [Lr])
+    assert rel_err(from_dev(o0), ref0) <= tol
+    si = syn.StreamInputs(H, d, Lr, Lc, dtype, "D0", syn.seed_for(15, 1, extra=Lr))
+    so = oracle.StreamOracle()
+    for st in range(2):
+        so.put_reference(0, st, k0.f64, v0.f64)
+    for t in (1, 2):
+        for st in range(2):
+            q, k, v = si.chunk(0, st, t)
+            o = torch.empty_like(to_dev(q))
+            ca.attend(0, st, t, to_dev(q), to_dev(k), to_dev(v), o)
+            assert rel_err(from_dev(o), so.attend(0, st, t, q.f64, k.f64, v.f64)) <= tol
+    with pytest.raises(tm.TMError) as e:              # immutable after chunk 1 (S:287)
+        ca.reference_attend(0, 0, to_dev(q0), to_dev(k0), to_dev(v0), o0)
+    assert e.value.status == 5
+    ca.close()
+
+
 # ------------------------------------------------------------------ SURVEY Sec 8(f) f1: full window
 
 def _window_inputs(H, d, lens, dtype, dist, seed):
