@@ -3,7 +3,17 @@
 CTA entry, first S seen by the softmax, second item start, exit).  Shows the
 fixed per-launch costs (prologue latency, tail spread) at a given head count:
     SWEEP_H=5 python tools/cta_spans.py      (one rank's heads at P = 8)
-Rebuilds libtm.so with -DTM_SPANS_ENABLED; rebuild normally afterwards."""
+Rebuilds libtm.so with -DTM_SPANS_ENABLED; rebuild normally afterwards.
+
+Per-CTA words: 0 entry, 1 first S seen, 2 second item start, 3 exit,
+4 merge wait begin, 5 merge go (globaltimer ns), 6 tiles, 7 items | smid << 16.
+Extra A/B instrumentation via TM_EXTRA_DEFINES (same slots, other meanings):
+  TM_SPANS_MERGE  2 = start of each item's epilogue (the last one survives),
+                  1 = O loaded from TMEM in the row store, 4 = softmax loop left,
+                  5 = merge go (mergers) / row store done (others)
+  TM_SPANS_PROD   1 = producer clock64 cycles waiting on store_done,
+                  5 = producer cycles waiting on kv_empty (raw values in "raw")
+"""
 import os
 import statistics
 import subprocess
