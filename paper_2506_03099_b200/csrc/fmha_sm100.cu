@@ -1012,9 +1012,10 @@ cudaError_t launch_t(const FmhaParams& p, int grid, cudaStream_t stream) {
 // sustained).  Measured (random data, independent S/PV issuers, exact tile max):
 // 2/16 vs all-MUFU 1382 vs 1363 TFLOP/s burst, 1172 vs 1156 sustained;
 // 3/16 = 2/16, 4/16 and more slower (profiles/README.md).  With the fused
-// c_t append (store warp busy, 66 MB more DRAM writes) all-MUFU measured
-// better: 328.3 vs 332.0 us, while zero-copy calls prefer 2/16: 317.8 vs 324.0
-// (profiles/r1_poly_append_sweep.txt) -- so the default picks by launch.
+// c_t append all-MUFU measured ~1 % better (328.3 vs 332.0 us) and zero-copy
+// calls prefer 2/16 (317.8 vs 324.0; profiles/r1_poly_append_sweep.txt), but
+// one split for every launch keeps the append, zero-copy, window and Ulysses
+// paths bitwise identical (S:303 window == streaming), so the default is 2/16.
 // TM_POLY selects a split for tuning: 1 = all MUFU, 2 = 2/16, 3 = 3/16, 4 = 4/16.
 constexpr uint32_t kPolyDefault = 0x0808u;   // pairs {3, 11} of every 16
 template <int D>
@@ -1023,7 +1024,7 @@ cudaError_t launch_d(const FmhaParams& p, int grid, cudaStream_t stream) {
         const char* e = getenv("TM_POLY");
         return e ? atoi(e) : 0;
     }();
-    const int sel = env_sel ? env_sel : (p.store_seg >= 0 ? 1 : 2);
+    const int sel = env_sel ? env_sel : 2;
     switch (sel) {
         case 1: return launch_t<D, 0x0000u>(p, grid, stream);   // all MUFU
         case 3: return launch_t<D, 0x1084u>(p, grid, stream);   // {2,7,12}
