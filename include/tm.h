@@ -322,9 +322,9 @@ tm_status tm_peer_route_host(int32_t mode, const void* src, void* dst, int32_t b
                              int32_t heads_per_rank, int32_t world_size, int32_t rank,
                              int32_t head_dim, int32_t elem_bytes);
 
-/* Introspection for tests / bench: number of device kernels the last
- * tm_chunk_attention launched on this ctx, and the attention kernel
- * variant name ("sm100_tcgen05" or "fp32_simt"). */
+/* Introspection for tests / bench: number of device kernels the last call
+ * on this ctx launched (the TM_DEBUG finiteness check not counted), and the
+ * attention kernel variant name ("sm100_tcgen05" or "fp32_simt"). */
 int32_t tm_last_launch_count(const tm_ctx* ctx);
 const char* tm_kernel_variant(const tm_ctx* ctx);
 

@@ -199,7 +199,7 @@ tm_status debug_check(tm_ctx* c, const void* x, int64_t n, int is_bf16, cudaStre
     if (!c->debug) return TM_OK;
     tm_status st = cuda_check(cudaMemsetAsync(c->flag(), 0, sizeof(int), s), "debug memset");
     if (st) return st;
-    st = cuda_check(launch_nonfinite(x, is_bf16, n, c->flag(), s, &c->launches), "nonfinite check");
+    st = cuda_check(launch_nonfinite(x, is_bf16, n, c->flag(), s, nullptr), "nonfinite check");
     if (st) return st;
     int h = 0;
     st = cuda_check(cudaMemcpyAsync(&h, c->flag(), sizeof(int), cudaMemcpyDeviceToHost, s),
