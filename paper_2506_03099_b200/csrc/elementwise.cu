@@ -120,6 +120,22 @@ __global__ void __launch_bounds__(256) sampler_kernel(float* __restrict__ x,
     const bool aligned = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(vv) |
                            reinterpret_cast<uintptr_t>(xb)) & 15) == 0;
     for (int64_t gi = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; gi < groups; gi += stride) {
+        // Vector-path operands are loaded first so their latency overlaps the
+        // Philox / Box-Muller arithmetic below.
+        const bool vec = 4 * gi + 4 <= n && aligned;
+        float4 xv = make_float4(0.f, 0.f, 0.f, 0.f);
+        float vf[4] = {0.f, 0.f, 0.f, 0.f};
+        if (vec) {
+            xv = reinterpret_cast<const float4*>(x)[gi];
+            if constexpr (kBf16V) {
+                const uint2 w = reinterpret_cast<const uint2*>(vv)[gi];
+                vf[0] = __uint_as_float(w.x << 16); vf[1] = __uint_as_float(w.x & 0xffff0000u);
+                vf[2] = __uint_as_float(w.y << 16); vf[3] = __uint_as_float(w.y & 0xffff0000u);
+            } else {
+                const float4 w = reinterpret_cast<const float4*>(vv)[gi];
+                vf[0] = w.x; vf[1] = w.y; vf[2] = w.z; vf[3] = w.w;
+            }
+        }
         float e[4] = {0.f, 0.f, 0.f, 0.f};
         if (!final_step) {
             if constexpr (kEps) {
@@ -140,17 +156,7 @@ __global__ void __launch_bounds__(256) sampler_kernel(float* __restrict__ x,
             }
         }
         const int64_t i0 = 4 * gi;
-        if (i0 + 4 <= n && aligned) {            // vector path: 16 B x, 8 / 16 B v, 8 B bf16 out
-            const float4 xv = reinterpret_cast<const float4*>(x)[gi];
-            float vf[4];
-            if constexpr (kBf16V) {
-                const uint2 w = reinterpret_cast<const uint2*>(vv)[gi];
-                vf[0] = __uint_as_float(w.x << 16); vf[1] = __uint_as_float(w.x & 0xffff0000u);
-                vf[2] = __uint_as_float(w.y << 16); vf[3] = __uint_as_float(w.y & 0xffff0000u);
-            } else {
-                const float4 w = reinterpret_cast<const float4*>(vv)[gi];
-                vf[0] = w.x; vf[1] = w.y; vf[2] = w.z; vf[3] = w.w;
-            }
+        if (vec) {                               // vector path: 16 B x, 8 / 16 B v, 8 B bf16 out
             const float xs[4] = {xv.x, xv.y, xv.z, xv.w};
             float xn[4];
 #pragma unroll
