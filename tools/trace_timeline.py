@@ -42,7 +42,8 @@ for t in (1, 2, 3):
     o = torch.empty_like(q)
     ca.attend(0, 0, t, q, k, v, o)
 torch.cuda.synchronize()
-raw = np.fromfile(PATH, dtype=np.uint64).reshape(-1, 13, 4096)[-1]   # last call
+W = 13 * 4096 + 8 * 160        # role timelines + per-CTA span words (csrc/internal.h kTraceWords)
+raw = np.fromfile(PATH, dtype=np.uint64).reshape(-1, W)[-1][:13 * 4096].reshape(13, 4096)   # last call
 names = ["prod", "mma", "store", "mmapv", "obs"] + [f"w{k}" for k in range(8)]
 ev = []
 for r in range(13):
