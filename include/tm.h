@@ -117,7 +117,7 @@ typedef struct {
 typedef struct tm_ctx tm_ctx;
 
 /* Version of the ABI (major * 100 + minor). */
-int32_t tm_version(void);   /* 101: tm_config.transport, peer transport */
+int32_t tm_version(void);   /* 101: tm_config.transport, peer transport, tm_reference_attention */
 
 /* Thread-local message for the last non-OK status returned on this thread. */
 const char* tm_last_error(void);
@@ -128,7 +128,8 @@ const char* tm_last_error(void);
  * the config, independent of stream length.  0 on invalid config. */
 size_t tm_kvcache_bytes(const tm_config* cfg);
 
-/* Bytes of device workspace: split-KV scratch and a debug flag, plus the
+/* Bytes of device workspace: the split-unit partials and merge counters of
+ * the attention schedule and a debug flag, plus the
  * Ulysses staging (NCCL transport, world_size > 1) or the peer window
  * (TM_TRANSPORT_PEER: counters and Q, K, V windows [B][max(Lc,Lr)][H/P][d],
  * O window [B][Lc/P][H][d]).  0 is never returned for a valid config. */
@@ -140,7 +141,8 @@ tm_status tm_get_unique_id(uint8_t id[128]);
 
 /* Create a context.  `cache` (device, >= tm_kvcache_bytes, 1024-B aligned)
  * and `workspace` (device, >= tm_workspace_bytes, 256-B aligned) are owned
- * by the caller and must outlive the ctx.  nccl_id: NULL when world_size==1.
+ * by the caller and must outlive the ctx.  nccl_id: NULL when world_size==1
+ * or with TM_TRANSPORT_PEER (which then needs tm_peer_connect before use).
  * Validates the config (TM_ERR_SHAPE for H % P != 0, d not in {64,128},
  * non-positive lengths).  Collective when world_size > 1. */
 tm_status tm_attn_init(const tm_config* cfg, const uint8_t* nccl_id, void* cache,
@@ -168,7 +170,10 @@ tm_status tm_kvcache_put_reference(tm_ctx* ctx, int32_t layer, int32_t step, con
  * (a redo of the same chunk, which re-reads the same c_{t-1});
  * otherwise TM_ERR_STREAM_ORDER; chunk 1 without a reference ->
  * TM_ERR_STREAM_ORDER (cache miss).  k/v may alias the slot returned
- * by tm_kvcache_slot_ptr (zero-copy append). */
+ * by tm_kvcache_slot_ptr (zero-copy append).  With TM_TRANSPORT_PEER, o may be
+ * the rank's O window (tm_peer_output_ptr: no receive copy); the call is then
+ * an attention kernel (which also pushes this rank's shard) plus a receive
+ * kernel, see tm_transport. */
 tm_status tm_chunk_attention(tm_ctx* ctx, int32_t layer, int32_t step, int64_t chunk,
                              const void* q, const void* k, const void* v, void* o,
                              void* stream);
