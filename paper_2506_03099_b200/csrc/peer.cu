@@ -38,13 +38,17 @@ __global__ void __launch_bounds__(kThreads) peer_push_kernel(const __grid_consta
     }
 }
 
-// Thread 0 waits on counters[which] >= epoch for every source, then the CTA proceeds.
+// Warp 0 waits on counters[which] >= epoch for every source -- lane s polls
+// source s, so the P system-scope acquire round trips overlap -- then the CTA
+// proceeds.
 __device__ __forceinline__ void cta_wait_all(PeerCounters* own, int which, uint32_t epoch, int P) {
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < P; ++s) {
+    if (threadIdx.x < 32) {
+        const int s = threadIdx.x;
+        if (s < P) {
             const uint32_t* c = which < 3 ? &own->arr[which][s] : &own->done[s];
-            if (!peer_wait_ge(c, epoch, &own->err)) break;
+            peer_wait_ge(c, epoch, &own->err);
         }
+        __syncwarp();
         __threadfence();
     }
     __syncthreads();
@@ -56,11 +60,24 @@ __global__ void __launch_bounds__(kThreads) peer_recv_o_kernel(PeerCounters* own
                                                                int rank, int W) {
     asm volatile("griddepcontrol.wait;" ::: "memory");   // PDL: after the attention grid
     cta_wait_all(own, 3, epoch, P);
-    const int64_t n = int64_t(B) * Ls * W;
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
-         i += int64_t(gridDim.x) * blockDim.x) {
-        const int64_t t = (i / W) % Ls;
-        o[i] = int64_t(rank) * Ls + t < L ? __ldcg(owin + i) : make_uint4(0, 0, 0, 0);
+    // 16-B words, 4 loads in flight per thread; rows of global token >= L are
+    // shard padding (zero).  32-bit index math (the window is < 2^31 words).
+    const uint32_t n = uint32_t(int64_t(B) * Ls * W);
+    const uint32_t valid_rows = uint32_t(L - int64_t(rank) * Ls);   // per batch element
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t base = blockIdx.x * blockDim.x + threadIdx.x; base < n; base += 4 * stride) {
+        uint4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uint32_t i = base + u * stride;
+            v[u] = make_uint4(0, 0, 0, 0);
+            if (i < n && (i / uint32_t(W)) % uint32_t(Ls) < valid_rows) v[u] = __ldcg(owin + i);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uint32_t i = base + u * stride;
+            if (i < n) o[i] = v[u];
+        }
     }
 }
 
@@ -107,7 +124,8 @@ cudaError_t launch_peer_recv_o(PeerCounters* own, uint32_t epoch, int P, const v
                                int B, int64_t Ls, int64_t L, int rank, int row_bytes,
                                cudaStream_t s, int* launches) {
     if (row_bytes % 16) return cudaErrorInvalidValue;
-    const cudaError_t e = launch_pdl(peer_recv_o_kernel, dim3(sm_count_peer()), dim3(kThreads), 0, s,
+    if (int64_t(B) * Ls * (row_bytes / 16) >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
+    const cudaError_t e = launch_pdl(peer_recv_o_kernel, dim3(4 * sm_count_peer()), dim3(kThreads), 0, s,
                                      own, epoch, P, static_cast<const uint4*>(owin),
                                      static_cast<uint4*>(o), B, Ls, L, rank, row_bytes / 16);
     if (e == cudaSuccess && launches) ++*launches;
