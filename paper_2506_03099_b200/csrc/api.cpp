@@ -644,11 +644,16 @@ tm_status tm_chunk_attention_phases(tm_ctx* ctx, int32_t layer, int32_t step, in
             pa.rank = r;
             pr.peer = &pa;
             ++ctx->e_done;
+            // zero-copy output with RECV in the same call: the kernel's last CTA
+            // waits for every rank's rows itself; no receive kernel follows.
+            if ((phases & TM_PHASE_RECV) && o == ctx->wo(r)) pa.wait_done = ctx->e_done;
             st = cuda_check(launch_fmha_sm100(pr, ctx->scratch(), cs, &ctx->launches),
                             "attention kernel launch (peer)");
             if (st) return st;
         }
-        if ((phases & TM_PHASE_RECV) && o == ctx->wo(r)) {
+        if ((phases & TM_PHASE_RECV) && (phases & TM_PHASE_ATTEND) && o == ctx->wo(r)) {
+            // zero-copy output, waited for inside the attention kernel
+        } else if ((phases & TM_PHASE_RECV) && o == ctx->wo(r)) {
             // zero-copy output (tm_peer_output_ptr): only wait for every rank's rows
             st = cuda_check(launch_peer_wait_done(ctx->ctr(r), ctx->e_done, Ly.P, cs, &ctx->launches),
                             "peer receive (zero-copy)");

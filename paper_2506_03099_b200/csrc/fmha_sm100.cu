@@ -112,6 +112,7 @@ struct __align__(64) FmhaParams {
     // and before tiles of segment wait_seg (K: T=1, V: T=2); fused push of
     // this rank's shard at kernel start; done signal at kernel end.
     int peer, push, signal_done, wait_seg, src_rows, P, rank;
+    uint32_t wait_done;               // nonzero: the last CTA waits for every rank's done (zero-copy O)
     uint32_t epoch[3];
     PeerCounters* own;
     PeerCounters* done_ctr[kMaxPeers];
@@ -942,7 +943,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
     }
     // a6 fused: this rank's O rows are in the owners' windows once every CTA
     // is here; the last CTA bumps done[rank] at each owner.
-    if (p.signal_done) peer_signal(p.done_ctr, p.own, p.P, p.rank, 3);
+    if (p.signal_done) peer_signal(p.done_ctr, p.own, p.P, p.rank, 3, p.wait_done);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -1161,6 +1162,7 @@ cudaError_t launch_fmha_sm100(const AttnProblem& pr, void* scratch, cudaStream_t
         p.push = pa->push;
         p.pp = pa->pp;
         p.signal_done = pa->signal_done;
+        p.wait_done = pa->wait_done;
         for (int r = 0; r < pa->P; ++r) p.done_ctr[r] = pa->done_ctr[r];
         p.P = pa->P;
         p.rank = pa->rank;

@@ -55,6 +55,7 @@ struct PeerAttnArgs {
     int64_t o_rows = 0;               // output row q goes to owner q / o_rows, row q % o_rows
     int o_H = 0, o_h0 = 0;            // heads of a row in the O window; this rank's first head
     bool signal_done = false;         // bump every owner's done[rank] when all CTAs finished
+    uint32_t wait_done = 0;           // nonzero: then wait for every rank's done (zero-copy receive)
     PeerCounters* done_ctr[kMaxPeers] = {};
     int P = 1, rank = 0;
 };

@@ -63,8 +63,11 @@ __device__ __forceinline__ bool peer_wait_ge(const uint32_t* ctr, uint32_t targe
 // Last-CTA signal: every thread of the CTA calls this after its stores; when
 // the grid's last CTA arrives, it bumps slot `slot` of counter array `which`
 // (0..2: arr[T], 3: done) at every peer.
+// `wait_epoch` (done signals only, 0 = none): the grid's last CTA then also
+// waits until every source's done counter reaches it, so the kernel completes
+// only when all ranks' rows have landed here (replaces a receive kernel).
 __device__ __forceinline__ void peer_signal(PeerCounters* const* ctr, PeerCounters* own, int P,
-                                            int rank, int which) {
+                                            int rank, int which, uint32_t wait_epoch = 0) {
     fence_acq_rel_sys();
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -76,6 +79,9 @@ __device__ __forceinline__ void peer_signal(PeerCounters* const* ctr, PeerCounte
                 uint32_t* c = which < 3 ? &ctr[p]->arr[which][rank] : &ctr[p]->done[rank];
                 red_release_sys_add(c, 1u);
             }
+            if (wait_epoch != 0)
+                for (int p = 0; p < P; ++p)
+                    if (!peer_wait_ge(&own->done[p], wait_epoch, &own->err)) break;
         }
     }
 }

@@ -263,7 +263,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _ipc_worker(rank, world, port, H, d, Lr, Lc, outdir, errq):
+def _ipc_worker(rank, world, port, H, d, Lr, Lc, outdir, errq, zero_copy=False):
     try:
         import torch.distributed as dist
         os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -277,11 +277,17 @@ def _ipc_worker(rank, world, port, H, d, Lr, Lc, outdir, errq):
         ca.put_reference(0, 0, shard(kr, Lr, world, rank), shard(vr, Lr, world, rank))
         for t in (1, 2, 3):
             q, k, v = dev[t]
-            o = torch.full_like(shard(q, Lc, world, rank), 7.0)
+            o = ca.output_window()[0] if zero_copy else torch.full_like(shard(q, Lc, world, rank), 7.0)
             ca.attend(0, 0, t, shard(q, Lc, world, rank), shard(k, Lc, world, rank),
                       shard(v, Lc, world, rank), o)
+            if zero_copy:
+                assert ca.launches == 1        # the fused kernel waits for every rank itself
             torch.cuda.synchronize()
-            np.save(os.path.join(outdir, f"o_r{rank}_t{t}.npy"), bits(o))
+            ob = bits(o)
+            if zero_copy:                      # shard padding rows are unspecified there
+                n = min(-(-Lc // world), Lc - rank * (-(-Lc // world)))
+                ob[n:] = 0
+            np.save(os.path.join(outdir, f"o_r{rank}_t{t}.npy"), ob)
         ca.check()
         dist.barrier()
         ca.close()
@@ -291,20 +297,23 @@ def _ipc_worker(rank, world, port, H, d, Lr, Lc, outdir, errq):
         raise
 
 
-@pytest.mark.parametrize("P", [2, 4, 8])
-def test_peer_two_processes_ipc_fused(tmp_path, P):
+@pytest.mark.parametrize("P,zero_copy", [(2, False), (4, False), (8, False), (2, True), (8, True)])
+def test_peer_two_processes_ipc_fused(tmp_path, P, zero_copy):
     """World size 2 (and 4) as processes sharing the device: windows exchanged
     as CUDA IPC handles over torch.distributed (gloo), every call fused (push
     in the attention kernel, epilogue scatter, receive).  Each rank's shard of
     the output equals the direct path's rows bit for bit per head block.  At
     P = 4 and 8 the shards are 250 and 125 rows, so Q and K/V tiles span two
-    source ranks; P = 8 is the node-size group of the multi-GPU benchmark."""
+    source ranks; P = 8 is the node-size group of the multi-GPU benchmark.
+    zero_copy: o is the rank's O window (as bench.py runs it), so the fused
+    kernel's last CTA waits for every rank and no receive kernel follows."""
     import torch.multiprocessing as mp
     H, d, Lr, Lc = 8, 128, 256, 1000
     ctx = mp.get_context("spawn")
     errq = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_ipc_worker, args=(r, P, port, H, d, Lr, Lc, str(tmp_path), errq))
+    procs = [ctx.Process(target=_ipc_worker,
+                         args=(r, P, port, H, d, Lr, Lc, str(tmp_path), errq, zero_copy))
              for r in range(P)]
     for p in procs:
         p.start()
