@@ -22,6 +22,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "comm.h"
 #include "internal.h"
 #include "peer_map.h"
@@ -32,6 +34,13 @@ using namespace tmk;
 namespace {
 
 thread_local std::string g_err;
+
+// NVTX range around each public call (header-only NVTX v3: no cost without a
+// profiler attached; ncu --nvtx / nsys show the tm_* calls on the timeline).
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 tm_status fail(tm_status s, const char* fmt, ...) {
     char buf[512];
@@ -476,6 +485,7 @@ tm_status tm_kvcache_put_reference(tm_ctx* ctx, int32_t layer, int32_t step, con
 
 tm_status tm_kvcache_put_reference_phases(tm_ctx* ctx, int32_t layer, int32_t step, const void* k,
                                           const void* v, uint32_t phases, void* stream) {
+    NvtxRange nvtx_range("tm_kvcache_put_reference_phases");
     if (!ctx || !k || !v) return fail(TM_ERR_INVALID_ARG, "null argument");
     tm_status st = check_layer_step(ctx, layer, step, true);
     if (st) return st;
@@ -567,6 +577,7 @@ tm_status tm_chunk_attention(tm_ctx* ctx, int32_t layer, int32_t step, int64_t c
 tm_status tm_chunk_attention_phases(tm_ctx* ctx, int32_t layer, int32_t step, int64_t chunk,
                                     const void* q, const void* k, const void* v, void* o,
                                     uint32_t phases, void* stream) {
+    NvtxRange nvtx_range("tm_chunk_attention_phases");
     if (!ctx || !q || !k || !v || !o) return fail(TM_ERR_INVALID_ARG, "null argument");
     tm_status st = check_layer_step(ctx, layer, step, false);
     if (st) return st;
@@ -765,6 +776,7 @@ tm_status tm_chunk_attention_phases(tm_ctx* ctx, int32_t layer, int32_t step, in
 
 tm_status tm_reference_attention(tm_ctx* ctx, int32_t layer, int32_t step, const void* q,
                                  const void* k, const void* v, void* o, void* stream) {
+    NvtxRange nvtx_range("tm_reference_attention");
     if (!ctx || !q || !k || !v || !o) return fail(TM_ERR_INVALID_ARG, "null argument");
     if (ctx->lay.exchange || ctx->lay.P > 1 || ctx->lay.peer)
         return fail(TM_ERR_UNSUPPORTED, "tm_reference_attention needs a world_size == 1 direct context");
@@ -820,6 +832,7 @@ tm_status tm_reference_attention(tm_ctx* ctx, int32_t layer, int32_t step, const
 
 tm_status tm_window_attention(tm_ctx* ctx, const void* q, const void* k, const void* v, void* o,
                               const int64_t* chunk_len, int32_t n_chunks, void* stream) {
+    NvtxRange nvtx_range("tm_window_attention");
     if (!ctx || !q || !k || !v || !o || !chunk_len) return fail(TM_ERR_INVALID_ARG, "null argument");
     if (ctx->lay.exchange || ctx->lay.P > 1)
         return fail(TM_ERR_UNSUPPORTED, "tm_window_attention needs a world_size == 1 context");
@@ -881,6 +894,7 @@ tm_status tm_audio_cross_attention(tm_ctx* ctx, const void* q, const void* k_aud
                                    int64_t tokens_per_frame, int64_t audio_tokens_per_frame,
                                    const int32_t* face_ids, int64_t n_face, int32_t window,
                                    void* scratch, size_t scratch_bytes, void* stream) {
+    NvtxRange nvtx_range("tm_audio_cross_attention");
     if (!ctx || !q || !k_audio || !v_audio || !o || !scratch)
         return fail(TM_ERR_INVALID_ARG, "null argument");
     if (ctx->lay.exchange || ctx->lay.P > 1)
@@ -956,6 +970,7 @@ tm_status tm_audio_cross_attention(tm_ctx* ctx, const void* q, const void* k_aud
 
 tm_status tm_flow_euler_step(tm_ctx* ctx, float* x, const void* v, int32_t v_dtype, int64_t n,
                              float dt, void* stream) {
+    NvtxRange nvtx_range("tm_flow_euler_step");
     if (n < 0) return fail(TM_ERR_SHAPE, "n = %lld < 0", (long long)n);
     if (n == 0) return TM_OK;
     if (!x || !v) return fail(TM_ERR_INVALID_ARG, "null argument");
@@ -1043,6 +1058,7 @@ tm_status tm_peer_route_host(int32_t mode, const void* src, void* dst, int32_t b
 tm_status tm_flow_sampler_step(tm_ctx* ctx, float* x, const void* v, int32_t v_dtype, int64_t n,
                                float t_cur, float t_next, const float* eps, uint64_t seed,
                                uint64_t offset, void* x_bf16_out, void* stream) {
+    NvtxRange nvtx_range("tm_flow_sampler_step");
     if (n < 0) return fail(TM_ERR_SHAPE, "n = %lld < 0", (long long)n);
     if (n == 0) return TM_OK;
     if (!x || !v) return fail(TM_ERR_INVALID_ARG, "null argument");
