@@ -258,6 +258,41 @@ def test_zero_copy_append_via_slot_ptr():
         assert (a == b).all()
 
 
+@pytest.mark.parametrize("what", ["prev_k", "ref_v"])
+def test_corrupted_cache_is_detected(what):
+    """Fault injection (SURVEY Sec 5): corrupt one head of the cached c_{t-1}
+    K (or the reference V) between chunks; the next chunk must then miss the
+    oracle by far more than the bf16 alarm -- the parity check sees the cache,
+    it does not just recompute from the inputs."""
+    H, d, Lr, Lc = 4, 128, 128, 384
+    si = syn.StreamInputs(H, d, Lr, Lc, "bf16", "D0", 23)
+    ca = tm.ChunkAttention(H, d, Lr, Lc, 1, 1)
+    so = oracle.StreamOracle()
+    _, kr, vr = si.chunk(0, 0, 0)
+    ca.put_reference(0, 0, to_dev(kr), to_dev(vr))
+    so.put_reference(0, 0, kr.f64, vr.f64)
+    q, k, v = si.chunk(0, 0, 1)
+    o = torch.empty_like(to_dev(q))
+    ca.attend(0, 0, 1, to_dev(q), to_dev(k), to_dev(v), o)
+    assert rel_err(from_dev(o), so.attend(0, 0, 1, q.f64, k.f64, v.f64)) <= BF16_ALARM
+    torch.cuda.synchronize()
+    # overwrite head 1 of the cached tensor with large values
+    if what == "prev_k":
+        ptr, L = ca.slot_ptr(0, 0, 1)[0], Lc
+    else:
+        ptr, L = ca.ref_ptr(0, 0)[1], Lr
+    garbage = torch.full((L, H, d), 8.0, device="cuda", dtype=torch.bfloat16)
+    cur = torch.empty_like(garbage)
+    dev_copy(cur.data_ptr(), ptr, cur.numel() * 2)
+    cur[:, 1] = garbage[:, 1]
+    dev_copy(ptr, cur.data_ptr(), cur.numel() * 2)
+    q, k, v = si.chunk(0, 0, 2)
+    ca.attend(0, 0, 2, to_dev(q), to_dev(k), to_dev(v), o)
+    err = rel_err(from_dev(o), so.attend(0, 0, 2, q.f64, k.f64, v.f64))
+    assert err > 20 * BF16_ALARM, err
+    ca.close()
+
+
 def test_launch_count_and_variant():
     ca = tm.ChunkAttention(2, 128, 128, 128, 1, 1)
     assert ca.variant == "sm100_tcgen05"
