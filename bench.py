@@ -374,6 +374,10 @@ def main():
     ap.add_argument("--stream-chunks", type=int, default=64,
                     help="BJ.configs[3] streaming measurement over this many chunks (0: off)")
     args = ap.parse_args()
+    # Watchdog: a rank stuck in a collective (a hung exchange is the realistic
+    # multi-GPU failure) dumps its stacks and exits instead of holding the box.
+    import faulthandler
+    faulthandler.dump_traceback_later(int(os.environ.get("TM_BENCH_WATCHDOG_S", "1800")), exit=True)
     if args.warmup < 3:
         args.warmup = 3
     c = CONFIGS[args.config]
