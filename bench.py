@@ -554,8 +554,8 @@ def main():
         kev.append((a, b))
     barrier()
     w3 = time.time()
-    if transport == "peer":
-        ca.check()      # raises if any device-side peer wait timed out (results would be garbage)
+    if P > 1 or transport == "peer":
+        ca.check()      # peer: a device-side wait timed out; nccl: the communicator's async error
     clocks.stop()
     clk = nvml.summary() or clocks.summary(window=(w0, w1))
     kclk = clocks.summary(window=(w2, w3))
@@ -667,7 +667,7 @@ def main():
         sb.record(stream)
         barrier()
         s_ms = max_over_ranks(sa.elapsed_time(sb)) / (args.stream_chunks - 1)
-        if transport == "peer":
+        if P > 1 or transport == "peer":
             sc.check()
         streaming = {"config": f"BJ.configs[3] shape: {NLs} layers x {NS} steps per chunk, "
                                f"chunks 2..{args.stream_chunks} timed (steady state, t>=2)",

@@ -259,9 +259,11 @@ tm_status tm_peer_connect_local(tm_ctx* const* ctxs, int32_t n);
  * unspecified (the copying RECV writes zeros there). */
 tm_status tm_peer_output_ptr(tm_ctx* ctx, void** o);
 
-/* Synchronises the device and reports whether a device-side peer wait timed
- * out (10 s without the expected peer signal) since the last check:
- * TM_ERR_CUDA with a message, else TM_OK.  Clears the flag. */
+/* Health check of a multi-rank context.  NCCL transport: the communicator's
+ * asynchronous error state (ncclCommGetAsyncError -> TM_ERR_NCCL).  Peer
+ * transport: synchronises the device and reports whether a device-side peer
+ * wait timed out (10 s without the expected peer signal) since the last
+ * check: TM_ERR_CUDA with a message, else TM_OK; clears the flag. */
 tm_status tm_peer_check(tm_ctx* ctx);
 
 /* Device pointers of the cache slot that chunk `chunk` at (layer, step) is

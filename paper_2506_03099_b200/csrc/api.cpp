@@ -1148,6 +1148,10 @@ tm_status tm_peer_output_ptr(tm_ctx* ctx, void** o) {
 
 tm_status tm_peer_check(tm_ctx* ctx) {
     if (!ctx) return fail(TM_ERR_INVALID_ARG, "null ctx");
+    if (ctx->comm) {                       // NCCL transport: the communicator's async state
+        const char* e = comm_async_error(ctx->comm);
+        if (e) return fail(TM_ERR_NCCL, "NCCL asynchronous error: %s", e);
+    }
     if (!ctx->lay.peer) return TM_OK;
     tm_status st = cuda_check(cudaDeviceSynchronize(), "synchronize");
     if (st) return st;

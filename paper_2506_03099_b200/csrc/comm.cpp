@@ -88,6 +88,15 @@ void comm_destroy(void* comm) {
     if (n && comm && n->CommDestroy) n->CommDestroy(comm);
 }
 
+const char* comm_async_error(void* comm) {
+    Nccl* n = nccl();
+    if (!n || !comm || !n->CommGetAsyncError) return nullptr;
+    ncclResult_t st = 0;
+    const ncclResult_t r = n->CommGetAsyncError(comm, &st);
+    if (r) return err(r);
+    return st ? err(st) : nullptr;
+}
+
 // Block p of `send` (count_bytes bytes) goes to rank p; block q of `recv`
 // comes from rank q.  ncclAlltoAll when the library has it, else grouped
 // send/recv (same semantics, nccl.h:460 / :507 / :526).
