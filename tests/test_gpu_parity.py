@@ -405,6 +405,7 @@ def test_forced_ulysses_path_matches_direct(dtype, monkeypatch):
             res.append(o.view(torch.int16 if dtype == "bf16" else torch.int32).cpu().numpy())
         if forced:
             assert ca.launches >= 5          # pack x3, attention, pack, unpack (+ unpacks)
+            ca.check()                       # the communicator reports no async error
         outs.append(res)
         ca.close()
     for a, b in zip(*outs):
