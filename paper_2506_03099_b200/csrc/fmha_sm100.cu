@@ -106,6 +106,8 @@ struct __align__(64) FmhaParams {
     // Output rows (a6 scatter): query row q is stored to o_dst[q / o_rows], row
     // q % o_rows, heads [o_h0, o_h0 + H) of o_H; P = 1: o_dst[0] = o, o_rows = Lq.
     uint16_t* o_dst[kMaxPeers];       // bf16 bits [B][o_rows][o_H][d] each
+    CUtensorMap to;                   // o as a TMA store map (box 32 rows x 64), one owner only
+    int tma_epi;                      // 1: epilogue rows leave through TMA stores of the staging
     int64_t o_bstride;                // rows between batch elements of an o_dst
     int o_rows, o_H, o_h0;
     // Peer transport: waits on the own counters before Q tiles (T=0)
@@ -260,6 +262,37 @@ __device__ __forceinline__ uint16_t* out_row(const FmhaParams& p, int b, int q, 
 template <int D>
 __device__ __forceinline__ void store_rows_bf16(const FmhaParams& p, uint32_t tsrc, float scale,
                                                 uint8_t* stg, int b, int q0, int h, int lane) {
+    if (p.tma_epi) {
+        // One owner: the swizzled staging tile is exactly a 128B-swizzled TMA box
+        // (32 rows x 64 columns), so lane 0 stores it asynchronously (rows past
+        // Lq clipped) and the warp moves on; the buffer is reused only after the
+        // previous store has read it.
+#pragma unroll 1
+        for (int half = 0; half < D / 64; ++half) {
+            uint32_t o[64];
+            tmem_ld32(tsrc + half * 64, o);
+            tmem_ld32(tsrc + half * 64 + 32, o + 32);
+            tmem_wait_ld();
+            if (lane == 0) tma_store_wait_read();
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                uint4 v;
+                v.x = pack_bf16x2(__uint_as_float(o[8 * j]) * scale, __uint_as_float(o[8 * j + 1]) * scale);
+                v.y = pack_bf16x2(__uint_as_float(o[8 * j + 2]) * scale, __uint_as_float(o[8 * j + 3]) * scale);
+                v.z = pack_bf16x2(__uint_as_float(o[8 * j + 4]) * scale, __uint_as_float(o[8 * j + 5]) * scale);
+                v.w = pack_bf16x2(__uint_as_float(o[8 * j + 6]) * scale, __uint_as_float(o[8 * j + 7]) * scale);
+                *reinterpret_cast<uint4*>(stg + lane * 128 + ((j ^ (lane & 7)) << 4)) = v;
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+                tma_store_4d(&p.to, stg, half * 64, h, q0, b);
+                tma_store_commit();
+            }
+        }
+        return;
+    }
     // This lane stores rows t*4 + lane/8 (t < 8), 16 B at column chunk lane%8:
     // destinations computed once for both halves (32-bit index math).
     uint16_t* dsts[8];
@@ -835,6 +868,10 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                 // (deterministic) and store the output.  No partial of its own.
                 constexpr int kPieceFloats = 256 * D + 512;
                 if (threadIdx.x == 0) trace_span(p, 4);
+                // the merge copies over the ring and the staging: every earlier
+                // epilogue TMA store must have read its staging buffer first
+                if (lane == 0) tma_store_wait_read();
+                __syncwarp();
                 if (threadIdx.x == 0) {
                     volatile int* ctr = p.counters + it.cfirst;
                     const long long t0 = clock64();
@@ -924,6 +961,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                 mbar_arrive(&o_empty[i]);
             }
         }
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");   // epilogue stores done
 #ifdef TM_SPANS_MERGE
         if (threadIdx.x == 0) trace_span(p, 4);   // (spans A/B) softmax loop left, before the final barrier
 #endif
@@ -962,13 +1000,14 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 // Token-major bf16 [B][L][H][d]: dims (inner first) {d, H, L, B}; box {64, 1, 128, 1}.
 // `bstride` = tokens between batch elements (>= L; a sub-range of a longer sequence).
-bool make_map(CUtensorMap* m, const void* base, int d, int H, int64_t L, int B, int64_t bstride = 0) {
+bool make_map(CUtensorMap* m, const void* base, int d, int H, int64_t L, int B, int64_t bstride = 0,
+              int box_rows = 128) {
     if (bstride <= 0) bstride = L;
     auto fn = encode_fn();
     if (!fn) return false;
     cuuint64_t dims[4] = {cuuint64_t(d), cuuint64_t(H), cuuint64_t(L), cuuint64_t(B)};
     cuuint64_t strides[3] = {cuuint64_t(d) * 2, cuuint64_t(H) * d * 2, cuuint64_t(bstride) * H * d * 2};
-    cuuint32_t box[4] = {64, 1, 128, 1};
+    cuuint32_t box[4] = {64, 1, cuuint32_t(box_rows), 1};
     cuuint32_t es[4] = {1, 1, 1, 1};
     CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides,
                     box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -1143,6 +1182,13 @@ cudaError_t launch_fmha_sm100(const AttnProblem& pr, void* scratch, cudaStream_t
     p.scale_log2 = pr.scale * 1.4426950408889634f;
     p.o_dst[0] = static_cast<uint16_t*>(pr.o);
     p.o_bstride = pr.q_bstride > 0 ? pr.q_bstride : pr.Lq;
+    static const bool tma_epi_env = [] {
+        const char* e = getenv("TM_TMA_EPI");
+        return !(e && strcmp(e, "0") == 0);
+    }();
+    p.tma_epi = 0;
+    if (tma_epi_env && !pr.peer && make_map(&p.to, pr.o, pr.d, pr.H, pr.Lq, pr.B, p.o_bstride, 32))
+        p.tma_epi = 1;
     p.o_rows = int(pr.Lq);
     p.o_H = pr.H;
     p.o_h0 = 0;
