@@ -329,6 +329,13 @@ tm_status tm_peer_route_host(int32_t mode, const void* src, void* dst, int32_t b
                              int32_t heads_per_rank, int32_t world_size, int32_t rank,
                              int32_t head_dim, int32_t elem_bytes);
 
+/* Host reference of the attention kernel's tail schedule (stream-K; DESIGN
+ * Sec 6), for tests without a GPU: the KV tiles of `units` tail units of
+ * `tiles_per_unit` tiles each, flattened, are cut into G <= ctas contiguous
+ * ranges [bounds[c], bounds[c+1]) (bounds: >= ctas + 1 ints).  Returns G, or
+ * -1 on invalid arguments (ctas <= 160). */
+int32_t tm_schedule_tail_host(int32_t units, int32_t tiles_per_unit, int32_t ctas, int32_t* bounds);
+
 /* Introspection for tests / bench: number of device kernels the last call
  * on this ctx launched (the TM_DEBUG finiteness check not counted), and the
  * attention kernel variant name ("sm100_tcgen05" or "fp32_simt"). */

@@ -1011,6 +1011,15 @@ tm_status tm_ulysses_shuffle_host(int32_t mode, const void* src, void* dst, int3
     return TM_OK;
 }
 
+int32_t tm_schedule_tail_host(int32_t units, int32_t tiles_per_unit, int32_t ctas, int32_t* bounds) {
+    if (units <= 0 || tiles_per_unit <= 0 || ctas <= 0 || ctas > kMaxPersistentCtas || !bounds ||
+        int64_t(units) * tiles_per_unit >= (int64_t(1) << 30)) {
+        fail(TM_ERR_INVALID_ARG, "invalid schedule query");
+        return -1;
+    }
+    return tail_bounds(units, tiles_per_unit, ctas, 4, bounds);
+}
+
 tm_status tm_peer_route_host(int32_t mode, const void* src, void* dst, int32_t batch,
                              int64_t shard_tokens, int64_t tokens, int64_t window_tokens,
                              int32_t heads_per_rank, int32_t world_size, int32_t rank,

@@ -1101,11 +1101,13 @@ int tail_bounds(int T, int n, int C, int min_piece, int* bound) {
         for (int c = 0; c <= G; ++c) bound[c] = int((long long)c * W / G);
         return G;
     }
-    auto fill = [&](float B, int* out) -> int {   // ranges used, or C+1 if more are needed
+    // At most G ranges: never more than W / min_piece (short problems would
+    // otherwise be cut into 1-tile pieces whose merges cost more than the work).
+    auto fill = [&](float B, int* out) -> int {   // ranges used, or G+1 if more are needed
         int x = 0, g = 0;
         if (out) out[0] = 0;
         while (x < W) {
-            if (g == C) return C + 1;
+            if (g == G) return G + 1;
             const int start = x;
             float cost = 0.f;
             while (x < W) {
@@ -1128,11 +1130,11 @@ int tail_bounds(int T, int n, int C, int min_piece, int* bound) {
         }
         return g;
     };
-    float lo = float(W) / C, hi = float(W) / C + item_cost * 4 + n;
-    while (fill(hi, nullptr) > C) hi *= 2;
+    float lo = float(W) / G, hi = float(W) / G + item_cost * 4 + n;
+    while (fill(hi, nullptr) > G) hi *= 2;
     for (int it = 0; it < 40; ++it) {
         const float mid = 0.5f * (lo + hi);
-        if (fill(mid, nullptr) <= C) hi = mid;
+        if (fill(mid, nullptr) <= G) hi = mid;
         else lo = mid;
     }
     return fill(hi, bound);

@@ -113,6 +113,9 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
 // `scratch` (fmha_sm100_scratch_bytes(d) bytes, zero-initialised once) holds
 // the split-KV partials and merge counters; counters return to zero.
 size_t fmha_sm100_scratch_bytes(int d);
+// Host: the stream-K tail ranges of the attention schedule (fmha_sm100.cu):
+// T tail units of n KV tiles each over at most C CTAs; writes G+1 bounds, returns G.
+int tail_bounds(int T, int n, int C, int min_piece, int* bound);
 // `trace` (debug, may be null): 4 x 4096 uint64 clock64 timeline of CTA 0.
 cudaError_t launch_fmha_sm100(const AttnProblem& p, void* scratch, cudaStream_t s, int* launches,
                               unsigned long long* trace = nullptr);

@@ -73,6 +73,7 @@ def _load():
         "tm_peer_connect_local": ([P(V), i32], i32),
         "tm_peer_check": ([V], i32),
         "tm_peer_output_ptr": ([V, P(V)], i32),
+        "tm_schedule_tail_host": ([i32, i32, i32, P(i32)], i32),
         "tm_peer_route_host": ([i32, V, V, i32, i64, i64, i64, i32, i32, i32, i32, i32], i32),
         "tm_kvcache_slot_ptr": ([V, i32, i32, i64, P(V), P(V)], i32),
         "tm_kvcache_ref_ptr": ([V, i32, i32, P(V), P(V)], i32),
@@ -104,6 +105,7 @@ EXPORTED = ("tm_version", "tm_last_error", "tm_kvcache_bytes", "tm_workspace_byt
             "tm_audio_cross_attention", "tm_chunk_attention_phases",
             "tm_kvcache_put_reference_phases", "tm_peer_export", "tm_peer_connect",
             "tm_peer_connect_local", "tm_peer_check", "tm_peer_route_host", "tm_peer_output_ptr",
+            "tm_schedule_tail_host",
             "tm_last_launch_count",
             "tm_kernel_variant")
 
@@ -271,6 +273,15 @@ def tm_peer_route_host(mode, src, dst, batch, shard_tokens, tokens, window_token
     _check(lib.tm_peer_route_host(mode, src.ctypes.data, dst.ctypes.data, batch, shard_tokens,
                                   tokens, window_tokens, heads_per_rank, world_size, rank,
                                   head_dim, elem_bytes))
+
+
+def tm_schedule_tail_host(units, tiles_per_unit, ctas):
+    """The stream-K tail ranges (list of G+1 bounds) the kernel would use."""
+    buf = (ctypes.c_int32 * (ctas + 1))()
+    g = lib.tm_schedule_tail_host(units, tiles_per_unit, ctas, buf)
+    if g < 0:
+        raise TMError(1, lib.tm_last_error().decode())
+    return list(buf[:g + 1])
 
 
 def tm_last_launch_count(ctx) -> int:
