@@ -563,6 +563,24 @@ def main():
     k_ms = max_over_ranks(statistics.mean(k_list))
     k_med = max_over_ranks(statistics.median(k_list))
 
+    # ---------------------------------------------------------------- chunk t = 1
+    # The first chunk of a stream attends {c_0, c_1} only (Lk = Lr + Lc): a new
+    # stream on the same context (tm_stream_reset), every layer's chunk 1 timed.
+    ca.reset()
+    for layer in range(NL):
+        ca.put_reference(layer, 0, kref, vref, stream)
+    ev1 = []
+    barrier()
+    for layer in range(NL):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        q, k, v = sets[layer % NB]
+        a.record(stream)
+        ca.attend(layer, 0, 1, q, k, v, outs[layer % NB], stream)
+        b.record(stream)
+        ev1.append((a, b))
+    barrier()
+    t1_ms = max_over_ranks(statistics.median(a.elapsed_time(b) for a, b in ev1))
+
     # ---------------------------------------------------------------- end to end, host buffers
     e2e = None
     if not args.no_e2e:
@@ -716,6 +734,10 @@ def main():
                        "l2": "inputs larger than L2 (8 layer caches x 4 input sets rotated)"},
             "ms_per_chunk_attention": k_ms,
             "ms_per_chunk_attention_median": k_med,
+            "chunk1": {"ms": t1_ms, "keys_attended": Lr + Lc,
+                       "tflops_per_gpu": flop_per_call(c, t=1) / P / (t1_ms * 1e-3) / 1e12,
+                       "note": "first chunk of a stream (Lk = Lr + Lc), fused append, median of "
+                               f"{NL} calls"},
             "kernel_clocks": kclk,
             "frac_of_bf16_peak": achieved / peak,
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak,
