@@ -427,8 +427,8 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
     uint64_t* s_free = o_done + 2;           // [1]  S buffer loaded into registers
     uint64_t* store_done = s_free + 1;       // [kStages] append-store finished reading a slot
     uint64_t* store_idle = store_done + kStages;   // [1] append warp done (one phase per launch)
-    uint64_t* merge_bar = store_idle + 1;          // [1] a piece's partial landed in smem (merge)
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(merge_bar + 1);
+    uint64_t* merge_bar = store_idle + 1;          // [3] a half partial landed in merge buffer j
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(merge_bar + 3);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -452,7 +452,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
             mbar_init(&store_done[s], 1);
         }
         mbar_init(store_idle, 1);
-        mbar_init(merge_bar, 1);
+        for (int j = 0; j < 3; ++j) mbar_init(&merge_bar[j], 1);
         fence_mbar_init();
     }
     if (warp == 8 && lane == 0) {
@@ -868,10 +868,6 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                 // (deterministic) and store the output.  No partial of its own.
                 constexpr int kPieceFloats = 256 * D + 512;
                 if (threadIdx.x == 0) trace_span(p, 4);
-                // the merge copies over the ring and the staging: every earlier
-                // epilogue TMA store must have read its staging buffer first
-                if (lane == 0) tma_store_wait_read();
-                __syncwarp();
                 if (threadIdx.x == 0) {
                     volatile int* ctr = p.counters + it.cfirst;
                     const long long t0 = clock64();
@@ -885,77 +881,93 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                 auto piece_base = [&](int k) {
                     return p.part + size_t(it.cfirst + k) * kPieceFloats;
                 };
-                // This is the CTA's last item: no more K/V loads, and once store_idle
-                // has completed no append store reads the ring.  The pieces' partials
-                // (O 128 KB, then m and l) are pulled one at a time into the K/V ring
-                // by a bulk copy; each thread reads its row from shared memory
-                // (conflict-free [d/4][256] float4 layout) and accumulates into O_i in
-                // TMEM.  The weights need every piece's m and l first: loaded from
-                // global, up to 8 pieces per batch of independent loads.
-                constexpr uint32_t kPieceBytes = kPieceFloats * 4;
-                static_assert(kPieceBytes <= kStages * kTileBytes + kEpiBytes,
-                              "a partial fits the ring + staging");
+                // This is the CTA's last item: no more Q or K/V loads, and once
+                // store_idle has completed no append store reads the ring.  The
+                // pieces' O partials are pulled in column halves (chunk j = piece
+                // 1 + j/2, half j%2) by bulk copies into three buffers over the Q
+                // tiles and the ring, three chunks in flight; each thread reads its
+                // row from shared memory (conflict-free [d/4][256] float4 layout)
+                // and accumulates into O_i in TMEM.  The weights need every piece's
+                // m and l first: loaded from global, up to 8 pieces per batch of
+                // independent loads, overlapping the first copies.
+                constexpr uint32_t kChunkBytes = 256 * (D / 2) * 4;
+                static_assert(3 * kChunkBytes <= (2 + kStages) * kTileBytes,
+                              "three merge buffers fit the Q tiles + the ring");
                 const int np = it.npieces;
+                const int nchunks = 2 * (np - 1);
+                auto issue_chunk = [&](int j) {
+                    mbar_arrive_expect_tx(&merge_bar[j % 3], kChunkBytes);
+                    bulk_g2s(smem + (j % 3) * kChunkBytes, piece_base(1 + j / 2) + (j & 1) * 128 * D,
+                             kChunkBytes, &merge_bar[j % 3]);
+                };
                 if (threadIdx.x == 0) {
                     mbar_wait(store_idle, 0);
                     fence_proxy_async_global();
-                    mbar_arrive_expect_tx(merge_bar, kPieceBytes);
-                    bulk_g2s(sKV, piece_base(1), kPieceBytes, merge_bar);
+                    for (int j = 0; j < 3 && j < nchunks; ++j) issue_chunk(j);
+                }
+                float mm[8], ll[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    const bool in = 1 + e < np;
+                    mm[e] = in ? __ldcg(piece_base(1 + e) + 256 * D + row_in_pair) : -INFINITY;
+                    ll[e] = in ? __ldcg(piece_base(1 + e) + 256 * D + 256 + row_in_pair) : 0.f;
                 }
                 float mstar = m_run;
-                for (int k0 = 1; k0 < np; k0 += 8) {
-                    float mm[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) mstar = fmaxf(mstar, mm[e]);
+                for (int k0 = 9; k0 < np; k0 += 8) {        // more than 9 pieces (long units)
 #pragma unroll
                     for (int e = 0; e < 8; ++e)
-                        mm[e] = k0 + e < np ? __ldcg(piece_base(k0 + e) + 256 * D + row_in_pair) : -INFINITY;
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) mstar = fmaxf(mstar, mm[e]);
+                        if (k0 + e < np) mstar = fmaxf(mstar, __ldcg(piece_base(k0 + e) + 256 * D + row_in_pair));
                 }
                 const float w0 = ex2(m_run - mstar);
                 float wsum = w0 * l;
-                for (int k0 = 1; k0 < np; k0 += 8) {
-                    float mm[8], ll[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) wsum += ex2(mm[e] - mstar) * ll[e];
+                for (int k0 = 9; k0 < np; k0 += 8) {
 #pragma unroll
                     for (int e = 0; e < 8; ++e) {
                         const bool in = k0 + e < np;
-                        mm[e] = in ? __ldcg(piece_base(k0 + e) + 256 * D + row_in_pair) : -INFINITY;
-                        ll[e] = in ? __ldcg(piece_base(k0 + e) + 256 * D + 256 + row_in_pair) : 0.f;
+                        const float m2 = in ? __ldcg(piece_base(k0 + e) + 256 * D + row_in_pair) : -INFINITY;
+                        const float l2 = in ? __ldcg(piece_base(k0 + e) + 256 * D + 256 + row_in_pair) : 0.f;
+                        wsum += ex2(m2 - mstar) * l2;
                     }
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) wsum += ex2(mm[e] - mstar) * ll[e];
                 }
                 const float inv = 1.f / wsum;
-                const float* sml = reinterpret_cast<const float*>(sKV) + 256 * D;
-                const float4* sp = reinterpret_cast<const float4*>(sKV);
+                float m_cur = mm[0];
                 for (int k = 1; k < np; ++k) {
-                    if (k > 1) {
-                        softmax_bar();              // everyone done with the previous piece
-                        if (threadIdx.x == 0) {
-                            mbar_arrive_expect_tx(merge_bar, kPieceBytes);
-                            bulk_g2s(sKV, piece_base(k), kPieceBytes, merge_bar);
-                        }
-                    }
-                    mbar_wait(merge_bar, (k - 1) & 1);
-                    const float wk = ex2(sml[row_in_pair] - mstar);
+                    // piece k+1's m, consumed one piece later (latency hidden)
+                    const float m_nxt = k + 1 < np ? __ldcg(piece_base(k + 1) + 256 * D + row_in_pair) : 0.f;
+                    const float wk = ex2(m_cur - mstar);
                     const float wo = k == 1 ? w0 : 1.f;
 #pragma unroll 1
-                    for (int c = 0; c < D; c += 32) {
-                        uint32_t o[32];
-                        tmem_ld32(tOi + c, o);
-                        tmem_wait_ld();
+                    for (int h = 0; h < 2; ++h) {
+                        const int j = 2 * (k - 1) + h;
+                        mbar_wait(&merge_bar[j % 3], (j / 3) & 1);
+                        const float4* sp = reinterpret_cast<const float4*>(smem + (j % 3) * kChunkBytes);
+#pragma unroll 1
+                        for (int c = 0; c < D / 2; c += 32) {
+                            uint32_t o[32];
+                            tmem_ld32(tOi + h * (D / 2) + c, o);
+                            tmem_wait_ld();
 #pragma unroll
-                        for (int e = 0; e < 8; ++e) {
-                            const float4 x = sp[((c >> 2) + e) * 256 + row_in_pair];
-                            o[4 * e] = __float_as_uint(__uint_as_float(o[4 * e]) * wo + wk * x.x);
-                            o[4 * e + 1] = __float_as_uint(__uint_as_float(o[4 * e + 1]) * wo + wk * x.y);
-                            o[4 * e + 2] = __float_as_uint(__uint_as_float(o[4 * e + 2]) * wo + wk * x.z);
-                            o[4 * e + 3] = __float_as_uint(__uint_as_float(o[4 * e + 3]) * wo + wk * x.w);
+                            for (int e = 0; e < 8; ++e) {
+                                const float4 x = sp[((c >> 2) + e) * 256 + row_in_pair];
+                                o[4 * e] = __float_as_uint(__uint_as_float(o[4 * e]) * wo + wk * x.x);
+                                o[4 * e + 1] = __float_as_uint(__uint_as_float(o[4 * e + 1]) * wo + wk * x.y);
+                                o[4 * e + 2] = __float_as_uint(__uint_as_float(o[4 * e + 2]) * wo + wk * x.z);
+                                o[4 * e + 3] = __float_as_uint(__uint_as_float(o[4 * e + 3]) * wo + wk * x.w);
+                            }
+                            tmem_st32(tOi + h * (D / 2) + c, o);
                         }
-                        tmem_st32(tOi + c, o);
+                        if (j + 3 < nchunks) {
+                            softmax_bar();          // everyone done with buffer j % 3
+                            if (threadIdx.x == 0) issue_chunk(j + 3);
+                        }
                     }
-                    tmem_wait_st();
+                    m_cur = m_nxt;
                 }
-                softmax_bar();                      // the last piece's smem is read: staging free
+                tmem_wait_st();
                 store_rows_bf16<D>(p, tOi, inv, sEpi + warp * 4096, it.b, q - lane, it.h, lane);
                 tc_fence_before();
                 mbar_arrive(&o_empty[i]);

@@ -80,6 +80,14 @@ def test_few_units_long_kv_many_pieces(dtype, H, Lr, Lc):
     assert err <= (FP32_TOL if dtype == "fp32" else BF16_ALARM), err
 
 
+@pytest.mark.parametrize("Lr,Lc", [(7000, 200), (1024, 512)])
+def test_many_pieces_d64_bf16(Lr, Lc):
+    """d = 64 merges: the partials' column halves are 32 KB, three in flight
+    over the Q tiles and the ring (13 partials at Lr=7000, 3 at Lr=1024)."""
+    err = run_stream(1, 64, Lr, Lc, "bf16", chunks=2)
+    assert err <= BF16_ALARM, err
+
+
 @pytest.mark.parametrize("dist", ["D1", "D2", "D3", "D6"])
 def test_distributions_bf16(dist):
     err = run_stream(4, 128, 256, 640, "bf16", dist=dist, chunks=3)

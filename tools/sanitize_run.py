@@ -37,6 +37,10 @@ stream(2, 64, 17, 130, tm.TM_BF16)
 stream(2, 128, 200, 300, tm.TM_BF16, zero_copy=True)
 stream(2, 128, 130, 70, tm.TM_FP32)
 stream(2, 128, 200, 300, tm.TM_BF16, transport=tm.TM_TRANSPORT_PEER)
+# stream-K merges: 3 partials (six column-half copies through three buffers), 16 partials
+stream(1, 128, 1024, 512, tm.TM_BF16)
+stream(1, 64, 1024, 512, tm.TM_BF16)
+stream(1, 128, 8192, 256, tm.TM_BF16)
 # f1 window, f4 audio, a7 Euler, f2 sampler
 H, d = 2, 128
 ca = tm.ChunkAttention(H, d, 16, 16, 1, 1)
