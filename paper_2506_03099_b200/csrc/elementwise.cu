@@ -148,11 +148,21 @@ __global__ void __launch_bounds__(256) sampler_kernel(float* __restrict__ x,
                 const float k32 = 2.3283064365386963e-10f;      // 2^-32
                 const float u0 = fmaf(float(w.x), k32, 0.5f * k32), u1 = fmaf(float(w.y), k32, 0.5f * k32);
                 const float u2 = fmaf(float(w.z), k32, 0.5f * k32), u3 = fmaf(float(w.w), k32, 0.5f * k32);
-                const float r0 = sqrtf(-2.f * logf(u0)), r1 = sqrtf(-2.f * logf(u2));
+                // r = sqrt(-2 ln u) as t * rsqrt(t) (MUFU, rel. error ~2^-23).  u
+                // rounds to exactly 1 for the top 128 words (t = 0, r = 0): the
+                // clamp keeps 0 * rsqrt(0) from being NaN.  ln stays the accurate
+                // logf: near u = 1 an absolute log error is amplified by 1/r.
+                // The angle 2 pi u is taken as pi (2u - 1) + pi, inside MUFU
+                // sin/cos's accurate range [-pi, pi] (abs. error ~2^-21), so
+                // sin and cos flip sign.
+                const float t0 = -2.f * logf(u0), t2 = -2.f * logf(u2);
+                const float r0 = t0 * rsqrtf(fmaxf(t0, 1e-30f)), r1 = t2 * rsqrtf(fmaxf(t2, 1e-30f));
+                const float a1 = 3.14159265358979f * fmaf(2.f, u1, -1.f);
+                const float a3 = 3.14159265358979f * fmaf(2.f, u3, -1.f);
                 float s0, c0, s1, c1;
-                sincospif(2.f * u1, &s0, &c0);
-                sincospif(2.f * u3, &s1, &c1);
-                e[0] = r0 * c0; e[1] = r0 * s0; e[2] = r1 * c1; e[3] = r1 * s1;
+                __sincosf(a1, &s0, &c0);
+                __sincosf(a3, &s1, &c1);
+                e[0] = -r0 * c0; e[1] = -r0 * s0; e[2] = -r1 * c1; e[3] = -r1 * s1;
             }
         }
         const int64_t i0 = 4 * gi;
