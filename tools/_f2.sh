@@ -1,6 +1,6 @@
 timeout 300 python -m pytest tests -m gpu -q -x -k "sampler" > gpurun_out/g22.log 2>&1
-for rep in 1 2 3; do for v in old g16 new g12 g24; do
-  unset TM_SAMPLER_GRID; L=paper_2506_03099_b200/libtm.so; case $v in old) L=paper_2506_03099_b200/libtm_old.so;; g16) export TM_SAMPLER_GRID=16;; g12) export TM_SAMPLER_GRID=12;; g24) export TM_SAMPLER_GRID=24;; esac
+for rep in 1 2 3; do for v in old a new; do
+  L=paper_2506_03099_b200/libtm.so; case $v in old) L=paper_2506_03099_b200/libtm_old.so;; a) L=paper_2506_03099_b200/libtm_a.so;; esac
   TM_LIB_PATH=$L python - <<'PY'
 import os, sys, torch, statistics
 sys.path.insert(0, '.')
