@@ -2,6 +2,8 @@
 same seeded inputs.  Tolerances (BJ.north_star): bf16 max|err| <= 2e-2 *
 max|O| (internal alarm 8e-3), fp32 validation mode <= 1e-4, Euler fp32
 <= 1e-6 * max|x|."""
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -574,6 +576,31 @@ def test_sampler_in_kernel_philox_matches_oracle_generator():
     with pytest.raises(tm.TMError):
         tm.tm_flow_sampler_step(None, xd, vd, tm.TM_FP32, n, 0.5, 0.5)     # t_next must exceed t
 
+
+
+def test_sampler_uniform_rounding_to_one_is_finite():
+    """f2 edge: Philox words in the top 128 values make the kernel's fp32
+    uniform exactly 1 (ln u = 0, radius 0); the draw must stay finite.  The
+    fp64 oracle keeps u < 1, radius sqrt(-2 ln u) <= 2.44e-4 there, which
+    bounds the difference.  Counters from tests/golden/sampler_u_one.json
+    (written by tests/golden/make_sampler_u_one.py from the oracle's Philox)."""
+    import json
+    with open(os.path.join(os.path.dirname(__file__), "golden", "sampler_u_one.json")) as f:
+        g = json.load(f)
+    assert {h["word"] for h in g["hits"]} == {0, 2}
+    for h in g["hits"]:
+        xd = torch.zeros(4, device="cuda")
+        vd = torch.zeros(4, device="cuda")
+        tm.tm_flow_sampler_step(None, xd, vd, tm.TM_FP32, 4, 0.0, 0.5, seed=g["seed"], offset=h["offset"])
+        torch.cuda.synchronize()
+        z = 2.0 * xd.double().cpu().numpy()
+        assert np.isfinite(z).all(), z
+        ref = oracle.philox_normal(4, g["seed"], h["offset"])
+        pair = slice(h["word"], h["word"] + 2)         # the two draws sharing that radius
+        assert np.abs(z[pair]).max() < 2.5e-4, z
+        assert np.abs(z[pair] - ref[pair]).max() < 2.5e-4
+        other = slice(2 - h["word"], 4 - h["word"])
+        assert np.abs(z[other] - ref[other]).max() < 2e-4
 
 # ------------------------------------------------------------------ SURVEY Sec 8(f) f4: audio cross-attention
 

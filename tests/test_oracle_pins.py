@@ -403,3 +403,17 @@ def test_audio_empty_face_mask_is_error():
     q, k, v = _audio_inputs()
     with pytest.raises(oracle.OracleError):
         oracle.audio_cross_attention(q, k, v, [])
+
+
+def test_sampler_u_one_fixture_matches_oracle_philox():
+    """tests/golden/sampler_u_one.json (GPU edge test of f2): each stored
+    counter's word is the oracle Philox output and lies in the top 128 values."""
+    import json
+    import os
+    with open(os.path.join(os.path.dirname(__file__), "golden", "sampler_u_one.json")) as f:
+        g = json.load(f)
+    for h in g["hits"]:
+        ctr = np.array([[0, 0, h["offset"] & 0xFFFFFFFF, h["offset"] >> 32]], dtype=np.uint32)
+        key = np.array([[g["seed"] & 0xFFFFFFFF, g["seed"] >> 32]], dtype=np.uint32)
+        w = int(oracle.philox4x32_10(ctr, key)[0, h["word"]])
+        assert w == h["w"] and w >= 2**32 - 128
