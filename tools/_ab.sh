@@ -1,7 +1,6 @@
-timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/g17.log 2>&1
-for rep in 1 2; do for H in 40 20 10 5; do for v in old new; do
-  if [ $v = old ]; then L=paper_2506_03099_b200/libtm_old.so; else L=paper_2506_03099_b200/libtm.so; fi
-  echo "$v $(TM_LIB_PATH=$L SWEEP_H=$H timeout 120 python tools/sweep.py 2>&1 | tail -1)"
-done; done; done > gpurun_out/ab17.txt 2>&1
-for H in 40 5; do SWEEP_H=$H timeout 200 python tools/cta_spans.py > gpurun_out/spans17_H$H.txt 2>&1; cp gpurun_out/spans_512_$H.json gpurun_out/spans17_512_$H.json; done
-python -m paper_2506_03099_b200.build > /dev/null 2>&1
+# bench step A/B of the tail schedule: TM_SCHED_LEAD=0 (previous) vs 1 (default), interleaved
+for rep in 1 2 3; do for v in 0 1; do
+  TM_SCHED_LEAD=$v python bench.py --no-extras --no-cpu-baseline --no-e2e --stream-chunks 0 2>/dev/null | python -c "
+import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); r=d['roofline']
+print('lead=$v', round(d['value'],1), 'live', round(r['achieved'],1), 'alone', round(r['achieved_kernel_alone'],1), 'chunk1', round(d['chunk1']['tflops_per_gpu'],1), d['clocks']['sm_mhz'])"
+done; done > gpurun_out/ab26.txt 2>&1

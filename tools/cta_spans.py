@@ -41,9 +41,12 @@ ca = tm.ChunkAttention(H, d, Lr, Lc, 1, 1)
 g = torch.Generator(device="cuda").manual_seed(1)
 mk = lambda L: torch.randn(L, H, d, device="cuda", dtype=torch.bfloat16, generator=g)
 ca.put_reference(0, 0, mk(Lr), mk(Lr))
+ZC = os.environ.get("SPANS_ZC") == "1"     # zero-copy calls (K/V already in the cache slot)
 for t in range(1, 6):
     q, k, v = mk(Lc), mk(Lc), mk(Lc)
     o = torch.empty_like(q)
+    if ZC:
+        k, v = ca.slot_ptr(0, 0, t)
     ca.attend(0, 0, t, q, k, v, o)
 torch.cuda.synchronize()
 W = 13 * 4096 + 8 * 160
