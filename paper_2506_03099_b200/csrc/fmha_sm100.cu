@@ -122,7 +122,7 @@ struct __align__(64) FmhaParams {
     // persistent schedule
     int n_qpairs;                     // Q-tile pairs per (b, h)
     int rounds;                       // R: whole units per CTA (unit c + k*C, k < R)
-    int l2_prefetch;                  // first item's Q and K/V tiles prefetched into L2 before the PDL wait
+    int l2_prefetch;                  // K/V tiles of the first item prefetched into L2 (with its Q) before the PDL wait
     int sk_units;                     // T = U - R*C tail units, spread stream-K style ...
     int sk_ctas;                      // ... over the first G' CTAs (contiguous tile ranges):
     int sk_bound[kMaxPersistentCtas + 1];   // CTA c takes tail tiles [sk_bound[c], sk_bound[c+1])
@@ -464,13 +464,13 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
         }
         // The first item's Q tiles and first K/V tiles into L2 while the
         // previous grid drains (one-GPU problems; peer windows are filled by
-        // other ranks during the launch).  TM_L2_PREFETCH=0 disables (A/B).
+        // other ranks during the launch).  TM_L2_PREFETCH=n: n K/V tiles (0: off).
         Item it0;
         if (p.l2_prefetch && get_item(p, 0, it0)) {
             for (int i = 0; i < 2; ++i)
                 for (int hf = 0; hf < D / 64; ++hf)
                     tma_prefetch_l2_4d(&p.tq, hf * 64, it0.h, it0.qp * 2 * kBM + i * kBM, it0.b);
-            for (int j = it0.lo; j < it0.hi && j < it0.lo + 2; ++j) {
+            for (int j = it0.lo; j < it0.hi && j < it0.lo + p.l2_prefetch; ++j) {
                 int seg, row, valid;
                 tile_info(p, j, seg, row, valid);
                 for (int hf = 0; hf < D / 64; ++hf) {
@@ -1277,11 +1277,11 @@ cudaError_t launch_fmha_sm100(const AttnProblem& pr, void* scratch, cudaStream_t
         if (G <= 0) return cudaErrorInvalidValue;
         for (int c = 0; c <= G; ++c) p.sk_bound[c] = b[c];
     }
-    static const bool l2_prefetch_env = [] {
+    static const int l2_prefetch_env = [] {
         const char* e = getenv("TM_L2_PREFETCH");
-        return !(e && strcmp(e, "0") == 0);
+        return e ? atoi(e) : 2;
     }();
-    p.l2_prefetch = l2_prefetch_env && !pr.peer;
+    p.l2_prefetch = pr.peer ? 0 : l2_prefetch_env;
     p.rounds = R;
     p.sk_units = T;
     p.sk_ctas = G;
