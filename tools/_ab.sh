@@ -1,6 +1,10 @@
-# bench step A/B of the L2 prefetch depth: TM_L2_PREFETCH = K/V tiles of the first item (0 = off)
-for rep in 1 2 3; do for v in 0 2 4 8; do
-  TM_L2_PREFETCH=$v python bench.py --no-extras --no-cpu-baseline --no-e2e --stream-chunks 0 2>/dev/null | python -c "
+# same-lib A/B of the early PDL trigger: TM_PDL_TRIGGER=0 vs 1 (default)
+timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/g30.log 2>&1
+for rep in 1 2 3; do for v in 0 1; do
+  TM_PDL_TRIGGER=$v python bench.py --no-extras --no-cpu-baseline --no-e2e --stream-chunks 0 2>/dev/null | python -c "
 import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); r=d['roofline']
-print('pf=$v', round(d['value'],1), 'live', round(r['achieved'],1), 'alone', round(r['achieved_kernel_alone'],1), 'chunk1', round(d['chunk1']['tflops_per_gpu'],1), d['clocks']['sm_mhz'])"
-done; done > gpurun_out/ab29.txt 2>&1
+print('trig=$v', round(d['value'],1), 'live', round(r['achieved'],1), 'alone', round(r['achieved_kernel_alone'],1), 'chunk1', round(d['chunk1']['tflops_per_gpu'],1), d['clocks']['sm_mhz'])"
+done; done > gpurun_out/ab30.txt 2>&1
+for rep in 1 2; do for cfg in "512 40" "512 5"; do set -- $cfg; for v in 0 1; do
+  echo "trig=$v $(TM_PDL_TRIGGER=$v SWEEP_CFG=$1 SWEEP_H=$2 timeout 120 python tools/sweep.py 2>&1 | tail -1)"
+done; done; done >> gpurun_out/ab30.txt 2>&1
