@@ -1085,12 +1085,15 @@ cudaError_t launch_t(const FmhaParams& p, int grid, cudaStream_t stream) {
 // c_t append all-MUFU measured ~1 % better (328.3 vs 332.0 us) and zero-copy
 // calls prefer 2/16 (317.8 vs 324.0; profiles/r1_poly_append_sweep.txt), but
 // one split for every launch keeps the append, zero-copy, window and Ulysses
-// paths bitwise identical (S:303 window == streaming).  The default is all
-// MUFU: with the v19 kernel (pipelined merge, L2 prefetch) it measured better
-// on the fused-append workload -- bench step 1368-1369 vs 1358-1363, chunk 1
-// +1.5 %, streaming 30.15 vs 30.53 ms/chunk -- at the cost of the zero-copy
-// kernel alone (1404-1409 vs 1429-1431; profiles/r1_v20_poly_ab.txt).
-// TM_POLY selects a split for tuning: 1 = all MUFU, 2 = 2/16, 3 = 3/16, 4 = 4/16.
+// paths bitwise identical (S:303 window == streaming).  With the v19 kernel
+// (pipelined merge, L2 prefetch) all-MUFU beat 2/16 on the fused-append
+// workload (bench step 1368-1369 vs 1358-1363, streaming 30.15 vs 30.53
+// ms/chunk) but lost 1.7 % on the zero-copy kernel alone
+// (profiles/r1_v20_poly_ab.txt); 1/16 then beat all-MUFU on every measure
+// (step +0.4 %, zero-copy alone +0.9 %, streaming +0.3 %;
+// profiles/r1_v21_poly_ab.txt), so the default is 1/16.
+// TM_POLY selects a split for tuning: 1 = all MUFU, 2 = 2/16, 3 = 3/16,
+// 4 = 4/16, 5 = 1/16 (default).
 constexpr uint32_t kPolyDefault = 0x0808u;   // pairs {3, 11} of every 16 (TM_POLY=2)
 template <int D>
 cudaError_t launch_d(const FmhaParams& p, int grid, cudaStream_t stream) {
@@ -1098,10 +1101,11 @@ cudaError_t launch_d(const FmhaParams& p, int grid, cudaStream_t stream) {
         const char* e = getenv("TM_POLY");
         return e ? atoi(e) : 0;
     }();
-    const int sel = env_sel ? env_sel : 1;
+    const int sel = env_sel ? env_sel : 5;
     switch (sel) {
         case 1: return launch_t<D, 0x0000u>(p, grid, stream);   // all MUFU
         case 3: return launch_t<D, 0x1084u>(p, grid, stream);   // {2,7,12}
+        case 5: return launch_t<D, 0x0800u>(p, grid, stream);   // {11}: 1/16
         case 4: return launch_t<D, 0x4444u>(p, grid, stream);   // {2,6,10,14}
         default: return launch_t<D, kPolyDefault>(p, grid, stream);
     }
