@@ -146,6 +146,27 @@ Layout layout_of(const tm_config* c) {
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
+// Selects device `dev` for the scope of one public call and restores the
+// caller's device on exit (a process may drive several GPUs through several
+// contexts; the caller's current device is never changed by a tm_* call).
+struct DeviceScope {
+    int prev = -1;
+    bool ok = true;
+    explicit DeviceScope(int dev) {
+        if (dev < 0) return;
+        if (cudaGetDevice(&prev) != cudaSuccess) {
+            prev = -1;
+            ok = false;
+            return;
+        }
+        if (prev != dev) ok = cudaSetDevice(dev) == cudaSuccess;
+        else prev = -1;                  // nothing to restore
+    }
+    ~DeviceScope() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
 }  // namespace
 
 struct tm_ctx {
@@ -401,8 +422,8 @@ tm_status tm_attn_init(const tm_config* cfg, const uint8_t* nccl_id, void* cache
         return fail(TM_ERR_INVALID_ARG, "world_size > 1 needs an NCCL unique id");
     int cur = -1;
     if (cudaGetDevice(&cur) != cudaSuccess) return fail(TM_ERR_CUDA, "no CUDA device");
-    if (cur != cfg->device && cudaSetDevice(cfg->device) != cudaSuccess)
-        return fail(TM_ERR_CUDA, "cannot select device %d", cfg->device);
+    DeviceScope dev_scope(cfg->device);  // restored on every return path
+    if (!dev_scope.ok) return fail(TM_ERR_CUDA, "cannot select device %d", cfg->device);
     int major = 0, minor = 0;
     cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, cfg->device);
     cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, cfg->device);
@@ -444,6 +465,7 @@ tm_status tm_attn_init(const tm_config* cfg, const uint8_t* nccl_id, void* cache
 
 tm_status tm_attn_destroy(tm_ctx* ctx) {
     if (!ctx) return fail(TM_ERR_INVALID_ARG, "null ctx");
+    DeviceScope dev_scope(ctx->cfg.device);
     if (ctx->comm) comm_destroy(ctx->comm);
     for (void* p : ctx->ipc_opened) cudaIpcCloseMemHandle(p);
     if (ctx->trace) cudaFree(ctx->trace);
@@ -487,6 +509,7 @@ tm_status tm_kvcache_put_reference_phases(tm_ctx* ctx, int32_t layer, int32_t st
                                           const void* v, uint32_t phases, void* stream) {
     NvtxRange nvtx_range("tm_kvcache_put_reference_phases");
     if (!ctx || !k || !v) return fail(TM_ERR_INVALID_ARG, "null argument");
+    DeviceScope dev_scope(ctx->cfg.device);
     tm_status st = check_layer_step(ctx, layer, step, true);
     if (st) return st;
     bool first = false;
@@ -579,6 +602,7 @@ tm_status tm_chunk_attention_phases(tm_ctx* ctx, int32_t layer, int32_t step, in
                                     uint32_t phases, void* stream) {
     NvtxRange nvtx_range("tm_chunk_attention_phases");
     if (!ctx || !q || !k || !v || !o) return fail(TM_ERR_INVALID_ARG, "null argument");
+    DeviceScope dev_scope(ctx->cfg.device);
     tm_status st = check_layer_step(ctx, layer, step, false);
     if (st) return st;
     if (chunk < 1) return fail(TM_ERR_INVALID_ARG, "chunk %lld < 1 (the reference is chunk 0)",
@@ -778,6 +802,7 @@ tm_status tm_reference_attention(tm_ctx* ctx, int32_t layer, int32_t step, const
                                  const void* k, const void* v, void* o, void* stream) {
     NvtxRange nvtx_range("tm_reference_attention");
     if (!ctx || !q || !k || !v || !o) return fail(TM_ERR_INVALID_ARG, "null argument");
+    DeviceScope dev_scope(ctx->cfg.device);
     if (ctx->lay.exchange || ctx->lay.P > 1 || ctx->lay.peer)
         return fail(TM_ERR_UNSUPPORTED, "tm_reference_attention needs a world_size == 1 direct context");
     tm_status st = check_layer_step(ctx, layer, step, true);
@@ -834,6 +859,7 @@ tm_status tm_window_attention(tm_ctx* ctx, const void* q, const void* k, const v
                               const int64_t* chunk_len, int32_t n_chunks, void* stream) {
     NvtxRange nvtx_range("tm_window_attention");
     if (!ctx || !q || !k || !v || !o || !chunk_len) return fail(TM_ERR_INVALID_ARG, "null argument");
+    DeviceScope dev_scope(ctx->cfg.device);
     if (ctx->lay.exchange || ctx->lay.P > 1)
         return fail(TM_ERR_UNSUPPORTED, "tm_window_attention needs a world_size == 1 context");
     if (n_chunks <= 0) return fail(TM_ERR_SHAPE, "n_chunks = %d <= 0", n_chunks);
@@ -897,6 +923,7 @@ tm_status tm_audio_cross_attention(tm_ctx* ctx, const void* q, const void* k_aud
     NvtxRange nvtx_range("tm_audio_cross_attention");
     if (!ctx || !q || !k_audio || !v_audio || !o || !scratch)
         return fail(TM_ERR_INVALID_ARG, "null argument");
+    DeviceScope dev_scope(ctx->cfg.device);
     if (ctx->lay.exchange || ctx->lay.P > 1)
         return fail(TM_ERR_UNSUPPORTED, "tm_audio_cross_attention needs a world_size == 1 context");
     if (frames <= 0 || tokens_per_frame <= 0 || audio_tokens_per_frame <= 0)
@@ -917,7 +944,7 @@ tm_status tm_audio_cross_attention(tm_ctx* ctx, const void* q, const void* k_aud
     const int row = cf.heads * cf.head_dim * ctx->lay.esize;          // bytes per token
     const int64_t BF = int64_t(cf.batch) * frames;
     uint8_t* qf = static_cast<uint8_t*>(scratch);
-    uint8_t* of = qf + scratch_bytes / 2;
+    uint8_t* of = qf + tm_audio_scratch_bytes(ctx, frames, n_face) / 2;   // 1024-B aligned half
     cudaStream_t cs = static_cast<cudaStream_t>(stream);
     ctx->launches = 0;
     tm_status st = cuda_check(launch_face_rows(q, qf, face_ids, BF, tokens_per_frame, n_face, row, 0,
@@ -971,6 +998,7 @@ tm_status tm_audio_cross_attention(tm_ctx* ctx, const void* q, const void* k_aud
 tm_status tm_flow_euler_step(tm_ctx* ctx, float* x, const void* v, int32_t v_dtype, int64_t n,
                              float dt, void* stream) {
     NvtxRange nvtx_range("tm_flow_euler_step");
+    DeviceScope dev_scope(ctx ? ctx->cfg.device : -1);
     if (n < 0) return fail(TM_ERR_SHAPE, "n = %lld < 0", (long long)n);
     if (n == 0) return TM_OK;
     if (!x || !v) return fail(TM_ERR_INVALID_ARG, "null argument");
@@ -1068,6 +1096,7 @@ tm_status tm_flow_sampler_step(tm_ctx* ctx, float* x, const void* v, int32_t v_d
                                float t_cur, float t_next, const float* eps, uint64_t seed,
                                uint64_t offset, void* x_bf16_out, void* stream) {
     NvtxRange nvtx_range("tm_flow_sampler_step");
+    DeviceScope dev_scope(ctx ? ctx->cfg.device : -1);
     if (n < 0) return fail(TM_ERR_SHAPE, "n = %lld < 0", (long long)n);
     if (n == 0) return TM_OK;
     if (!x || !v) return fail(TM_ERR_INVALID_ARG, "null argument");
@@ -1088,6 +1117,7 @@ tm_status tm_flow_sampler_step(tm_ctx* ctx, float* x, const void* v, int32_t v_d
 
 tm_status tm_peer_export(tm_ctx* ctx, uint8_t* handle) {
     if (!ctx || !handle) return fail(TM_ERR_INVALID_ARG, "null argument");
+    DeviceScope dev_scope(ctx->cfg.device);
     if (!ctx->lay.peer) return fail(TM_ERR_INVALID_ARG, "not a TM_TRANSPORT_PEER context");
     auto range = address_range_fn();
     if (!range) return fail(TM_ERR_CUDA, "cuMemGetAddressRange unavailable");
@@ -1109,6 +1139,7 @@ tm_status tm_peer_export(tm_ctx* ctx, uint8_t* handle) {
 
 tm_status tm_peer_connect(tm_ctx* ctx, const uint8_t* handles) {
     if (!ctx || !handles) return fail(TM_ERR_INVALID_ARG, "null argument");
+    DeviceScope dev_scope(ctx->cfg.device);
     if (!ctx->lay.peer) return fail(TM_ERR_INVALID_ARG, "not a TM_TRANSPORT_PEER context");
     if (ctx->connected) return fail(TM_ERR_STREAM_ORDER, "already connected");
     for (int p = 0; p < ctx->lay.P; ++p) {
@@ -1157,6 +1188,7 @@ tm_status tm_peer_output_ptr(tm_ctx* ctx, void** o) {
 
 tm_status tm_peer_check(tm_ctx* ctx) {
     if (!ctx) return fail(TM_ERR_INVALID_ARG, "null ctx");
+    DeviceScope dev_scope(ctx->cfg.device);
     if (ctx->comm) {                       // NCCL transport: the communicator's async state
         const char* e = comm_async_error(ctx->comm);
         if (e) return fail(TM_ERR_NCCL, "NCCL asynchronous error: %s", e);

@@ -16,16 +16,7 @@
 namespace tmk {
 namespace {
 
-int num_sms() {
-    static int n = 0;
-    if (!n) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        if (n <= 0) n = 148;
-    }
-    return n;
-}
+int num_sms() { return current_sm_count(); }
 
 cudaError_t finish(cudaError_t e, int* launches) {
     if (e == cudaSuccess && launches) ++*launches;

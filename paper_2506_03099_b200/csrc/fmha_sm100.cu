@@ -1050,26 +1050,22 @@ constexpr int smem_bytes() {
     return 1024 + (2 + kStages) * kBN * D * 2 + kEpiBytes + 512;
 }
 
-int sm_count() {
-    static int n = 0;
-    if (!n) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        if (n <= 0) n = 148;
-    }
-    return n;
-}
+int sm_count() { return current_sm_count(); }
 
 template <int D, uint32_t kPolyMask>
 cudaError_t launch_t(const FmhaParams& p, int grid, cudaStream_t stream) {
-    static bool attr = false;
-    if (!attr) {
+    // The max-dynamic-shared-memory attribute is per device: set once per
+    // device ordinal (bit per device; ordinals >= 64 set it on every launch).
+    static unsigned long long attr_set = 0;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
+    const unsigned long long bit = dev < 64 ? 1ull << dev : 0;
+    if (!bit || !(__atomic_load_n(&attr_set, __ATOMIC_RELAXED) & bit)) {
         cudaError_t e = cudaFuncSetAttribute(fmha_sm100_kernel<D, kPolyMask>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              smem_bytes<D>());
         if (e != cudaSuccess) return e;
-        attr = true;
+        __atomic_fetch_or(&attr_set, bit, __ATOMIC_RELAXED);
     }
     return launch_pdl(fmha_sm100_kernel<D, kPolyMask>, dim3(grid), dim3(kThreads), smem_bytes<D>(),
                       stream, p);

@@ -86,6 +86,28 @@ struct AttnProblem {
     int max_ctas = 0;                     // persistent grid cap (0: one CTA per SM)
 };
 
+// SM count of the CURRENT device, cached per device ordinal (a process may
+// drive several GPUs through several contexts; each entry point selects its
+// context's device first, see DeviceScope in api.cpp).
+inline int current_sm_count() {
+    constexpr int kMaxDev = 64;
+    static int cache[kMaxDev] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0) dev = 0;
+    if (dev >= kMaxDev) {
+        int n = 0;
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        return n > 0 ? n : 148;
+    }
+    int n = __atomic_load_n(&cache[dev], __ATOMIC_RELAXED);
+    if (n <= 0) {
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+        __atomic_store_n(&cache[dev], n, __ATOMIC_RELAXED);
+    }
+    return n;
+}
+
 // Launch with programmatic dependent launch allowed (the kernel executes
 // griddepcontrol.wait before touching global data, so its prologue overlaps the
 // previous kernel's tail).  TM_PDL=0 disables the attribute (A/B).

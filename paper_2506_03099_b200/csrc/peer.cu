@@ -19,16 +19,7 @@ namespace {
 
 constexpr int kThreads = 512;
 
-int sm_count_peer() {
-    static int n = 0;
-    if (!n) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        if (n <= 0) n = 148;
-    }
-    return n;
-}
+int sm_count_peer() { return current_sm_count(); }
 
 __global__ void __launch_bounds__(kThreads) peer_push_kernel(const __grid_constant__ PeerPush pp) {
     for (int T = 0; T < 3; ++T) {
@@ -63,7 +54,10 @@ __global__ void __launch_bounds__(kThreads) peer_recv_o_kernel(PeerCounters* own
     // 16-B words, 4 loads in flight per thread; rows of global token >= L are
     // shard padding (zero).  32-bit index math (the window is < 2^31 words).
     const uint32_t n = uint32_t(int64_t(B) * Ls * W);
-    const uint32_t valid_rows = uint32_t(L - int64_t(rank) * Ls);   // per batch element
+    // per batch element; a shard lying wholly in padding (e.g. L = 5, P = 4,
+    // rank 3) has none: clamp before the cast
+    const int64_t vr = L - int64_t(rank) * Ls;
+    const uint32_t valid_rows = uint32_t(vr < 0 ? 0 : (vr > Ls ? Ls : vr));
     const uint32_t stride = gridDim.x * blockDim.x;
     for (uint32_t base = blockIdx.x * blockDim.x + threadIdx.x; base < n; base += 4 * stride) {
         uint4 v[4];

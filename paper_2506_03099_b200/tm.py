@@ -119,8 +119,12 @@ def _ptr(x):
 
 
 def _stream(s):
+    """cudaStream_t of `s`; None means torch's CURRENT stream on the current
+    device (not the legacy default stream, which torch's non-blocking side
+    streams do not wait on)."""
     if s is None:
-        return None
+        import torch
+        return torch.cuda.current_stream().cuda_stream
     if isinstance(s, int):
         return s
     return s.cuda_stream
@@ -468,6 +472,12 @@ class ChunkAttention:
         ptr = (scratch.data_ptr() + 1023) // 1024 * 1024
         tm_audio_cross_attention(self.ctx, q, k_audio, v_audio, o, frames, T, A, face_ids, n,
                                  window, ptr, nb, stream)
+        # the kernels queued on `stream` still read the scratch: keep the caching
+        # allocator from handing the block out before they are done
+        if isinstance(stream, torch.cuda.Stream):
+            scratch.record_stream(stream)
+        elif isinstance(stream, int) and stream != torch.cuda.current_stream().cuda_stream:
+            scratch.record_stream(torch.cuda.ExternalStream(stream))
         return o
 
     def euler(self, x, v, v_dtype, dt, stream=None):
