@@ -275,7 +275,7 @@ def reference_arm(args, c):
            "config": {"workload": c["workload"], "heads": c["H"], "head_dim": c["d"],
                       "ref_tokens": c["Lr"], "chunk_tokens": c["Lc"], "chunk_index": 2},
            "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": threads, "kind": "oracle",
-                            "sample": sample},
+                            "sample": sample, "cpu_model": cpu_model(), "nproc": os.cpu_count()},
            "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}}
     print(json.dumps(out))
@@ -349,6 +349,146 @@ def measure_extras(tm, c, torch, stream):
                                    "audio tokens, 40 heads", "ms": ms,
                        "tflops": fl / (ms * 1e-3) / 1e12, "gbs_io": byts / (ms * 1e-3) / 1e9}
     ca.close()
+    return out
+
+
+def stored_traffic(config, P):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu
+    --set full capture (profiles/ncu_fmha_traffic.json): ncu cannot run inside
+    the bench, so `traffic` is the STORED figure of that capture, labelled."""
+    prof = os.path.join(ROOT, "profiles", "ncu_fmha_traffic.json")
+    try:
+        with open(prof) as f:
+            pj = json.load(f)
+        if pj.get("config") == config and pj.get("n_gpus") == P:
+            return pj.get("dram_bytes_per_launch"), \
+                f"stored: profiles/ncu_fmha_traffic.json ({pj.get('source', 'ncu --set full')})"
+    except Exception:
+        pass
+    return None, "no stored ncu capture for this config"
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def cpu_baseline(c, rows):
+    """The oracle as it stands, on all host cores and on one core (SURVEY
+    Sec 8(d) oracle timing), on bounded row samples of one t>=2 call."""
+    import oracle
+    dt, sfl, th = run_oracle_sample(c, rows, 7)
+    one_rows = max(8, rows // 16)
+    oracle.set_num_threads(1)
+    try:
+        dt1, sfl1, _ = run_oracle_sample(c, one_rows, 7, offset=3)
+    finally:
+        oracle.set_num_threads(th)
+    Lk = c["Lr"] + 2 * c["Lc"]
+    return {"value": sfl / dt / 1e12, "unit": "TFLOP/s", "cores": th, "kind": "oracle",
+            "sample": f"{rows} query rows x {c['H']} heads of one t>=2 call (Lk={Lk}); {dt:.1f} s",
+            "cpu_model": cpu_model(), "nproc": os.cpu_count(),
+            "one_core": {"value": sfl1 / dt1 / 1e12, "unit": "TFLOP/s", "cores": 1,
+                         "sample": f"{one_rows} query rows x {c['H']} heads; {dt1:.1f} s"},
+            "extrapolated_full_call_s": {"all_cores": dt * c["Lc"] / rows,
+                                         "one_core": dt1 * c["Lc"] / one_rows}}
+
+
+def attention_loop(tm, torch, H, d, Lr, Lc, K, stream, zero_copy=False, NL=8, NB=4):
+    """ms per chunk-attention call (t >= 2) of a fresh H-head context: K calls
+    back to back between one event pair, operands rotated over NL layer caches
+    and NB input sets (larger than L2); fused c_t append unless zero_copy."""
+    bf = torch.bfloat16
+    g = torch.Generator(device="cuda").manual_seed(2506030990 + 55 + H)
+    ca = tm.ChunkAttention(H, d, Lr, Lc, NL, 1)
+    sets = [[torch.randn(Lc, H, d, device="cuda", dtype=bf, generator=g) for _ in range(3)]
+            for _ in range(NB)]
+    o = torch.empty(Lc, H, d, device="cuda", dtype=bf)
+    kr = torch.randn(Lr, H, d, device="cuda", dtype=bf, generator=g)
+    for layer in range(NL):
+        ca.put_reference(layer, 0, kr, kr)
+    chunk = [0] * NL
+
+    def call(i):
+        layer = i % NL
+        chunk[layer] += 1
+        q, k, v = sets[i % NB]
+        if zero_copy and chunk[layer] >= 2:
+            kp, vp = ca.slot_ptr(layer, 0, chunk[layer])
+            # the slot holds c_{t-2}'s random K/V: realistic data, no copy
+            k, v = kp, vp
+        ca.attend(layer, 0, chunk[layer], q, k, v, o, stream)
+
+    for i in range(3 * NL):
+        call(i)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for i in range(K):
+        call(i)
+    b.record(stream)
+    torch.cuda.synchronize()
+    ca.close()
+    del sets
+    return a.elapsed_time(b) / K
+
+
+def measure_other_configs(tm, torch, main, K, stream):
+    """Driver-run lines for the other single-GPU configs of BASELINE.json
+    (720^2, configs[4]) and the Table-1 chunk-7 shape: the
+    attention-only loop of each (fused append, t >= 2)."""
+    peak = measured_peaks()[0]
+    out = {}
+    for name in ("wan720", "wan512c7"):
+        if name == main:
+            continue
+        cc = CONFIGS[name]
+        ms = attention_loop(tm, torch, cc["H"], cc["d"], cc["Lr"], cc["Lc"], K, stream)
+        fl = flop_per_call(cc)
+        out[name] = {"workload": cc["workload"], "keys_attended": cc["Lr"] + 2 * cc["Lc"],
+                     "ms_per_call": ms, "tflops": fl / (ms * 1e-3) / 1e12,
+                     "frac_of_bf16_peak": fl / (ms * 1e-3) / 1e12 / peak,
+                     "gflop_per_call": fl / 1e9,
+                     "timing": f"{K} calls (fused append) between one event pair"}
+        torch.cuda.empty_cache()
+    return out
+
+
+# Peer-copy bandwidth per direction per GPU measured on this pool
+# (/opt/skills/guides/B200_PROFILING.md), for the modelled exposed Q push.
+NVLINK_PEER_GBS = 770.0
+
+
+def measure_shards(tm, torch, c, K, stream, t1_ms):
+    """One rank's share of the WAN-512 call at P = 2, 4, 8 (H/P heads) on one
+    GPU -- the per-rank kernel of the Ulysses head sharding -- with
+    the fused append (as the P > 1 call runs it) and zero-copy, and the scaling
+    MODEL E(P) = t(1) / (P t(P)), t(P) = shard kernel + exposed Q push (remote
+    share of this rank's Q shard at the measured 770 GB/s peer copy) + 1 us
+    done barrier.  A model from one-GPU numbers, not a multi-GPU measurement."""
+    H, d, Lr, Lc = c["H"], c["d"], c["Lr"], c["Lc"]
+    out = {"model": "t(P) = shard kernel (fused append) + exposed Q push at "
+                    f"{NVLINK_PEER_GBS:.0f} GB/s + 1 us; E(P) = t(1) / (P t(P)); "
+                    "t(1) = this run's attention-only loop", "t1_ms": t1_ms}
+    for P in (2, 4, 8):
+        Hs = H // P
+        ms = attention_loop(tm, torch, Hs, d, Lr, Lc, K, stream)
+        ms_zc = attention_loop(tm, torch, Hs, d, Lr, Lc, K, stream, zero_copy=True)
+        Ls = -(-Lc // P)
+        q_push_us = Ls * H * d * 2 * (P - 1) / P / (NVLINK_PEER_GBS * 1e3)
+        t = ms + (q_push_us + 1.0) * 1e-3
+        fl = flop_per_call(c) / P
+        out[f"h{Hs}"] = {"P": P, "heads": Hs, "ms_fused_append": ms, "ms_zero_copy": ms_zc,
+                         "tflops_fused_append": fl / (ms * 1e-3) / 1e12,
+                         "tflops_zero_copy": fl / (ms_zc * 1e-3) / 1e12,
+                         "q_push_us_model": q_push_us, "t_model_ms": t,
+                         "E_model": t1_ms / (P * t)}
     return out
 
 
@@ -500,26 +640,33 @@ def main():
     barrier()
     w0 = time.time()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    # Events around every 4th attention call inside the timed region give the
-    # dominant kernel's live duration (roofline.achieved).  Not every call: an
-    # event pair costs ~6 us per step (it also stops the next launch's prologue
-    # from overlapping the previous kernel).
-    EV_EVERY = 4
-    lev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(0, args.steps, EV_EVERY)]
     nvml.start()
     e0.record(stream)
     for i in range(args.steps):
-        step(i, ev=lev[i // EV_EVERY] if i % EV_EVERY == 0 else None)
+        step(i)
     e1.record(stream)
     barrier()
     nvml.stop()
     w1 = time.time()
     ms_total = max_over_ranks(e0.elapsed_time(e1))
-    live = [a.elapsed_time(b) for a, b in lev]
-    live_ms = max_over_ranks(statistics.mean(live))
-    live_med = max_over_ranks(statistics.median(live))
     gpu_launches = launches[0]
+
+    # ---------------------------------------------------------------- dominant kernel, live
+    # roofline.achieved: the same attention calls as the step (fused c_t append,
+    # same input rotation) back to back, WITHOUT the Euler update, between ONE
+    # event pair on the launching stream -- so the launches overlap exactly as
+    # in the step (PDL) and the per-launch time cannot exceed ms_per_step.
+    barrier()
+    la0, la1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    la0.record(stream)
+    for i in range(args.steps):
+        layer = i % NL
+        chunk[layer] += 1
+        q, k, v = sets[i % NB]
+        ca.attend(layer, 0, chunk[layer], q, k, v, outs[i % NB], stream)
+    la1.record(stream)
+    barrier()
+    live_ms = max_over_ranks(la0.elapsed_time(la1) / args.steps)
 
     # ---------------------------------------------------------------- attention kernel alone
     # P = 1: K/V pre-placed in the cache slot (zero-copy append) so each call is
@@ -695,32 +842,24 @@ def main():
                      "tflops": NLs * NS * flop_per_call(c) / (s_ms * 1e-3) / 1e12}
         sc.close()
 
-    extras = None
+    extras = others = shards = None
     if not args.no_extras and P == 1:
         extras = measure_extras(tm, c, torch, stream)
+        others = measure_other_configs(tm, torch, args.config, max(10, args.steps), stream)
+        if args.config == "wan512":
+            shards = measure_shards(tm, torch, c, max(10, args.steps), stream, live_ms)
 
     fl = flop_per_call(c)
     ms_step = ms_total / args.steps
     value = fl * args.steps / (ms_total * 1e-3) / 1e12
     peak, peak_sus, peak_src = measured_peaks()
-    # per GPU (each rank does 1/P of the heads); live = inside the timed region
+    # per GPU (each rank does 1/P of the heads); live = the attention-only loop
     achieved = fl / P / (live_ms * 1e-3) / 1e12
     achieved_alone = fl / P / (k_ms * 1e-3) / 1e12
-    prof = os.path.join(ROOT, "profiles", "ncu_fmha_traffic.json")
-    traffic = None
-    try:
-        with open(prof) as f:
-            pj = json.load(f)
-        if pj.get("config") == args.config and pj.get("n_gpus") == P:
-            traffic = pj.get("dram_bytes_per_launch")
-    except Exception:
-        pass
+    traffic, traffic_src = stored_traffic(args.config, P)
     cpu = None
     if rank == 0 and P == 1 and not args.no_cpu_baseline:
-        dt, sfl, th = run_oracle_sample(c, args.oracle_rows, 7)
-        cpu = {"value": sfl / dt / 1e12, "unit": "TFLOP/s", "cores": th, "kind": "oracle",
-               "sample": f"{args.oracle_rows} query rows x {H} heads of one t>=2 call "
-                         f"(Lk={Lr + 2 * Lc}); {dt:.1f} s"}
+        cpu = cpu_baseline(c, args.oracle_rows)
     if rank == 0:
         out = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": P,
@@ -743,22 +882,26 @@ def main():
             "frac_of_bf16_peak": achieved / peak,
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak,
                          "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+                         "traffic_source": traffic_src,
                          "kernel": "tm_fmha_sm100 (tcgen05, fused c_t append)" if P == 1 and
                                    transport == "nccl" else
                                    f"whole call ({transport} transport: exchange + attention)",
-                         "timing": f"CUDA events around every {EV_EVERY}th of the {args.steps} "
-                                   "attention calls inside the timed region (mean)",
-                         "peak_source": f"{peak_src} bf16 burst",
+                         "timing": f"{args.steps} attention calls of the step (fused append, same "
+                                   "inputs, no Euler) back to back between one CUDA event pair "
+                                   "on the launching stream, right after the timed region",
+                         "ms_per_launch": live_ms,
+                         "peak_source": f"{peak_src} bf16 burst (MEASURED_PEAKS.json)",
                          "flop_per_launch": fl / P,
-                         "achieved_median_launch": fl / P / (live_med * 1e-3) / 1e12,
+                         "algorithmic_bytes_per_launch": algo_bytes(c) / P,
                          "achieved_kernel_alone": achieved_alone,
                          "kernel_alone": "zero-copy calls (no append), per-call events, after the "
-                                         "timed region" if zc else "whole calls, per-call events",
-                         "algorithmic_bytes_per_launch": algo_bytes(c)},
+                                         "timed region" if zc else "whole calls, per-call events"},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "streaming": streaming,
             "next_rows": extras,
+            "other_configs": others,
+            "shards": shards,
             "gpu_launches": gpu_launches,
             "clocks": clk,
         }

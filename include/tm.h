@@ -142,7 +142,9 @@ tm_status tm_get_unique_id(uint8_t id[128]);
 /* Create a context.  `cache` (device, >= tm_kvcache_bytes, 1024-B aligned)
  * and `workspace` (device, >= tm_workspace_bytes, 256-B aligned) are owned
  * by the caller and must outlive the ctx.  nccl_id: NULL when world_size==1
- * or with TM_TRANSPORT_PEER (which then needs tm_peer_connect before use).
+ * or with TM_TRANSPORT_PEER (which then needs tm_peer_connect before use);
+ * NULL with TM_TRANSPORT_NCCL and world_size > 1 defers the communicator to a
+ * loopback group (tm_nccl_connect_local).
  * Validates the config (TM_ERR_SHAPE for H % P != 0, d not in {64,128},
  * non-positive lengths).  Collective when world_size > 1. */
 tm_status tm_attn_init(const tm_config* cfg, const uint8_t* nccl_id, void* cache,
@@ -229,7 +231,10 @@ tm_status tm_audio_cross_attention(tm_ctx* ctx, const void* q, const void* k_aud
  * call.  Arguments are validated on the operation's first phase; the later
  * phases of the same operation must repeat them (TM_ERR_STREAM_ORDER
  * otherwise, or if a phase is skipped or a new operation starts before the
- * previous one finished its RECV phase).  NCCL contexts accept only ALL. */
+ * previous one finished its RECV phase).  NCCL contexts accept only ALL,
+ * except loopback groups (tm_nccl_connect_local), where SEND packs the shard,
+ * ATTEND exchanges, unpacks, attends and packs O, and RECV exchanges O and
+ * unpacks it to o. */
 tm_status tm_chunk_attention_phases(tm_ctx* ctx, int32_t layer, int32_t step, int64_t chunk,
                                     const void* q, const void* k, const void* v, void* o,
                                     uint32_t phases, void* stream);
@@ -247,6 +252,17 @@ tm_status tm_kvcache_put_reference_phases(tm_ctx* ctx, int32_t layer, int32_t st
  * cudaMalloc (torch's default caching allocator), not VMM.
  * tm_peer_connect_local connects `n` contexts of ONE process (virtual ranks,
  * e.g. several on one device for tests): ctxs[i] must have rank i. */
+/* TM_TRANSPORT_NCCL loopback group (tests / single-process use): `n` >= 2
+ * contexts of ONE process with world_size n, ctxs[i] of rank i, each created
+ * with nccl_id = NULL (tm_attn_init then defers the communicator).  Their
+ * all-to-alls become device copies between the contexts' workspaces (the same
+ * block permutation ncclAlltoAll performs, so the pack / unpack kernels and
+ * the head-sharded attention run exactly as with NCCL).  The contexts must be
+ * driven on one stream with the phased calls, every rank's SEND before any
+ * rank's ATTEND and every ATTEND before any RECV.  Until connected, their
+ * exchanging calls return TM_ERR_STREAM_ORDER. */
+tm_status tm_nccl_connect_local(tm_ctx* const* ctxs, int32_t n);
+
 tm_status tm_peer_export(tm_ctx* ctx, uint8_t handle[TM_PEER_HANDLE_BYTES]);
 tm_status tm_peer_connect(tm_ctx* ctx, const uint8_t* handles);
 tm_status tm_peer_connect_local(tm_ctx* const* ctxs, int32_t n);

@@ -103,7 +103,7 @@ struct Layout {
     int esize, Hl, P;
     int64_t Lr, Lc, Lr_s, Lc_s;     // full and per-rank shard token counts
     size_t ref_bytes, slot_bytes, region_bytes, cache_bytes;
-    size_t flag_bytes, scratch_bytes, xfer_bytes, head_bytes, ws_bytes;
+    size_t flag_bytes, scratch_bytes, xfer_bytes, head_bytes, osend_bytes, ws_bytes;
 };
 
 Layout layout_of(const tm_config* c) {
@@ -137,7 +137,12 @@ Layout layout_of(const tm_config* c) {
         const size_t kv = 2 * align_up(size_t(c->batch) * L.Lr_s * full_row);
         L.xfer_bytes = qkv > kv ? qkv : kv;
         L.head_bytes = L.slot_bytes;                               // Q or O, [B][Lc][Hl][d]
-        L.ws_bytes = L.flag_bytes + L.scratch_bytes + 2 * L.xfer_bytes + 2 * L.head_bytes;
+        // O's send blocks [P][B][Lc/P][Hl][d] have their own region: in a
+        // loopback group (tm_nccl_connect_local) the other ranks may still read
+        // this rank's Q/K/V send blocks after it has packed O.
+        L.osend_bytes = align_up(size_t(c->batch) * L.Lc_s * full_row);
+        L.ws_bytes = L.flag_bytes + L.scratch_bytes + 2 * L.xfer_bytes + 2 * L.head_bytes +
+                     L.osend_bytes;
     } else {
         L.ws_bytes = L.flag_bytes + L.scratch_bytes;
     }
@@ -178,6 +183,7 @@ struct tm_ctx {
     std::vector<int64_t> last;        // [layer][step]: last chunk attended (0 = none)
     std::vector<uint8_t> ref_ok;      // [layer][step]: reference written
     void* comm = nullptr;
+    bool lb_pending = false;           // NCCL transport, world > 1, no unique id: loopback group
     int launches = 0;
     bool debug = false;
     // peer transport
@@ -209,6 +215,10 @@ struct tm_ctx {
     uint8_t* recv() const { return send() + lay.xfer_bytes; }
     uint8_t* qh() const { return recv() + lay.xfer_bytes; }
     uint8_t* oh() const { return qh() + lay.head_bytes; }
+    uint8_t* osend() const { return oh() + lay.head_bytes; }
+    // NCCL transport without a communicator: a loopback group of contexts in
+    // one process (tm_nccl_connect_local), all-to-all = device copies.
+    std::vector<tm_ctx*> lb_group;
     // peer window of rank r (own: r == cfg.rank)
     PeerCounters* ctr(int r) const { return reinterpret_cast<PeerCounters*>(win[r]); }
     uint8_t* wq(int r) const { return win[r] + 4096; }
@@ -250,23 +260,74 @@ tm_status check_layer_step(const tm_ctx* c, int32_t layer, int32_t step, bool al
     return TM_OK;
 }
 
-// Ulysses seq -> head exchange of `ntensors` tensors of [B][Ls][H][d] each;
-// received blocks are unpacked to dst[i] ([B][L][Hl][d]).  P:171.
-tm_status ulysses_in(tm_ctx* c, int ntensors, const void* const* src, void* const* dst, int64_t Ls,
-                     int64_t L, cudaStream_t s) {
+// The all-to-all of the NCCL transport: block p of `send` (bytes each) goes
+// to rank p, block q of `recv` comes from rank q.  With a communicator:
+// ncclAlltoAll.  In a loopback group (tm_nccl_connect_local; ranks of one
+// process, e.g. virtual ranks on one device for tests) the same permutation
+// is done with device copies from the other ranks' send regions: the group
+// shares one stream and every rank's pack precedes any rank's exchange
+// (the phased calls, TM_PHASE_*), so the copies see the packed blocks.
+tm_status exchange_a2a(tm_ctx* c, const uint8_t* send, uint8_t* recv, size_t bytes, cudaStream_t s,
+                       const char* what) {
+    const int P = c->lay.P;
+    if (c->comm) {
+        const char* e = comm_alltoall(c->comm, send, recv, bytes, P, s);
+        return e ? fail(TM_ERR_NCCL, "all-to-all (%s): %s", what, e) : TM_OK;
+    }
+    if (int(c->lb_group.size()) != P)
+        return fail(TM_ERR_STREAM_ORDER, "NCCL transport without a communicator: connect the "
+                                         "loopback group first (tm_nccl_connect_local)");
+    const size_t off = size_t(send - c->ws);
+    const int r = c->cfg.rank;
+    for (int q = 0; q < P; ++q) {
+        const uint8_t* src = c->lb_group[q]->ws + off + size_t(r) * bytes;
+        tm_status st = cuda_check(cudaMemcpyAsync(recv + size_t(q) * bytes, src, bytes,
+                                                  cudaMemcpyDeviceToDevice, s),
+                                  "loopback all-to-all copy");
+        if (st) return st;
+    }
+    return TM_OK;
+}
+
+// An NCCL-transport context can exchange: a communicator, or a connected
+// loopback group.  Checked before any launch (host error, no side effects).
+tm_status exchange_ready(const tm_ctx* c) {
+    if (!c->lay.exchange || c->comm || int(c->lb_group.size()) == c->lay.P) return TM_OK;
+    return fail(TM_ERR_STREAM_ORDER, "NCCL transport without a communicator: connect the loopback "
+                                     "group first (tm_nccl_connect_local)");
+}
+
+// Ulysses seq -> head exchange of `ntensors` tensors of [B][Ls][H][d] each
+// (P:171), in two halves: pack into the per-peer send blocks, then exchange
+// and unpack the received blocks to dst[i] ([B][L][Hl][d]).
+size_t xfer_block(const tm_ctx* c, int64_t Ls) {
+    return align_up(size_t(c->cfg.batch) * Ls * c->cfg.heads * c->cfg.head_dim * c->lay.esize);
+}
+
+tm_status ulysses_pack_in(tm_ctx* c, int ntensors, const void* const* src, int64_t Ls,
+                          cudaStream_t s) {
     const Layout& Ly = c->lay;
     const int d = c->cfg.head_dim, B = c->cfg.batch, H = c->cfg.heads;
-    const size_t blk = align_up(size_t(B) * Ls * H * d * Ly.esize);
+    const size_t blk = xfer_block(c, Ls);
     for (int i = 0; i < ntensors; ++i) {
         tm_status st = cuda_check(launch_pack_seq_to_peers(src[i], c->send() + i * blk, B, Ls, H,
                                                            Ly.P, d, Ly.esize, s, &c->launches),
                                   "pack seq->peers");
         if (st) return st;
     }
+    return TM_OK;
+}
+
+tm_status ulysses_exchange_in(tm_ctx* c, int ntensors, void* const* dst, int64_t Ls, int64_t L,
+                              cudaStream_t s) {
+    const Layout& Ly = c->lay;
+    const int d = c->cfg.head_dim, B = c->cfg.batch;
+    const size_t blk = xfer_block(c, Ls);
+    const size_t per_peer = size_t(B) * Ls * Ly.Hl * d * Ly.esize;
     for (int i = 0; i < ntensors; ++i) {
-        const char* e = comm_alltoall(c->comm, c->send() + i * blk, c->recv() + i * blk,
-                                      size_t(B) * Ls * Ly.Hl * d * Ly.esize, Ly.P, s);
-        if (e) return fail(TM_ERR_NCCL, "all-to-all (seq->head): %s", e);
+        tm_status st = exchange_a2a(c, c->send() + i * blk, c->recv() + i * blk, per_peer, s,
+                                    "seq->head");
+        if (st) return st;
     }
     for (int i = 0; i < ntensors; ++i) {
         tm_status st = cuda_check(launch_unpack_peers_to_heads(c->recv() + i * blk, dst[i], B, Ls,
@@ -315,8 +376,9 @@ tm_status begin_phases(tm_ctx* c, int kind, uint32_t phases, int layer, int step
                        const void* a0, const void* a1, const void* a2, const void* a3, bool* first) {
     if (phases == 0 || phases > TM_PHASE_ALL || phases == (TM_PHASE_SEND | TM_PHASE_RECV))
         return fail(TM_ERR_INVALID_ARG, "phases 0x%x: a non-empty run of SEND, ATTEND, RECV", phases);
-    if (!c->lay.peer && phases != TM_PHASE_ALL)
-        return fail(TM_ERR_UNSUPPORTED, "phased calls need TM_TRANSPORT_PEER");
+    if (!c->lay.peer && phases != TM_PHASE_ALL && !(c->lay.exchange && c->lb_pending))
+        return fail(TM_ERR_UNSUPPORTED, "phased calls need TM_TRANSPORT_PEER or a loopback "
+                                        "NCCL-transport group (tm_nccl_connect_local)");
     const uint32_t lowest = phases & (~phases + 1);
     if (c->op_kind == 0) {
         if (lowest != TM_PHASE_SEND)
@@ -418,8 +480,9 @@ tm_status tm_attn_init(const tm_config* cfg, const uint8_t* nccl_id, void* cache
         if (e) return fail(TM_ERR_NCCL, "%s", e);
         nccl_id = local_id;
     }
-    if (L.exchange && !nccl_id)
-        return fail(TM_ERR_INVALID_ARG, "world_size > 1 needs an NCCL unique id");
+    // world_size > 1 without an id: a loopback group, connected later with
+    // tm_nccl_connect_local (test / single-process use)
+    const bool lb_pending = L.exchange && !nccl_id;
     int cur = -1;
     if (cudaGetDevice(&cur) != cudaSuccess) return fail(TM_ERR_CUDA, "no CUDA device");
     DeviceScope dev_scope(cfg->device);  // restored on every return path
@@ -452,7 +515,8 @@ tm_status tm_attn_init(const tm_config* cfg, const uint8_t* nccl_id, void* cache
         c->win[cfg->rank] = c->ws + L.win_off;
         c->connected = L.P == 1;       // a one-rank group is its own peer
     }
-    if (L.exchange) {
+    c->lb_pending = lb_pending;
+    if (L.exchange && !lb_pending) {
         const char* e = comm_init(&c->comm, cfg->world_size, cfg->rank, nccl_id);
         if (e) {
             delete c;
@@ -512,6 +576,8 @@ tm_status tm_kvcache_put_reference_phases(tm_ctx* ctx, int32_t layer, int32_t st
     DeviceScope dev_scope(ctx->cfg.device);
     tm_status st = check_layer_step(ctx, layer, step, true);
     if (st) return st;
+    st = exchange_ready(ctx);
+    if (st) return st;
     bool first = false;
     st = begin_phases(ctx, 2, phases, layer, step, 0, k, v, nullptr, nullptr, &first);
     if (st) return st;
@@ -565,8 +631,8 @@ tm_status tm_kvcache_put_reference_phases(tm_ctx* ctx, int32_t layer, int32_t st
             for (int s = s0; s < s1; ++s) ctx->ref_ok[ctx->idx(layer, s)] = 1;
         return TM_OK;
     }
-    note_phases(ctx, 2, phases, layer, step, 0, k, v, nullptr, nullptr);
     if (!Ly.exchange) {
+        note_phases(ctx, 2, phases, layer, step, 0, k, v, nullptr, nullptr);
         const size_t bytes = size_t(ctx->cfg.batch) * Ly.Lr * Ly.Hl * ctx->cfg.head_dim * Ly.esize;
         for (int s = s0; s < s1; ++s) {
             st = cuda_check(cudaMemcpyAsync(ctx->kref(layer, s), k, bytes, cudaMemcpyDeviceToDevice, cs),
@@ -577,16 +643,26 @@ tm_status tm_kvcache_put_reference_phases(tm_ctx* ctx, int32_t layer, int32_t st
             if (st) return st;
         }
     } else {
-        const void* src[2] = {k, v};
-        void* dst[2] = {ctx->kref(layer, s0), ctx->vref(layer, s0)};
-        st = ulysses_in(ctx, 2, src, dst, Ly.Lr_s, Ly.Lr, cs);
-        if (st) return st;
-        for (int s = s0 + 1; s < s1; ++s) {
-            st = cuda_check(cudaMemcpyAsync(ctx->kref(layer, s), ctx->kref(layer, s0), 2 * Ly.ref_bytes,
-                                            cudaMemcpyDeviceToDevice, cs),
-                            "reference alias copy");
+        // NCCL transport: SEND packs the shard, ATTEND exchanges and unpacks
+        // into the cache's reference region (RECV has nothing left to do).
+        if (phases & TM_PHASE_SEND) {
+            const void* src[2] = {k, v};
+            st = ulysses_pack_in(ctx, 2, src, Ly.Lr_s, cs);
             if (st) return st;
         }
+        if (phases & TM_PHASE_ATTEND) {
+            void* dst[2] = {ctx->kref(layer, s0), ctx->vref(layer, s0)};
+            st = ulysses_exchange_in(ctx, 2, dst, Ly.Lr_s, Ly.Lr, cs);
+            if (st) return st;
+            for (int s = s0 + 1; s < s1; ++s) {
+                st = cuda_check(cudaMemcpyAsync(ctx->kref(layer, s), ctx->kref(layer, s0),
+                                                2 * Ly.ref_bytes, cudaMemcpyDeviceToDevice, cs),
+                                "reference alias copy");
+                if (st) return st;
+            }
+        }
+        note_phases(ctx, 2, phases, layer, step, 0, k, v, nullptr, nullptr);
+        if (!(phases & TM_PHASE_RECV)) return TM_OK;
     }
     for (int s = s0; s < s1; ++s) ctx->ref_ok[ctx->idx(layer, s)] = 1;
     return TM_OK;
@@ -609,6 +685,8 @@ tm_status tm_chunk_attention_phases(tm_ctx* ctx, int32_t layer, int32_t step, in
                                (long long)chunk);
     if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o))
         return fail(TM_ERR_INVALID_ARG, "q, k, v, o must be 16-byte aligned");
+    st = exchange_ready(ctx);
+    if (st) return st;
     bool first = false;
     st = begin_phases(ctx, 1, phases, layer, step, chunk, q, k, v, o, &first);
     if (st) return st;
@@ -731,14 +809,23 @@ tm_status tm_chunk_attention_phases(tm_ctx* ctx, int32_t layer, int32_t step, in
             }
         }
     } else {
-        // a2: seq -> head all-to-all; K/V land in the cache slot (a3), Q in workspace.
-        const void* src[3] = {q, k, v};
-        void* dst[3] = {ctx->qh(), kslot, vslot};
-        st = ulysses_in(ctx, 3, src, dst, Ly.Lc_s, Ly.Lc, cs);
-        if (st) return st;
+        // a2: seq -> head all-to-all; K/V land in the cache slot (a3), Q in
+        // workspace.  Phases (loopback groups): SEND packs, ATTEND exchanges,
+        // unpacks, attends and packs O, RECV exchanges O and unpacks it.
+        if (phases & TM_PHASE_SEND) {
+            const void* src[3] = {q, k, v};
+            st = ulysses_pack_in(ctx, 3, src, Ly.Lc_s, cs);
+            if (st) return st;
+        }
+        if (phases & TM_PHASE_ATTEND) {
+            void* dst[3] = {ctx->qh(), kslot, vslot};
+            st = ulysses_exchange_in(ctx, 3, dst, Ly.Lc_s, Ly.Lc, cs);
+            if (st) return st;
+        }
         qattn = ctx->qh();
         oattn = ctx->oh();
     }
+    const bool attend = !Ly.exchange || (phases & TM_PHASE_ATTEND);
 
     // a4: mask {c_0, c_{t-1}, c_t} -> segment schedule.  c_{t-1} is
     // the other slot; at chunk 1 it coincides with c_0 and is not repeated
@@ -763,12 +850,14 @@ tm_status tm_chunk_attention_phases(tm_ctx* ctx, int32_t layer, int32_t step, in
         pr.seg[pr.nseg++] = Segment{kslot, vslot, Ly.Lc};
     }
 
+    if (attend) {
     if (ctx->trace) cudaMemsetAsync(ctx->trace, 0, kTraceWords * 8, cs);
     cudaError_t e = cf.dtype == TM_BF16 ? launch_fmha_sm100(pr, ctx->scratch(), cs, &ctx->launches, ctx->trace)
                                         : launch_fmha_fp32(pr, cs, &ctx->launches);
     st = cuda_check(e, "attention kernel launch");
     if (st) return st;
-    if (ctx->trace) {   // debug only: dump CTA 0's timeline (synchronises)
+    }
+    if (attend && ctx->trace) {   // debug only: dump CTA 0's timeline (synchronises)
         std::vector<unsigned long long> h(kTraceWords);
         cudaMemcpyAsync(h.data(), ctx->trace, h.size() * 8, cudaMemcpyDeviceToHost, cs);
         cudaStreamSynchronize(cs);
@@ -779,15 +868,19 @@ tm_status tm_chunk_attention_phases(tm_ctx* ctx, int32_t layer, int32_t step, in
     }
 
     if (Ly.exchange) {
-        // a6: head -> seq all-to-all of O.
+        // a6: head -> seq all-to-all of O (packed at the end of ATTEND into its
+        // own send region, exchanged and unpacked in RECV).
         const size_t blk = size_t(cf.batch) * Ly.Lc_s * Ly.Hl * cf.head_dim * Ly.esize;
-        st = cuda_check(launch_pack_heads_to_peers(ctx->oh(), ctx->send(), cf.batch, Ly.Lc_s, Ly.Lc,
-                                                   Ly.Hl, Ly.P, cf.head_dim, Ly.esize, cs,
-                                                   &ctx->launches),
-                        "pack heads->peers");
+        if (phases & TM_PHASE_ATTEND) {
+            st = cuda_check(launch_pack_heads_to_peers(ctx->oh(), ctx->osend(), cf.batch, Ly.Lc_s,
+                                                       Ly.Lc, Ly.Hl, Ly.P, cf.head_dim, Ly.esize, cs,
+                                                       &ctx->launches),
+                            "pack heads->peers");
+            if (st) return st;
+        }
+        if (!(phases & TM_PHASE_RECV)) return TM_OK;
+        st = exchange_a2a(ctx, ctx->osend(), ctx->recv(), blk, cs, "head->seq");
         if (st) return st;
-        const char* ce = comm_alltoall(ctx->comm, ctx->send(), ctx->recv(), blk, Ly.P, cs);
-        if (ce) return fail(TM_ERR_NCCL, "all-to-all (head->seq): %s", ce);
         st = cuda_check(launch_unpack_peers_to_seq(ctx->recv(), o, cf.batch, Ly.Lc_s, cf.heads, Ly.P,
                                                    cf.head_dim, Ly.esize, cs, &ctx->launches),
                         "unpack peers->seq");
@@ -1176,6 +1269,23 @@ tm_status tm_peer_connect_local(tm_ctx* const* ctxs, int32_t n) {
         for (int p = 0; p < n; ++p) ctxs[i]->win[p] = ctxs[p]->win[p];
         ctxs[i]->connected = true;
     }
+    return TM_OK;
+}
+
+tm_status tm_nccl_connect_local(tm_ctx* const* ctxs, int32_t n) {
+    if (!ctxs || n <= 1 || n > 64) return fail(TM_ERR_INVALID_ARG, "need 2..64 contexts");
+    for (int i = 0; i < n; ++i) {
+        const tm_ctx* c = ctxs[i];
+        if (!c || c->lay.peer || !c->lay.exchange || !c->lb_pending || c->cfg.world_size != n ||
+            c->cfg.rank != i)
+            return fail(TM_ERR_INVALID_ARG, "ctxs[%d] must be a TM_TRANSPORT_NCCL context of rank %d "
+                                            "in a group of %d created without an NCCL unique id",
+                        i, i, n);
+        if (!c->lb_group.empty()) return fail(TM_ERR_STREAM_ORDER, "ctxs[%d] already connected", i);
+        if (c->lay.ws_bytes != ctxs[0]->lay.ws_bytes)
+            return fail(TM_ERR_INVALID_ARG, "ctxs[%d] has a different workspace layout", i);
+    }
+    for (int i = 0; i < n; ++i) ctxs[i]->lb_group.assign(ctxs, ctxs + n);
     return TM_OK;
 }
 

@@ -71,6 +71,7 @@ def _load():
         "tm_peer_export": ([V, ctypes.c_char_p], i32),
         "tm_peer_connect": ([V, ctypes.c_char_p], i32),
         "tm_peer_connect_local": ([P(V), i32], i32),
+        "tm_nccl_connect_local": ([P(V), i32], i32),
         "tm_peer_check": ([V], i32),
         "tm_peer_output_ptr": ([V, P(V)], i32),
         "tm_schedule_tail_host": ([i32, i32, i32, P(i32)], i32),
@@ -104,7 +105,7 @@ EXPORTED = ("tm_version", "tm_last_error", "tm_kvcache_bytes", "tm_workspace_byt
             "tm_window_attention", "tm_reference_attention", "tm_flow_sampler_step", "tm_audio_scratch_bytes",
             "tm_audio_cross_attention", "tm_chunk_attention_phases",
             "tm_kvcache_put_reference_phases", "tm_peer_export", "tm_peer_connect",
-            "tm_peer_connect_local", "tm_peer_check", "tm_peer_route_host", "tm_peer_output_ptr",
+            "tm_peer_connect_local", "tm_nccl_connect_local", "tm_peer_check", "tm_peer_route_host", "tm_peer_output_ptr",
             "tm_schedule_tail_host",
             "tm_last_launch_count",
             "tm_kernel_variant")
@@ -124,6 +125,8 @@ def _stream(s):
     streams do not wait on)."""
     if s is None:
         import torch
+        if not torch.cuda.is_available():     # host-only calls (argument errors, CPU tests)
+            return None
         return torch.cuda.current_stream().cuda_stream
     if isinstance(s, int):
         return s
@@ -206,6 +209,11 @@ def tm_peer_connect(ctx, handles) -> None:
 def tm_peer_connect_local(ctxs) -> None:
     arr = (ctypes.c_void_p * len(ctxs))(*ctxs)
     _check(lib.tm_peer_connect_local(arr, len(ctxs)))
+
+
+def tm_nccl_connect_local(ctxs) -> None:
+    arr = (ctypes.c_void_p * len(ctxs))(*ctxs)
+    _check(lib.tm_nccl_connect_local(arr, len(ctxs)))
 
 
 def tm_peer_output_ptr(ctx) -> int:
@@ -431,6 +439,12 @@ class ChunkAttention:
     @staticmethod
     def connect_local(cas):
         tm_peer_connect_local([c.ctx for c in cas])
+
+    @staticmethod
+    def nccl_connect_local(cas):
+        """Loopback NCCL-transport group of contexts in this process (created
+        with nccl_id=None): all-to-all as device copies (tm_nccl_connect_local)."""
+        tm_nccl_connect_local([c.ctx for c in cas])
 
     def check(self):
         tm_peer_check(self.ctx)
