@@ -112,12 +112,22 @@ typedef struct {
     int32_t rank;          /* this process's rank in [0, P)                           */
     int32_t device;        /* CUDA device ordinal used by this ctx                    */
     int32_t transport;     /* tm_transport (ignored when world_size == 1 and NCCL)    */
+    int32_t sched_heads;   /* heads per SCHEDULE BLOCK of the attention kernel; 0 =
+                            * all heads of the rank in one block (fastest).  k > 0
+                            * (must divide heads / world_size): every k heads are
+                            * scheduled as a block of their own -- which units are
+                            * split for load balance, where, and the merge order are
+                            * a function of the block's shape only -- so a head's
+                            * output is BITWISE the same for every world size P
+                            * with (heads / P) % k == 0 (e.g.
+                            * k = 5 at H = 40 for P in {1, 2, 4, 8}).  The cost is
+                            * measured in DESIGN.md Sec 7.                       */
 } tm_config;
 
 typedef struct tm_ctx tm_ctx;
 
 /* Version of the ABI (major * 100 + minor). */
-int32_t tm_version(void);   /* 101: tm_config.transport, peer transport, tm_reference_attention */
+int32_t tm_version(void);   /* 102: tm_config.sched_heads, one-launch window / audio, loopback NCCL groups */
 
 /* Thread-local message for the last non-OK status returned on this thread. */
 const char* tm_last_error(void);
@@ -200,7 +210,10 @@ tm_status tm_reference_attention(tm_ctx* ctx, int32_t layer, int32_t step, const
  * keys of chunks {0, c-1, c} as a set (chunk 0 attends itself only).
  * No cache is read or written; B, H, d, dtype and the scale come from ctx
  * (world_size must be 1, else TM_ERR_UNSUPPORTED).  An empty chunk returns
- * TM_ERR_DEGENERATE_MASK.  One kernel launch per chunk. */
+ * TM_ERR_DEGENERATE_MASK.  bf16: ONE attention launch for up to 16
+ * chunks (each chunk's units scheduled exactly as a tm_chunk_attention call
+ * over the same segments would schedule them, so chunk c's rows equal that
+ * call's output bit for bit); fp32 mode: one launch per chunk. */
 tm_status tm_window_attention(tm_ctx* ctx, const void* q, const void* k, const void* v, void* o,
                               const int64_t* chunk_len, int32_t n_chunks, void* stream);
 
@@ -216,9 +229,12 @@ tm_status tm_window_attention(tm_ctx* ctx, const void* q, const void* k, const v
  *   window: odd, <= 5; frames outside [0, frames) are clamped by repeating the
  *   boundary frame (SPEC S:117 design decision; frame 0 -> {0,0,0,1,2}).
  *   scratch: device, >= tm_audio_scratch_bytes(ctx, frames, n_face), 1024-B
- *   aligned (gathered face rows of q and o).
+ *   aligned (gathered face rows of q; fp32 mode also of o).
  * n_face == 0 -> TM_ERR_DEGENERATE_MASK.  B, H, d, dtype, scale from
- * ctx (world_size 1).  Launches: gather, one attention per frame, scatter. */
+ * ctx (world_size 1).  bf16 launches: one prep kernel (gathers the face rows
+ * of q, zeroes the non-face rows of o) and ONE attention launch for up to 16
+ * frames whose epilogue writes each face row to o directly; T <= 49152.
+ * fp32 mode: gather, one attention per frame, zero, scatter. */
 size_t tm_audio_scratch_bytes(const tm_ctx* ctx, int64_t frames, int64_t n_face);
 tm_status tm_audio_cross_attention(tm_ctx* ctx, const void* q, const void* k_audio,
                                    const void* v_audio, void* o, int64_t frames,

@@ -77,6 +77,9 @@ tm_status validate(const tm_config* c) {
     if (c->transport != TM_TRANSPORT_NCCL && c->transport != TM_TRANSPORT_PEER)
         return fail(TM_ERR_INVALID_ARG, "transport %d not in {TM_TRANSPORT_NCCL, TM_TRANSPORT_PEER}",
                     c->transport);
+    if (c->sched_heads < 0 || (c->sched_heads > 0 && (c->heads / c->world_size) % c->sched_heads))
+        return fail(TM_ERR_SHAPE, "sched_heads %d must be 0 or divide the %d heads per rank",
+                    c->sched_heads, c->heads / c->world_size);
     if (c->transport == TM_TRANSPORT_PEER) {
         if (c->dtype != TM_BF16)
             return fail(TM_ERR_UNSUPPORTED, "TM_TRANSPORT_PEER is bf16 only (the fp32 validation "
@@ -437,7 +440,7 @@ PFN_getAddressRange address_range_fn() {
 
 extern "C" {
 
-int32_t tm_version(void) { return 101; }
+int32_t tm_version(void) { return 102; }
 
 const char* tm_last_error(void) { return g_err.c_str(); }
 
@@ -731,6 +734,7 @@ tm_status tm_chunk_attention_phases(tm_ctx* ctx, int32_t layer, int32_t step, in
             pr.H = Ly.Hl;
             pr.d = cf.head_dim;
             pr.scale = ctx->scale;
+            pr.sched_heads = ctx->cfg.sched_heads;
             pr.seg[pr.nseg++] = Segment{ctx->kref(layer, step), ctx->vref(layer, step), Ly.Lr};
             if (chunk >= 2)
                 pr.seg[pr.nseg++] = Segment{ctx->kslot(layer, step, chunk - 1),
@@ -838,6 +842,7 @@ tm_status tm_chunk_attention_phases(tm_ctx* ctx, int32_t layer, int32_t step, in
     pr.H = Ly.Hl;
     pr.d = cf.head_dim;
     pr.scale = ctx->scale;
+    pr.sched_heads = ctx->cfg.sched_heads;
     pr.seg[pr.nseg++] = Segment{ctx->kref(layer, step), ctx->vref(layer, step), Ly.Lr};
     if (chunk >= 2)
         pr.seg[pr.nseg++] = Segment{ctx->kslot(layer, step, chunk - 1),
@@ -922,6 +927,7 @@ tm_status tm_reference_attention(tm_ctx* ctx, int32_t layer, int32_t step, const
     pr.H = Ly.Hl;
     pr.d = cf.head_dim;
     pr.scale = ctx->scale;
+    pr.sched_heads = ctx->cfg.sched_heads;
     pr.seg[pr.nseg++] = Segment{k, v, Ly.Lr};
     cudaError_t e;
     if (cf.dtype == TM_BF16) {
@@ -975,7 +981,49 @@ tm_status tm_window_attention(tm_ctx* ctx, const void* q, const void* k, const v
     ctx->launches = 0;
     // a4 per query chunk c: key chunks {0, c-1, c} as a set (P:137-143, S:271:
     // chunk 0 attends itself only), each a token sub-range of the window.
-    for (int c = 0; c < n_chunks; ++c) {
+    auto key_chunks = [](int c, int* kc) {
+        int nk = 0;
+        kc[nk++] = 0;
+        if (c - 1 > 0) kc[nk++] = c - 1;
+        if (c > 0) kc[nk++] = c;
+        return nk;
+    };
+    if (cf.dtype == TM_BF16) {
+        // bf16: the query chunks are problems of ONE launch (up to kMaxProblems
+        // per launch; each chunk's units scheduled as in its own call).
+        for (int c0 = 0; c0 < n_chunks; c0 += kMaxProblems) {
+            MultiProblem mp;
+            mp.q = q;
+            mp.k = k;
+            mp.v = v;
+            mp.o = o;
+            mp.q_rows = mp.kv_rows = mp.o_rows = L;
+            mp.B = cf.batch;
+            mp.H = cf.heads;
+            mp.d = cf.head_dim;
+            mp.scale = ctx->scale;
+            mp.sched_heads = cf.sched_heads;
+            mp.nprob = std::min<int>(kMaxProblems, n_chunks - c0);
+            for (int i = 0; i < mp.nprob; ++i) {
+                const int c = c0 + i;
+                SubProblem& sp = mp.prob[i];
+                sp.q_row0 = sp.o_row0 = start[c];
+                sp.Lq = chunk_len[c];
+                int kc[3];
+                sp.nseg = key_chunks(c, kc);
+                for (int j = 0; j < sp.nseg; ++j) {
+                    sp.seg_row0[j] = start[kc[j]];
+                    sp.seg_len[j] = chunk_len[kc[j]];
+                }
+            }
+            tm_status st = cuda_check(launch_fmha_sm100_multi(mp, ctx->scratch(), cs, &ctx->launches),
+                                      "window attention launch");
+            if (st) return st;
+        }
+        return debug_check(ctx, o, int64_t(cf.batch) * L * cf.heads * cf.head_dim, 1, cs,
+                           "tm_window_attention");
+    }
+    for (int c = 0; c < n_chunks; ++c) {      // fp32 validation mode: one launch per chunk
         AttnProblem pr;
         pr.q = qb + start[c] * row;
         pr.o = ob + start[c] * row;
@@ -985,16 +1033,12 @@ tm_status tm_window_attention(tm_ctx* ctx, const void* q, const void* k, const v
         pr.H = cf.heads;
         pr.d = cf.head_dim;
         pr.scale = ctx->scale;
-        int kc[3], nk = 0;
-        kc[nk++] = 0;
-        if (c - 1 > 0) kc[nk++] = c - 1;
-        if (c > 0) kc[nk++] = c;
+        int kc[3];
+        const int nk = key_chunks(c, kc);
         for (int i = 0; i < nk; ++i)
             pr.seg[pr.nseg++] = Segment{kb + start[kc[i]] * row, vb + start[kc[i]] * row,
                                         chunk_len[kc[i]], L};
-        const cudaError_t e = cf.dtype == TM_BF16
-                                  ? launch_fmha_sm100(pr, ctx->scratch(), cs, &ctx->launches)
-                                  : launch_fmha_fp32(pr, cs, &ctx->launches);
+        const cudaError_t e = launch_fmha_fp32(pr, cs, &ctx->launches);
         tm_status st = cuda_check(e, "window attention launch");
         if (st) return st;
     }
@@ -1024,6 +1068,9 @@ tm_status tm_audio_cross_attention(tm_ctx* ctx, const void* q, const void* k_aud
     if (n_face <= 0 || !face_ids)
         return fail(TM_ERR_DEGENERATE_MASK, "empty face mask: no query attends the audio (S:124)");
     if (n_face > tokens_per_frame) return fail(TM_ERR_SHAPE, "more face tokens than frame tokens");
+    if (ctx->cfg.dtype == TM_BF16 && tokens_per_frame > 49152)
+        return fail(TM_ERR_UNSUPPORTED, "tokens_per_frame %lld > 49152 (face map in shared memory)",
+                    (long long)tokens_per_frame);
     if (window <= 0 || window % 2 == 0) return fail(TM_ERR_INVALID_ARG, "window must be odd, got %d", window);
     if (window > kMaxSegments)
         return fail(TM_ERR_UNSUPPORTED, "window %d > %d: an edge window needs more segments",
@@ -1040,19 +1087,73 @@ tm_status tm_audio_cross_attention(tm_ctx* ctx, const void* q, const void* k_aud
     uint8_t* of = qf + tm_audio_scratch_bytes(ctx, frames, n_face) / 2;   // 1024-B aligned half
     cudaStream_t cs = static_cast<cudaStream_t>(stream);
     ctx->launches = 0;
-    tm_status st = cuda_check(launch_face_rows(q, qf, face_ids, BF, tokens_per_frame, n_face, row, 0,
-                                               cs, &ctx->launches), "face gather");
-    if (st) return st;
     const uint8_t* kb = static_cast<const uint8_t*>(k_audio);
     const uint8_t* vb = static_cast<const uint8_t*>(v_audio);
-    for (int64_t f = 0; f < frames; ++f) {
-        // P:125 window, edges clamped by repetition, as runs of
-        // consecutive frames = contiguous audio-token segments (<= W of them).
+    // P:125 window of frame f, edges clamped by repetition, as runs
+    // of consecutive frames = contiguous audio-token row ranges (<= W of them).
+    auto window_runs = [&](int64_t f, int64_t* row0, int64_t* len) {
         int64_t win[kMaxSegments];
         for (int i = 0; i < window; ++i) {
-            int64_t g = f - window / 2 + i;
+            const int64_t g = f - window / 2 + i;
             win[i] = g < 0 ? 0 : (g > frames - 1 ? frames - 1 : g);
         }
+        int n = 0, i = 0;
+        while (i < window) {
+            int j = i;
+            while (j + 1 < window && win[j + 1] == win[j] + 1) ++j;
+            row0[n] = win[i] * audio_tokens_per_frame;
+            len[n] = (j - i + 1) * audio_tokens_per_frame;
+            ++n;
+            i = j + 1;
+        }
+        return n;
+    };
+    tm_status st;
+    if (cf.dtype == TM_BF16) {
+        // Two kinds of launch: (1) gather the face rows of q into scratch and
+        // zero the non-face rows of o (they get no audio update);
+        // (2) every frame's face rows attend its audio window as problems of
+        // ONE attention launch (up to kMaxProblems frames per launch) whose
+        // epilogue writes each face row straight to its token row of o.
+        st = cuda_check(launch_audio_prep(q, qf, o, face_ids, BF, tokens_per_frame, n_face, row, cs,
+                                          &ctx->launches), "audio prep (face gather, zero fill)");
+        if (st) return st;
+        for (int64_t f0 = 0; f0 < frames; f0 += kMaxProblems) {
+            MultiProblem mp;
+            mp.q = qf;
+            mp.k = k_audio;
+            mp.v = v_audio;
+            mp.o = o;
+            mp.q_rows = frames * n_face;
+            mp.kv_rows = frames * audio_tokens_per_frame;
+            mp.o_rows = frames * tokens_per_frame;
+            mp.o_row_map = face_ids;
+            mp.B = cf.batch;
+            mp.H = cf.heads;
+            mp.d = cf.head_dim;
+            mp.scale = ctx->scale;
+            mp.sched_heads = cf.sched_heads;
+            mp.nprob = int(std::min<int64_t>(kMaxProblems, frames - f0));
+            for (int i = 0; i < mp.nprob; ++i) {
+                const int64_t f = f0 + i;
+                SubProblem& sp = mp.prob[i];
+                sp.q_row0 = f * n_face;
+                sp.Lq = n_face;
+                sp.o_row0 = f * tokens_per_frame;
+                sp.nseg = window_runs(f, sp.seg_row0, sp.seg_len);
+            }
+            st = cuda_check(launch_fmha_sm100_multi(mp, ctx->scratch(), cs, &ctx->launches),
+                            "audio cross-attention launch");
+            if (st) return st;
+        }
+        return debug_check(ctx, o, BF * tokens_per_frame * cf.heads * cf.head_dim, 1, cs,
+                           "tm_audio_cross_attention");
+    }
+    // fp32 validation mode: gather, one attention launch per frame, zero, scatter
+    st = cuda_check(launch_face_rows(q, qf, face_ids, BF, tokens_per_frame, n_face, row, 0, cs,
+                                     &ctx->launches), "face gather");
+    if (st) return st;
+    for (int64_t f = 0; f < frames; ++f) {
         AttnProblem pr;
         pr.q = qf + f * n_face * row;
         pr.o = of + f * n_face * row;
@@ -1062,23 +1163,14 @@ tm_status tm_audio_cross_attention(tm_ctx* ctx, const void* q, const void* k_aud
         pr.H = cf.heads;
         pr.d = cf.head_dim;
         pr.scale = ctx->scale;
-        int i = 0;
-        while (i < window) {
-            int j = i;
-            while (j + 1 < window && win[j + 1] == win[j] + 1) ++j;
-            const int64_t tok0 = win[i] * audio_tokens_per_frame;
-            pr.seg[pr.nseg++] = Segment{kb + tok0 * row, vb + tok0 * row,
-                                        (j - i + 1) * audio_tokens_per_frame,
+        int64_t row0[kMaxSegments], len[kMaxSegments];
+        const int nseg = window_runs(f, row0, len);
+        for (int i = 0; i < nseg; ++i)
+            pr.seg[pr.nseg++] = Segment{kb + row0[i] * row, vb + row0[i] * row, len[i],
                                         frames * audio_tokens_per_frame};
-            i = j + 1;
-        }
-        const cudaError_t e = cf.dtype == TM_BF16
-                                  ? launch_fmha_sm100(pr, ctx->scratch(), cs, &ctx->launches)
-                                  : launch_fmha_fp32(pr, cs, &ctx->launches);
-        st = cuda_check(e, "audio cross-attention launch");
+        st = cuda_check(launch_fmha_fp32(pr, cs, &ctx->launches), "audio cross-attention launch");
         if (st) return st;
     }
-    // non-face rows get no update: zero, then scatter the face rows
     st = cuda_check(cudaMemsetAsync(o, 0, size_t(BF) * tokens_per_frame * row, cs), "zero output");
     if (st) return st;
     st = cuda_check(launch_face_rows(of, o, face_ids, BF, tokens_per_frame, n_face, row, 1, cs,

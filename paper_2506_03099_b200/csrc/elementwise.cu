@@ -210,6 +210,38 @@ __global__ void __launch_bounds__(256) face_rows_kernel(const uint4* __restrict_
     }
 }
 
+// f4 preparation (one pass over every token row of q / o, rows of W 16-byte
+// words): face rows of q are gathered, qf[bf][i] = q[bf][ids[i]], and the
+// non-face rows of o are zeroed (they receive no audio update);
+// the attention launch then writes the face rows of o itself (its epilogue
+// scatters through ids).  Each CTA builds the inverse map token -> face slot
+// in shared memory (T ints; ids outside [0, T) are ignored).
+__global__ void __launch_bounds__(256) audio_prep_kernel(const uint4* __restrict__ q,
+                                                         uint4* __restrict__ qf,
+                                                         uint4* __restrict__ o,
+                                                         const int32_t* __restrict__ ids,
+                                                         int64_t BF, int T, int nf, int W) {
+    extern __shared__ int inv[];
+    for (int t = threadIdx.x; t < T; t += blockDim.x) inv[t] = -1;
+    __syncthreads();
+    for (int i = threadIdx.x; i < nf; i += blockDim.x) {
+        const int t = ids[i];
+        if (t >= 0 && t < T) inv[t] = i;      // duplicates: any one slot (same row, same output)
+    }
+    __syncthreads();
+    const int64_t total = BF * T * W;
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < total; idx += stride) {
+        const int w = int(idx % W);
+        const int64_t r = idx / W;
+        const int t = int(r % T);
+        const int64_t bf = r / T;
+        const int i = inv[t];
+        if (i >= 0) qf[(bf * nf + i) * W + w] = __ldcs(q + idx);
+        else o[idx] = make_uint4(0, 0, 0, 0);
+    }
+}
+
 // ------------------------------------------------------------------ finiteness
 template <bool kBf16>
 __global__ void nonfinite_kernel(const void* __restrict__ x, int64_t n, int* flag) {
@@ -292,6 +324,23 @@ cudaError_t launch_face_rows(const void* src, void* dst, const int32_t* ids, int
     else
         face_rows_kernel<false><<<grid, 256, 0, s>>>(static_cast<const uint4*>(src),
                                                      static_cast<uint4*>(dst), ids, BF, T, nf, W);
+    if (launches) ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_audio_prep(const void* q, void* qf, void* o, const int32_t* ids, int64_t BF,
+                              int64_t T, int64_t nf, int row_bytes, cudaStream_t s, int* launches) {
+    if (row_bytes % 16 || T <= 0 || T > 49152 || nf <= 0) return cudaErrorInvalidValue;
+    const int W = row_bytes / 16;
+    const size_t smem = size_t(T) * 4;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(audio_prep_kernel,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (e != cudaSuccess) return e;
+    }
+    const unsigned grid = grid_for(BF * T * W, 256, 8);
+    audio_prep_kernel<<<grid, 256, smem, s>>>(static_cast<const uint4*>(q), static_cast<uint4*>(qf),
+                                              static_cast<uint4*>(o), ids, BF, int(T), int(nf), W);
     if (launches) ++*launches;
     return cudaGetLastError();
 }

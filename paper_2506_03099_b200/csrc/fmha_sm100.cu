@@ -91,17 +91,66 @@ constexpr float kLazyLog2 = 8.f;
 // latest (about 3 tiles of compute after Q arrived; the pushes have drained).
 constexpr int kKvReleaseLoads = 6;
 
-struct __align__(64) FmhaParams {
-    CUtensorMap tq;                   // Q [B][Lq][H][d]
-    CUtensorMap tk[kMaxSegments];     // K segments [B][len][H][d]
-    CUtensorMap tv[kMaxSegments];     // V segments
-    CUtensorMap tk_store, tv_store;   // a3: cache slot that the current segment is copied to
-    int store_seg;                    // segment whose tiles are appended to the slot (-1: none)
+// One attention problem of a launch: a range of query rows and its KV
+// segments (row a4).  A launch holds one problem (a chunk call: segments
+// c_0, c_{t-1}, c_t, each its own tensor map) or several sharing one Q, one
+// K/V and one O tensor (the f1 full window: query chunk c over key chunks
+// {0, c-1, c} as row ranges of the window; f4 audio: a frame's face rows
+// over its clamped window of audio frames).
+struct Prob {
+    int q_row0;                       // first query row in the Q map
+    int Lq;                           // query rows
+    int o_row0;                       // first output row in O (before o_row_map)
+    int o_clip;                       // 1: row o_row0 + Lq is O's end (a TMA store may clip there)
+    int n_qpairs;                     // Q-tile pairs per (b, h)
+    int n_tiles;                      // KV tiles of a unit
+    int nseg;
     int seg_tile_start[kMaxSegments + 1];
     int seg_len[kMaxSegments];
-    int nseg;
-    int n_tiles;                      // KV tiles of a whole unit
-    int Lq, H, B;
+    int seg_row0[kMaxSegments];       // first key row of the segment in its map
+    int seg_map[kMaxSegments];        // tensor map (tk / tv index) of the segment
+};
+
+// SCHEDULE BLOCKS.  A launch runs a sequence of blocks; block = (problem,
+// head range), scheduled exactly as if it were launched alone: its units
+// (b, h, pair of Q tiles) over the C persistent CTAs, R whole rounds (unit
+// c + k*C) then the T = U - R*C tail units' KV tiles in contiguous ranges
+// (stream-K, bounds of its class).  CTA c runs its items of block 0, then of
+// block 1, ...  So a block's arithmetic -- which units are split where and
+// merged in which order -- depends only on the block's own shape, never on
+// the other blocks of the launch: the f1 window's chunk c equals a streaming
+// call over the same segments bit for bit, and with schedule blocks
+// of a fixed head count (tm_config.sched_heads) a head's output is bitwise
+// the same for every world size.
+struct Block {
+    int pr;                           // problem
+    int h0, nh;                       // heads [h0, h0 + nh)
+    int rounds;                       // R: whole rounds
+    int cls;                          // stream-K class of the tail
+    int tail0;                        // first tail unit (R * C)
+    int off;                          // the block's CTA c runs on CTA (c + off) mod C: consecutive
+                                      // blocks' tails start where the previous tail ended
+};
+struct SkClass {
+    int ctas;                         // G': CTAs with a tail range
+    int bound[kMaxPersistentCtas + 1];   // CTA c takes tail tiles [bound[c], bound[c+1])
+};
+
+struct __align__(64) FmhaParams {
+    CUtensorMap tq;                   // Q [B][L][H][d]
+    CUtensorMap tk[kMaxSegments];     // K maps [B][len][H][d]
+    CUtensorMap tv[kMaxSegments];     // V maps
+    CUtensorMap tk_store, tv_store;   // a3: cache slot that the current segment is copied to
+    int store_seg;                    // segment whose tiles are appended to the slot (-1: none; one problem only)
+    int nmaps;                        // tk / tv maps in use
+    int nprob;
+    Prob prob[kMaxProblems];
+    int nblk, ncls;
+    Block blk[kMaxBlocks];
+    SkClass cls[kMaxSkClasses];
+    int cls_key[kMaxSkClasses][2];    // host bookkeeping: (T, n) of each class
+    const int* o_row_map;             // nullable: output row of problem-local query q is o_row0 + map[q]
+    int H, B;
     float scale_log2;                 // softmax scale * log2(e)
     // Output rows (a6 scatter): query row q is stored to o_dst[q / o_rows], row
     // q % o_rows, heads [o_h0, o_h0 + H) of o_H; P = 1: o_dst[0] = o, o_rows = Lq.
@@ -120,14 +169,10 @@ struct __align__(64) FmhaParams {
     PeerCounters* done_ctr[kMaxPeers];
     PeerPush pp;
     // persistent schedule
-    int n_qpairs;                     // Q-tile pairs per (b, h)
-    int rounds;                       // R: whole units per CTA (unit c + k*C, k < R)
+    int ctas;                         // C: persistent CTAs the blocks are scheduled over
     int l2_prefetch;                  // K/V tiles of the first item prefetched into L2 (with its Q) before the PDL wait
-    int sk_units;                     // T = U - R*C tail units, spread stream-K style ...
-    int sk_ctas;                      // ... over the first G' CTAs (contiguous tile ranges):
-    int sk_bound[kMaxPersistentCtas + 1];   // CTA c takes tail tiles [sk_bound[c], sk_bound[c+1])
-    float* part;                      // piece partials: per slot [d/4][256] float4 + m[256] + l[256]
-    int* counters;                    // per split unit (indexed by its first CTA), zero between launches
+    float* part;                      // piece partials: per (block, CTA) slot [d/4][256] float4 + m[256] + l[256]
+    int* counters;                    // per (block, first CTA of a split unit), zero between launches
     unsigned long long* trace;        // debug timeline (TM_TRACE=1), CTA 0 only; may be null
 };
 
@@ -159,17 +204,18 @@ __device__ __forceinline__ void trace_span(const FmhaParams& p, int j, long long
 }
 
 struct Item {
-    int b, h, qp, lo, hi, piece;
+    int pr, blk, b, h, qp, lo, hi, piece;
     int cfirst, npieces, pidx;        // split units: first CTA, piece count, this piece's index
+    int cl;                           // this CTA's index within the block (blockIdx.x - off mod C)
 };
 
 // Tail (stream-K) CTA holding tile x of the flattened tail space: the c with
 // sk_bound[c] <= x < sk_bound[c+1] (ranges are non-empty; binary search).
-__device__ __forceinline__ int sk_cta_of(const FmhaParams& p, int x) {
-    int lo = 0, hi = p.sk_ctas - 1;
+__device__ __forceinline__ int sk_cta_of(const SkClass& k, int x) {
+    int lo = 0, hi = k.ctas - 1;
     while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
-        if (p.sk_bound[mid] <= x) lo = mid;
+        if (k.bound[mid] <= x) lo = mid;
         else hi = mid - 1;
     }
     return lo;
@@ -178,54 +224,80 @@ __device__ __forceinline__ int sk_cta_of(const FmhaParams& p, int x) {
 // 0 is CTA cf's LAST item and merges; piece k >= 1 is CTA cf+k's FIRST item and
 // leaves its partial in slot cf + k (one partial slot per CTA suffices).
 
-// Item k of this CTA: first its R whole units c, c+C, ...; then its range of
-// the tail's tiles (stream-K: each of the first G' CTAs takes a contiguous
-// range of the T tail units' KV tiles, sized on the host so that tiles plus a
-// per-item cost are equal (fmha_sm100 launcher); a unit cut by range ends
-// becomes pieces, merged by piece 0).
-__device__ __forceinline__ bool get_item(const FmhaParams& p, int k, Item& it) {
+// Item k of this CTA within block bi: first its R whole units c, c+C, ...;
+// then its range of the block's tail tiles (stream-K: each of the first G'
+// CTAs takes a contiguous range of the T tail units' KV tiles, sized on the
+// host so that tiles plus a per-item cost are equal (tail_bounds); a unit cut
+// by range ends becomes pieces, merged by piece 0).
+__device__ __forceinline__ bool get_item(const FmhaParams& p, int bi, int k, Item& it) {
+    const Block& B = p.blk[bi];
+    const Prob& P = p.prob[B.pr];
+    const int c = B.off ? (int(blockIdx.x) + p.ctas - B.off) % p.ctas : int(blockIdx.x);
+    const int n = P.n_tiles;
     int unit;
-    const int c = blockIdx.x;
+    it.pr = B.pr;
+    it.blk = bi;
+    it.cl = c;
     it.cfirst = 0;
     it.npieces = 1;
     it.pidx = 0;
-    if (k < p.rounds) {
-        unit = c + k * int(gridDim.x);
+    if (k < B.rounds) {
+        unit = c + k * p.ctas;
         it.lo = 0;
-        it.hi = p.n_tiles;
+        it.hi = n;
         it.piece = 0;
     } else {
-        if (c >= p.sk_ctas) return false;
-        const int n = p.n_tiles;
-        const int start = p.sk_bound[c], end = p.sk_bound[c + 1];
-        const int u = start / n + (k - p.rounds);
+        if (B.cls < 0) return false;
+        const SkClass& K = p.cls[B.cls];
+        if (c >= K.ctas) return false;
+        const int start = K.bound[c], end = K.bound[c + 1];
+        const int u = start / n + (k - B.rounds);
         const int ub = u * n;
         if (start >= end || ub >= end) return false;
         it.lo = (start > ub ? start : ub) - ub;
         it.hi = (end < ub + n ? end : ub + n) - ub;
         it.piece = it.lo > 0 || it.hi < n;
         if (it.piece) {
-            it.cfirst = sk_cta_of(p, ub);
-            it.npieces = sk_cta_of(p, ub + n - 1) - it.cfirst + 1;
+            it.cfirst = sk_cta_of(K, ub);
+            it.npieces = sk_cta_of(K, ub + n - 1) - it.cfirst + 1;
             it.pidx = c - it.cfirst;
         }
-        unit = p.rounds * int(gridDim.x) + int(u);
+        unit = B.tail0 + u;
     }
-    it.qp = unit % p.n_qpairs;
-    const int bh = unit / p.n_qpairs;
-    it.h = bh % p.H;
-    it.b = bh / p.H;
+    it.qp = unit % P.n_qpairs;
+    const int bh = unit / P.n_qpairs;
+    it.h = B.h0 + bh % B.nh;
+    it.b = bh / B.nh;
     return true;
 }
 
-__device__ __forceinline__ void tile_info(const FmhaParams& p, int j, int& seg, int& row,
+// Every role walks the same item sequence: block by block, each block's items.
+struct Cursor {
+    int bi = 0, k = 0;
+};
+__device__ __forceinline__ bool next_item(const FmhaParams& p, Cursor& cu, Item& it) {
+    while (cu.bi < p.nblk) {
+        if (get_item(p, cu.bi, cu.k, it)) {
+            ++cu.k;
+            return true;
+        }
+        ++cu.bi;
+        cu.k = 0;
+    }
+    return false;
+}
+
+// KV tile j of a unit of problem `pr`: its segment, first key row within the
+// segment, valid keys (ragged tail masked), and the row in the segment's map.
+__device__ __forceinline__ void tile_info(const FmhaParams& p, int pr, int j, int& seg, int& row,
                                           int& valid) {
+    const Prob& P = p.prob[pr];
     seg = 0;
 #pragma unroll
     for (int s = 1; s < kMaxSegments; ++s)
-        if (s < p.nseg && j >= p.seg_tile_start[s]) seg = s;
-    row = (j - p.seg_tile_start[seg]) * kBN;
-    valid = min(kBN, p.seg_len[seg] - row);
+        if (s < P.nseg && j >= P.seg_tile_start[s]) seg = s;
+    row = (j - P.seg_tile_start[seg]) * kBN;
+    valid = min(kBN, P.seg_len[seg] - row);
 }
 
 // Position q (0..2n-1) of an item's K/V load sequence K0, K1, V0, K2, V1, ...,
@@ -240,16 +312,18 @@ __device__ __forceinline__ void load_order(int q, int nkv, int& jj, int& kv) {
 // cache slot by exactly one item of its (b, h): the unit with qp == tile % n_qpairs
 // (or the piece of that unit whose KV range holds it).
 __device__ __forceinline__ bool stores_tile(const FmhaParams& p, const Item& it, int seg, int row) {
-    return seg == p.store_seg && (row / kBN) % p.n_qpairs == it.qp;
+    return seg == p.store_seg && (row / kBN) % p.prob[it.pr].n_qpairs == it.qp;
 }
 
 // Destination of output row q of head h (row a6: the owner's O window when the
 // path is Ulysses-sharded over peer memory, else o itself); null for pad rows.
 template <int D>
-__device__ __forceinline__ uint16_t* out_row(const FmhaParams& p, int b, int q, int h) {
-    if (q >= p.Lq) return nullptr;
-    if (p.o_rows >= p.Lq)     // one owner (P = 1): no division
-        return p.o_dst[0] + ((int64_t(b) * p.o_bstride + q) * p.o_H + p.o_h0 + h) * D;
+__device__ __forceinline__ uint16_t* out_row(const FmhaParams& p, const Prob& P, int b, int q, int h) {
+    if (q >= P.Lq) return nullptr;
+    if (p.o_rows >= P.Lq) {   // one owner (P = 1): no division
+        const int row = P.o_row0 + (p.o_row_map ? p.o_row_map[q] : q);
+        return p.o_dst[0] + ((int64_t(b) * p.o_bstride + row) * p.o_H + p.o_h0 + h) * D;
+    }
     int own;
     const int64_t row = peer_out_route(b, q, h, p.o_rows, p.o_bstride, p.o_H, p.o_h0, own);
     return p.o_dst[own] + row * D;
@@ -261,9 +335,13 @@ __device__ __forceinline__ uint16_t* out_row(const FmhaParams& p, int b, int q, 
 // columns, 16-B chunks XOR-swizzled by row: conflict-free both ways) each
 // store instruction writes 4 rows x 128 B instead of 32 rows x 16 B.
 template <int D>
-__device__ __forceinline__ void store_rows_bf16(const FmhaParams& p, uint32_t tsrc, float scale,
-                                                uint8_t* stg, int b, int q0, int h, int lane) {
-    if (p.tma_epi) {
+__device__ __forceinline__ void store_rows_bf16(const FmhaParams& p, const Prob& P, uint32_t tsrc,
+                                                float scale, uint8_t* stg, int b, int q0, int h,
+                                                int lane) {
+    // TMA store of the warp's 32 rows when they are contiguous in O and either
+    // all inside the problem or clipped by O's end (a window's inner problems
+    // must not spill into the next problem's rows).
+    if (p.tma_epi && (q0 + 32 <= P.Lq || P.o_clip)) {
         // One owner: the swizzled staging tile is exactly a 128B-swizzled TMA box
         // (32 rows x 64 columns), so lane 0 stores it asynchronously (rows past
         // Lq clipped) and the warp moves on; the buffer is reused only after the
@@ -288,7 +366,7 @@ __device__ __forceinline__ void store_rows_bf16(const FmhaParams& p, uint32_t ts
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
-                tma_store_4d(&p.to, stg, half * 64, h, q0, b);
+                tma_store_4d(&p.to, stg, half * 64, h, P.o_row0 + q0, b);
                 tma_store_commit();
             }
         }
@@ -300,7 +378,7 @@ __device__ __forceinline__ void store_rows_bf16(const FmhaParams& p, uint32_t ts
 #pragma unroll
     for (int t = 0; t < 8; ++t) {
         const int q = q0 + t * 4 + (lane >> 3);
-        dsts[t] = q < p.Lq ? out_row<D>(p, b, q, h) : nullptr;
+        dsts[t] = out_row<D>(p, P, b, q, h);
     }
 #pragma unroll 1
     for (int half = 0; half < D / 64; ++half) {
@@ -346,6 +424,13 @@ __device__ __forceinline__ void peer_ready(const FmhaParams& p, uint32_t& ok, in
         waited = true;
     }
     if (waited) fence_proxy_async_global();   // generic-proxy acquire -> TMA (async proxy) reads
+}
+
+// One merge step of an output element (stream-K pieces):
+// o <- o * wo + wk * x with explicit roundings (the product o * wo rounded,
+// then one FMA), so every code path gives the same bits.
+__device__ __forceinline__ uint32_t merge_elem(uint32_t o, float wo, float wk, float x) {
+    return __float_as_uint(__fmaf_rn(wk, x, __fmul_rn(__uint_as_float(o), wo)));
 }
 
 __device__ __forceinline__ float max3(float a, float b, float c) {
@@ -458,7 +543,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
     }
     if (warp == 8 && lane == 0) {
         tma_prefetch(&p.tq);
-        for (int s = 0; s < p.nseg; ++s) {
+        for (int s = 0; s < p.nmaps; ++s) {
             tma_prefetch(&p.tk[s]);
             tma_prefetch(&p.tv[s]);
         }
@@ -466,16 +551,20 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
         // previous grid drains (one-GPU problems; peer windows are filled by
         // other ranks during the launch).  TM_L2_PREFETCH=n: n K/V tiles (0: off).
         Item it0;
-        if (p.l2_prefetch && get_item(p, 0, it0)) {
+        Cursor cu0;
+        if (p.l2_prefetch && next_item(p, cu0, it0)) {
             for (int i = 0; i < 2; ++i)
                 for (int hf = 0; hf < D / 64; ++hf)
-                    tma_prefetch_l2_4d(&p.tq, hf * 64, it0.h, it0.qp * 2 * kBM + i * kBM, it0.b);
+                    tma_prefetch_l2_4d(&p.tq, hf * 64, it0.h,
+                                       p.prob[it0.pr].q_row0 + it0.qp * 2 * kBM + i * kBM, it0.b);
             for (int j = it0.lo; j < it0.hi && j < it0.lo + p.l2_prefetch; ++j) {
                 int seg, row, valid;
-                tile_info(p, j, seg, row, valid);
+                tile_info(p, it0.pr, j, seg, row, valid);
+                const Prob& P0 = p.prob[it0.pr];
+                const int m = P0.seg_map[seg], r = P0.seg_row0[seg] + row;
                 for (int hf = 0; hf < D / 64; ++hf) {
-                    tma_prefetch_l2_4d(&p.tk[seg], hf * 64, it0.h, row, it0.b);
-                    tma_prefetch_l2_4d(&p.tv[seg], hf * 64, it0.h, row, it0.b);
+                    tma_prefetch_l2_4d(&p.tk[m], hf * 64, it0.h, r, it0.b);
+                    tma_prefetch_l2_4d(&p.tv[m], hf * 64, it0.h, r, it0.b);
                 }
             }
         }
@@ -525,7 +614,8 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
 #endif
             int n_loads = 0;
             Item it;
-            for (int w = 0; get_item(p, w, it); ++w, ++n_item) {
+            Cursor cu;
+            for (; next_item(p, cu, it); ++n_item) {
                 // Load order Q_0, K_lo, Q_1, K_lo+1, V_lo, K_lo+2, V_lo+1, ..., V_hi-1:
                 // S_0(lo) needs only Q_0 and K_lo, and K runs one tile ahead of V,
                 // matching the MMA's use (S(j+1) before PV(j)).
@@ -535,20 +625,21 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                         const int i = step >> 1;
                         if (p.peer) {
                             const int r0 = it.qp * 2 * kBM + i * kBM;
-                            peer_ready(p, ok, 0, r0, min(kBM, p.Lq - r0));
+                            peer_ready(p, ok, 0, r0, min(kBM, p.prob[0].Lq - r0));
                         }
                         mbar_wait(&q_empty[i], (n_item & 1) ^ 1);
                         mbar_arrive_expect_tx(&q_full[i], kTileBytes);
                         for (int hf = 0; hf < D / 64; ++hf)
                             tma_load_4d(sQ + i * kTileBytes + hf * kHalfBytes, &p.tq, &q_full[i],
-                                        hf * 64, it.h, it.qp * 2 * kBM + i * kBM, it.b);
+                                        hf * 64, it.h,
+                                        p.prob[it.pr].q_row0 + it.qp * 2 * kBM + i * kBM, it.b);
                         continue;
                     }
                     const int q = step == 1 ? 0 : step - 2;
                     int jj, kv;
                     load_order(q, nkv, jj, kv);
                     int seg, row, valid;
-                    tile_info(p, it.lo + jj, seg, row, valid);
+                    tile_info(p, it.pr, it.lo + jj, seg, row, valid);
                     const int s = kv_it % kStages;
                     trace_ev(p, 0, tn, 3 + kv);
 #ifdef TM_SPANS_PROD
@@ -578,11 +669,13 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                     }
                     if (p.peer && seg == p.wait_seg) peer_ready(p, ok, 1 + kv, row, valid);
                     trace_ev(p, 0, tn, 1 + kv);
-                    const CUtensorMap* m = kv ? &p.tv[seg] : &p.tk[seg];
+                    const Prob& P = p.prob[it.pr];
+                    const int mi = P.seg_map[seg];
+                    const CUtensorMap* m = kv ? &p.tv[mi] : &p.tk[mi];
                     mbar_arrive_expect_tx(&kv_full[s], kTileBytes);
                     for (int hf = 0; hf < D / 64; ++hf)
                         tma_load_4d(sKV + s * kTileBytes + hf * kHalfBytes, m, &kv_full[s],
-                                    hf * 64, it.h, row, it.b);
+                                    hf * 64, it.h, P.seg_row0[seg] + row, it.b);
                     ++kv_it;
                 }
             }
@@ -603,7 +696,8 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
             int tn = 0;
             uint32_t g = 0;
             Item it;
-            for (int w = 0; get_item(p, w, it); ++w)
+            Cursor cu;
+            while (next_item(p, cu, it))
                 for (int j = it.lo; j < it.hi; ++j, ++g)
                     for (int i = 0; i < 2; ++i) {
                         mbar_wait(&s_full[i], g & 1);
@@ -617,13 +711,14 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
             uint32_t kv_it = 0;
             int tn = 0;
             Item it;
-            for (int w = 0; get_item(p, w, it); ++w) {
+            Cursor cu;
+            while (next_item(p, cu, it)) {
                 const int nkv = it.hi - it.lo;
                 for (int q = 0; q < 2 * nkv; ++q, ++kv_it) {
                     int jj, kv;
                     load_order(q, nkv, jj, kv);
                     int seg, row, valid;
-                    tile_info(p, it.lo + jj, seg, row, valid);
+                    tile_info(p, it.pr, it.lo + jj, seg, row, valid);
                     // Observe EVERY position's kv_full phase in order: waiting only on
                     // stored tiles could run two phases ahead on a slot (parity ABA).
                     const int s = kv_it % kStages;
@@ -660,7 +755,8 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
         uint32_t kv_it = 0, g = 0, n_item = 0, s_count = 0;
         int tn = 0;
         Item it;
-        for (int w = 0; get_item(p, w, it); ++w, ++n_item) {
+        Cursor cu;
+        for (; next_item(p, cu, it); ++n_item) {
             const int nkv = it.hi - it.lo;
             if (warp == 9) {
                 for (int j = 0; j < nkv; ++j) {
@@ -718,14 +814,15 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
         int tn = 0;
         const bool tr = (lane == 0);   // every softmax warp records (equal trace overhead)
         Item it;
-        for (int w = 0; get_item(p, w, it); ++w, ++n_item) {
+        Cursor cu;
+        for (; next_item(p, cu, it); ++n_item) {
 #ifndef TM_SPANS_MERGE
             if (threadIdx.x == 0 && n_item == 1) trace_span(p, 2);   // first item's epilogue done
 #endif
             float m_run = -INFINITY, l = 0.f;
             for (int j = it.lo; j < it.hi; ++j, ++g) {
                 int seg, row, valid;
-                tile_info(p, j, seg, row, valid);
+                tile_info(p, it.pr, j, seg, row, valid);
                 uint32_t r[kBN];
                 mbar_wait(&s_full[i], g & 1);
                 if (tr) trace_ev(p, 5 + warp, tn, 20);
@@ -845,7 +942,8 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
 #endif
             const int q = it.qp * 2 * kBM + row_in_pair;
             if (!it.piece) {
-                store_rows_bf16<D>(p, tOi, 1.f / l, sEpi + warp * 4096, it.b, q - lane, it.h, lane);
+                store_rows_bf16<D>(p, p.prob[it.pr], tOi, 1.f / l, sEpi + warp * 4096, it.b, q - lane,
+                                   it.h, lane);
 #ifdef TM_SPANS_MERGE
                 if (threadIdx.x == 0) trace_span(p, 5);
 #endif
@@ -856,7 +954,8 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                 // O, running max m (log2 units) and l to this CTA's partial slot,
                 // then count it in for the unit's merger (piece 0).
                 constexpr int kPieceFloats = 256 * D + 512;
-                float* base = p.part + size_t(blockIdx.x) * kPieceFloats;
+                // the slot of this piece's block-local CTA (where the merger looks)
+                float* base = p.part + (size_t(it.blk) * kMaxPersistentCtas + it.cl) * kPieceFloats;
                 float4* po = reinterpret_cast<float4*>(base);
 #pragma unroll
                 for (int c = 0; c < D; c += 32) {
@@ -876,18 +975,19 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                 softmax_bar();                // every thread's partial stores precede ...
                 if (threadIdx.x == 0) {       // ... this one fence (cumulative) and the count
                     __threadfence();
-                    atomicAdd(&p.counters[it.cfirst], 1);
+                    atomicAdd(&p.counters[it.blk * kMaxPersistentCtas + it.cfirst], 1);
                 }
             } else {
-                // piece 0 of a split unit = this CTA's LAST item (its range ends
-                // inside the unit), so O_i stays in TMEM: wait until the other
-                // pieces (first items of the next CTAs, long finished) are in,
-                // then merge them into the TMEM accumulator in piece order
-                // (deterministic) and store the output.  No partial of its own.
+                // piece 0 of a split unit = this CTA's LAST item of the block (its
+                // range ends inside the unit), so O_i stays in TMEM: wait until
+                // the other pieces (first tail items of the next CTAs, long
+                // finished) are in, then merge them into the TMEM accumulator in
+                // piece order (deterministic) and store the output.  No partial
+                // of its own.
                 constexpr int kPieceFloats = 256 * D + 512;
                 if (threadIdx.x == 0) trace_span(p, 4);
                 if (threadIdx.x == 0) {
-                    volatile int* ctr = p.counters + it.cfirst;
+                    volatile int* ctr = p.counters + it.blk * kMaxPersistentCtas + it.cfirst;
                     const long long t0 = clock64();
                     while (*ctr != it.npieces - 1)
                         if (clock64() - t0 > (1ll << 33)) __trap();
@@ -897,28 +997,36 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                 softmax_bar();
                 if (threadIdx.x == 0) trace_span(p, 5);
                 auto piece_base = [&](int k) {
-                    return p.part + size_t(it.cfirst + k) * kPieceFloats;
+                    return p.part + (size_t(it.blk) * kMaxPersistentCtas + it.cfirst + k) * kPieceFloats;
                 };
-                // This is the CTA's last item: no more Q or K/V loads, and once
-                // store_idle has completed no append store reads the ring.  The
-                // pieces' O partials are pulled in column halves (chunk j = piece
-                // 1 + j/2, half j%2) by bulk copies into three buffers over the Q
-                // tiles and the ring, three chunks in flight; each thread reads its
-                // row from shared memory (conflict-free [d/4][256] float4 layout)
-                // and accumulates into O_i in TMEM.  The weights need every piece's
-                // m and l first: loaded from global, up to 8 pieces per batch of
-                // independent loads, overlapping the first copies.
+                // If this is the CTA's last item overall: no more Q or K/V loads,
+                // and once store_idle has completed no append store reads the
+                // ring.  The pieces' O partials are then pulled in column halves
+                // (chunk j = piece 1 + j/2, half j%2) by bulk copies into three
+                // buffers over the Q tiles and the ring, three chunks in flight;
+                // each thread reads its row from shared memory (conflict-free
+                // [d/4][256] float4 layout) and accumulates into O_i in TMEM.
+                // Otherwise (a later schedule block follows, its loads already in
+                // flight) each thread loads its row of the partials from L2
+                // directly.  Both apply the same per-element update in the same
+                // piece order (merge_elem), so the result is the same bits.  The
+                // weights need every piece's m and l first: loaded from global,
+                // up to 8 pieces per batch of independent loads, overlapping the
+                // first copies.
                 constexpr uint32_t kChunkBytes = 256 * (D / 2) * 4;
                 static_assert(3 * kChunkBytes <= (2 + kStages) * kTileBytes,
                               "three merge buffers fit the Q tiles + the ring");
                 const int np = it.npieces;
                 const int nchunks = 2 * (np - 1);
+                Cursor cpeek = cu;
+                Item nx;
+                const bool smem_merge = !next_item(p, cpeek, nx);
                 auto issue_chunk = [&](int j) {
                     mbar_arrive_expect_tx(&merge_bar[j % 3], kChunkBytes);
                     bulk_g2s(smem + (j % 3) * kChunkBytes, piece_base(1 + j / 2) + (j & 1) * 128 * D,
                              kChunkBytes, &merge_bar[j % 3]);
                 };
-                if (threadIdx.x == 0) {
+                if (smem_merge && threadIdx.x == 0) {
                     mbar_wait(store_idle, 0);
                     fence_proxy_async_global();
                     for (int j = 0; j < 3 && j < nchunks; ++j) issue_chunk(j);
@@ -958,6 +1066,28 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                     const float m_nxt = k + 1 < np ? __ldcg(piece_base(k + 1) + 256 * D + row_in_pair) : 0.f;
                     const float wk = ex2(m_cur - mstar);
                     const float wo = k == 1 ? w0 : 1.f;
+                    if (!smem_merge) {
+                        const float4* gp = reinterpret_cast<const float4*>(piece_base(k));
+#pragma unroll 1
+                        for (int c = 0; c < D; c += 32) {
+                            uint32_t o[32];
+                            tmem_ld32(tOi + c, o);
+                            float4 x[8];
+#pragma unroll
+                            for (int e = 0; e < 8; ++e) x[e] = __ldcg(gp + ((c >> 2) + e) * 256 + row_in_pair);
+                            tmem_wait_ld();
+#pragma unroll
+                            for (int e = 0; e < 8; ++e) {
+                                o[4 * e] = merge_elem(o[4 * e], wo, wk, x[e].x);
+                                o[4 * e + 1] = merge_elem(o[4 * e + 1], wo, wk, x[e].y);
+                                o[4 * e + 2] = merge_elem(o[4 * e + 2], wo, wk, x[e].z);
+                                o[4 * e + 3] = merge_elem(o[4 * e + 3], wo, wk, x[e].w);
+                            }
+                            tmem_st32(tOi + c, o);
+                        }
+                        m_cur = m_nxt;
+                        continue;
+                    }
 #pragma unroll 1
                     for (int h = 0; h < 2; ++h) {
                         const int j = 2 * (k - 1) + h;
@@ -971,10 +1101,10 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
 #pragma unroll
                             for (int e = 0; e < 8; ++e) {
                                 const float4 x = sp[((c >> 2) + e) * 256 + row_in_pair];
-                                o[4 * e] = __float_as_uint(__uint_as_float(o[4 * e]) * wo + wk * x.x);
-                                o[4 * e + 1] = __float_as_uint(__uint_as_float(o[4 * e + 1]) * wo + wk * x.y);
-                                o[4 * e + 2] = __float_as_uint(__uint_as_float(o[4 * e + 2]) * wo + wk * x.z);
-                                o[4 * e + 3] = __float_as_uint(__uint_as_float(o[4 * e + 3]) * wo + wk * x.w);
+                                o[4 * e] = merge_elem(o[4 * e], wo, wk, x.x);
+                                o[4 * e + 1] = merge_elem(o[4 * e + 1], wo, wk, x.y);
+                                o[4 * e + 2] = merge_elem(o[4 * e + 2], wo, wk, x.z);
+                                o[4 * e + 3] = merge_elem(o[4 * e + 3], wo, wk, x.w);
                             }
                             tmem_st32(tOi + h * (D / 2) + c, o);
                         }
@@ -986,7 +1116,8 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                     m_cur = m_nxt;
                 }
                 tmem_wait_st();
-                store_rows_bf16<D>(p, tOi, inv, sEpi + warp * 4096, it.b, q - lane, it.h, lane);
+                store_rows_bf16<D>(p, p.prob[it.pr], tOi, inv, sEpi + warp * 4096, it.b, q - lane, it.h,
+                                   lane);
                 tc_fence_before();
                 mbar_arrive(&o_empty[i]);
             }
@@ -1109,15 +1240,17 @@ cudaError_t launch_d(const FmhaParams& p, int grid, cudaStream_t stream) {
 
 }  // namespace
 
-// Host: cut the tail's W = T*n tiles into at most C contiguous ranges whose
-// cost -- tiles plus kItemCost per item after a range's first -- is as equal
-// as possible (a CTA that switches to another unit pays its epilogue / partial
-// write, the next Q load and pipeline refill, and as the unit's merger the
-// partial reads: ~6 tiles' time measured, profiles/r1_v8_cta_spans.txt).  A
-// greedy fill under budget B, the smallest B (bisection) that needs <= C
-// ranges.  Pieces shorter than kMinPiece are not started at a range's end.
-// TM_SCHED_SPLIT=1 (A/B only): plain equal ranges.  Returns G'.
-int tail_bounds(int T, int n, int C, int min_piece, int* bound) {
+// Host: cut the tail's W tiles -- runs of units, run r holding units[r]
+// units of tiles[r] KV tiles each, flattened in order -- into at most C
+// contiguous ranges whose cost -- tiles plus kItemCost per item after a
+// range's first -- is as equal as possible (a CTA that switches to another
+// unit pays its epilogue / partial write, the next Q load and pipeline
+// refill, and as the unit's merger the partial reads: ~6 tiles' time
+// measured, profiles/r1_v8_cta_spans.txt).  A greedy fill under budget B, the
+// smallest B (bisection) that needs <= C ranges.  Pieces shorter than
+// kMinPiece are not started at a range's end.  TM_SCHED_SPLIT=1 (A/B only):
+// plain equal ranges.  Returns G'.
+int tail_bounds_runs(int nruns, const int* units, const int* tiles, int C, int min_piece, int* bound) {
     static const float item_cost = [] {
         const char* e = getenv("TM_SCHED_ITEM_COST");
         return e ? float(atof(e)) : 3.f;
@@ -1126,11 +1259,25 @@ int tail_bounds(int T, int n, int C, int min_piece, int* bound) {
         const char* e = getenv("TM_SCHED_SPLIT");
         return e && *e && strcmp(e, "0") != 0;
     }();
-    const int W = T * n;
+    std::vector<long long> run0(nruns + 1, 0);
+    long long T = 0;
+    for (int r = 0; r < nruns; ++r) {
+        run0[r + 1] = run0[r] + (long long)units[r] * tiles[r];
+        T += units[r];
+    }
+    const int W = int(run0[nruns]);
+    // end of the unit holding tile x
+    auto unit_end = [&](int x) -> int {
+        int r = 0;
+        while (r + 1 < nruns && run0[r + 1] <= x) ++r;
+        const long long off = x - run0[r];
+        return int(run0[r] + (off / tiles[r] + 1) * tiles[r]);
+    };
     int G = C;
     if (G > W / min_piece) G = W / min_piece;
-    if (G < T) G = T;
+    if (G < T) G = int(T < C ? T : C);
     if (G > C) G = C;
+    if (G < 1) G = 1;
     if (split_sched || item_cost <= 0.f) {
         for (int c = 0; c <= G; ++c) bound[c] = int((long long)c * W / G);
         return G;
@@ -1145,7 +1292,7 @@ int tail_bounds(int T, int n, int C, int min_piece, int* bound) {
             const int start = x;
             float cost = 0.f;
             while (x < W) {
-                const int ue = (x / n + 1) * n;
+                const int ue = unit_end(x);
                 const float extra = x > start ? item_cost : 0.f;
                 const float avail = B - cost - extra;
                 int take = int(avail);
@@ -1164,7 +1311,9 @@ int tail_bounds(int T, int n, int C, int min_piece, int* bound) {
         }
         return g;
     };
-    float lo = float(W) / G, hi = float(W) / G + item_cost * 4 + n;
+    int maxn = 1;
+    for (int r = 0; r < nruns; ++r) maxn = tiles[r] > maxn ? tiles[r] : maxn;
+    float lo = float(W) / G, hi = float(W) / G + item_cost * 4 + maxn;
     while (fill(hi, nullptr) > G) hi *= 2;
     for (int it = 0; it < 40; ++it) {
         const float mid = 0.5f * (lo + hi);
@@ -1172,6 +1321,10 @@ int tail_bounds(int T, int n, int C, int min_piece, int* bound) {
         else lo = mid;
     }
     return fill(hi, bound);
+}
+
+int tail_bounds(int T, int n, int C, int min_piece, int* bound) {
+    return tail_bounds_runs(1, &T, &n, C, min_piece, bound);
 }
 
 bool pdl_enabled() {
@@ -1183,25 +1336,157 @@ bool pdl_enabled() {
 }
 
 size_t fmha_sm100_scratch_bytes(int d) {
-    return size_t(kMaxPersistentCtas) * (256 * size_t(d) + 512) * 4 + kMaxPersistentCtas * 4;
+    return size_t(kMaxBlocks) * kMaxPersistentCtas * (256 * size_t(d) + 512) * 4 +
+           size_t(kMaxBlocks) * kMaxPersistentCtas * 4;
 }
+
+namespace {
+
+// KV segments of one problem: tile starts, lengths, rows and maps.
+void set_segments(Prob& P, int nseg, const int64_t* len, const int64_t* row0, const int* map) {
+    int tiles = 0;
+    P.nseg = nseg;
+    for (int s = 0; s < nseg; ++s) {
+        P.seg_tile_start[s] = tiles;
+        P.seg_len[s] = int(len[s]);
+        P.seg_row0[s] = int(row0[s]);
+        P.seg_map[s] = map[s];
+        tiles += int((len[s] + kBN - 1) / kBN);
+    }
+    P.seg_tile_start[nseg] = tiles;
+    P.n_tiles = tiles;
+}
+
+int grid_ctas(int max_ctas) {
+    int C = sm_count() < kMaxPersistentCtas ? sm_count() : kMaxPersistentCtas;
+    if (max_ctas > 0 && max_ctas < C) C = max_ctas;
+    return C;
+}
+
+// The stream-K bounds of T tail units of n tiles over C CTAs, cached per
+// (T, n, C): a shape's schedule is computed once.
+bool cached_class(int T, int n, int C, SkClass& k) {
+    constexpr int kMinPiece = 4;
+    if ((long long)T * n >= (1ll << 30)) return false;
+    static std::mutex mu;
+    static std::map<std::tuple<int, int, int>, std::vector<int>> cache;
+    std::lock_guard<std::mutex> lock(mu);
+    std::vector<int>& b = cache[std::make_tuple(T, n, C)];
+    if (b.empty()) {
+        b.assign(kMaxPersistentCtas + 1, 0);
+        const int g = tail_bounds(T, n, C, kMinPiece, b.data());
+        b.resize(g + 1);
+    }
+    const int G = int(b.size()) - 1;
+    if (G <= 0) return false;
+    for (int c = 0; c <= G; ++c) k.bound[c] = b[c];
+    k.ctas = G;
+    return true;
+}
+
+// Appends block (problem pr, heads [h0, h0 + nh)) to the launch's schedule:
+// R whole rounds, then the tail's stream-K class (shared by the blocks of the
+// same tail shape).  *full: the launch has no room left (the caller launches
+// what it has and continues); false otherwise means an invalid shape.
+bool add_block(FmhaParams& p, int pr, int h0, int nh, int C, bool* full) {
+    *full = false;
+    const Prob& P = p.prob[pr];
+    const int U = p.B * nh * P.n_qpairs;
+    const int R = U / C, T = U - R * C;
+    int cls = -1;
+    if (T > 0) {
+        for (int i = 0; i < p.ncls; ++i)
+            if (p.cls_key[i][0] == T && p.cls_key[i][1] == P.n_tiles) cls = i;
+        if (cls < 0) {
+            if (p.ncls == kMaxSkClasses) {
+                *full = true;
+                return false;
+            }
+            if (!cached_class(T, P.n_tiles, C, p.cls[p.ncls])) return false;
+            p.cls_key[p.ncls][0] = T;
+            p.cls_key[p.ncls][1] = P.n_tiles;
+            cls = p.ncls++;
+        }
+    }
+    if (p.nblk == kMaxBlocks) {
+        *full = true;
+        return false;
+    }
+    Block& b = p.blk[p.nblk];
+    b.pr = pr;
+    b.h0 = h0;
+    b.nh = nh;
+    b.rounds = R;
+    b.cls = cls;
+    b.tail0 = R * C;
+    b.off = 0;
+    if (p.nblk > 0) {
+        const Block& a = p.blk[p.nblk - 1];
+        b.off = (a.off + (a.cls >= 0 ? p.cls[a.cls].ctas : 0)) % C;
+    }
+    ++p.nblk;
+    return true;
+}
+
+// Grid: C when a block has whole rounds or several blocks are rotated over
+// the CTAs, else the single block's tail width.
+int launch_grid(const FmhaParams& p) {
+    if (p.nblk > 1) return p.ctas;
+    if (p.nblk == 0) return 0;
+    if (p.blk[0].rounds > 0) return p.ctas;
+    return p.blk[0].cls >= 0 ? p.cls[p.blk[0].cls].ctas : 0;
+}
+
+cudaError_t finish_and_launch(FmhaParams& p, int d, int grid, void* scratch, cudaStream_t stream,
+                              int* launches, unsigned long long* trace, bool peer) {
+    static const int l2_prefetch_env = [] {
+        const char* e = getenv("TM_L2_PREFETCH");
+        return e ? atoi(e) : 2;
+    }();
+    p.l2_prefetch = peer ? 0 : l2_prefetch_env;
+    p.trace = trace;
+    p.part = static_cast<float*>(scratch);
+    p.counters = reinterpret_cast<int*>(static_cast<uint8_t*>(scratch) +
+                                        size_t(kMaxBlocks) * kMaxPersistentCtas *
+                                            (256 * size_t(d) + 512) * 4);
+    if (grid <= 0) return cudaErrorInvalidValue;
+    cudaError_t e = d == 128 ? launch_d<128>(p, grid, stream) : launch_d<64>(p, grid, stream);
+    if (e == cudaSuccess && launches) ++*launches;
+    return e;
+}
+
+bool tma_epi_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("TM_TMA_EPI");
+        return !(e && strcmp(e, "0") == 0);
+    }();
+    return on;
+}
+
+}  // namespace
 
 cudaError_t launch_fmha_sm100(const AttnProblem& pr, void* scratch, cudaStream_t stream,
                               int* launches, unsigned long long* trace) {
     if (pr.d != 64 && pr.d != 128) return cudaErrorInvalidValue;
+    if (pr.nseg < 1 || pr.nseg > kMaxSegments) return cudaErrorInvalidValue;
     FmhaParams p;
     memset(&p, 0, sizeof(p));
     if (!make_map(&p.tq, pr.q, pr.d, pr.H, pr.Lq, pr.B, pr.q_bstride)) return cudaErrorInvalidValue;
-    int tiles = 0;
+    int64_t len[kMaxSegments], row0[kMaxSegments];
+    int map[kMaxSegments];
     for (int s = 0; s < pr.nseg; ++s) {
         if (!make_map(&p.tk[s], pr.seg[s].k, pr.d, pr.H, pr.seg[s].len, pr.B, pr.seg[s].bstride) ||
             !make_map(&p.tv[s], pr.seg[s].v, pr.d, pr.H, pr.seg[s].len, pr.B, pr.seg[s].bstride))
             return cudaErrorInvalidValue;
-        p.seg_tile_start[s] = tiles;
-        p.seg_len[s] = int(pr.seg[s].len);
-        tiles += int((pr.seg[s].len + kBN - 1) / kBN);
+        len[s] = pr.seg[s].len;
+        row0[s] = 0;
+        map[s] = s;
     }
-    p.seg_tile_start[pr.nseg] = tiles;
+    p.nmaps = pr.nseg;
+    p.nprob = 1;
+    Prob& P = p.prob[0];
+    set_segments(P, pr.nseg, len, row0, map);
+    const int tiles = P.n_tiles;
     p.store_seg = -1;
     if (pr.store_k && pr.store_v) {
         const Segment& cur = pr.seg[pr.nseg - 1];
@@ -1210,20 +1495,17 @@ cudaError_t launch_fmha_sm100(const AttnProblem& pr, void* scratch, cudaStream_t
             return cudaErrorInvalidValue;
         p.store_seg = pr.nseg - 1;
     }
-    p.nseg = pr.nseg;
-    p.n_tiles = tiles;
-    p.Lq = int(pr.Lq);
+    P.Lq = int(pr.Lq);
+    P.q_row0 = 0;
+    P.o_row0 = 0;
+    P.o_clip = 1;
     p.H = pr.H;
     p.B = pr.B;
     p.scale_log2 = pr.scale * 1.4426950408889634f;
     p.o_dst[0] = static_cast<uint16_t*>(pr.o);
     p.o_bstride = pr.q_bstride > 0 ? pr.q_bstride : pr.Lq;
-    static const bool tma_epi_env = [] {
-        const char* e = getenv("TM_TMA_EPI");
-        return !(e && strcmp(e, "0") == 0);
-    }();
     p.tma_epi = 0;
-    if (tma_epi_env && !pr.peer && make_map(&p.to, pr.o, pr.d, pr.H, pr.Lq, pr.B, p.o_bstride, 32))
+    if (tma_epi_enabled() && !pr.peer && make_map(&p.to, pr.o, pr.d, pr.H, pr.Lq, pr.B, p.o_bstride, 32))
         p.tma_epi = 1;
     p.o_rows = int(pr.Lq);
     p.o_H = pr.H;
@@ -1253,50 +1535,85 @@ cudaError_t launch_fmha_sm100(const AttnProblem& pr, void* scratch, cudaStream_t
             return cudaErrorInvalidValue;
     }
     const int qtiles = int((pr.Lq + kBM - 1) / kBM);
-    p.n_qpairs = (qtiles + 1) / 2;
+    P.n_qpairs = (qtiles + 1) / 2;
     // Persistent schedule: R whole rounds over C CTAs, then the T tail units'
     // T*n KV tiles in contiguous ranges over G' CTAs (stream-K).  P = 2, 4, 8
     // head shards leave T >= C/2 (240, 120, 60 units of 56 tiles at WAN-512),
     // where whole-unit or even-split tails idle ~19% of the machine.
-    constexpr int kMinPiece = 4;
-    int C = sm_count() < kMaxPersistentCtas ? sm_count() : kMaxPersistentCtas;
-    if (pr.max_ctas > 0 && pr.max_ctas < C) C = pr.max_ctas;
-    const int U = pr.B * pr.H * p.n_qpairs;
-    const int R = U / C;
-    const int T = U - R * C;
-    int G = 0;
-    if (T > 0) {
-        if ((long long)T * tiles >= (1ll << 30)) return cudaErrorInvalidValue;
-        // the bounds depend only on (T, n, C): computed once, then cached
-        static std::mutex mu;
-        static std::map<std::tuple<int, int, int>, std::vector<int>> cache;
-        std::lock_guard<std::mutex> lock(mu);
-        std::vector<int>& b = cache[std::make_tuple(T, tiles, C)];
-        if (b.empty()) {
-            b.assign(kMaxPersistentCtas + 1, 0);
-            const int g = tail_bounds(T, tiles, C, kMinPiece, b.data());
-            b.resize(g + 1);
-        }
-        G = int(b.size()) - 1;
-        if (G <= 0) return cudaErrorInvalidValue;
-        for (int c = 0; c <= G; ++c) p.sk_bound[c] = b[c];
+    // Schedule blocks of sched_heads heads (0: all heads in one block).
+    const int C = grid_ctas(pr.max_ctas);
+    p.ctas = C;
+    const int hb = pr.sched_heads > 0 ? pr.sched_heads : pr.H;
+    if (pr.H % hb) return cudaErrorInvalidValue;
+    for (int h0 = 0; h0 < pr.H; h0 += hb) {
+        bool full = false;
+        if (!add_block(p, 0, h0, hb, C, &full)) return cudaErrorInvalidValue;
     }
-    static const int l2_prefetch_env = [] {
-        const char* e = getenv("TM_L2_PREFETCH");
-        return e ? atoi(e) : 2;
-    }();
-    p.l2_prefetch = pr.peer ? 0 : l2_prefetch_env;
-    p.rounds = R;
-    p.sk_units = T;
-    p.sk_ctas = G;
-    p.trace = trace;
-    p.part = static_cast<float*>(scratch);
-    p.counters = reinterpret_cast<int*>(static_cast<uint8_t*>(scratch) +
-                                        size_t(kMaxPersistentCtas) * (256 * size_t(pr.d) + 512) * 4);
-    const int grid = R > 0 ? C : G;
-    cudaError_t e = pr.d == 128 ? launch_d<128>(p, grid, stream) : launch_d<64>(p, grid, stream);
-    if (e == cudaSuccess && launches) ++*launches;
-    return e;
+    (void)tiles;
+    return finish_and_launch(p, pr.d, launch_grid(p), scratch, stream, launches, trace,
+                             pr.peer != nullptr);
+}
+
+cudaError_t launch_fmha_sm100_multi(const MultiProblem& mp, void* scratch, cudaStream_t stream,
+                                    int* launches) {
+    if (mp.d != 64 && mp.d != 128) return cudaErrorInvalidValue;
+    if (mp.nprob < 1 || mp.nprob > kMaxProblems) return cudaErrorInvalidValue;
+    FmhaParams p;
+    memset(&p, 0, sizeof(p));
+    if (!make_map(&p.tq, mp.q, mp.d, mp.H, mp.q_rows, mp.B, mp.q_bstride) ||
+        !make_map(&p.tk[0], mp.k, mp.d, mp.H, mp.kv_rows, mp.B, mp.kv_bstride) ||
+        !make_map(&p.tv[0], mp.v, mp.d, mp.H, mp.kv_rows, mp.B, mp.kv_bstride))
+        return cudaErrorInvalidValue;
+    p.nmaps = 1;
+    p.nprob = mp.nprob;
+    p.store_seg = -1;
+    p.H = mp.H;
+    p.B = mp.B;
+    p.scale_log2 = mp.scale * 1.4426950408889634f;
+    p.o_dst[0] = static_cast<uint16_t*>(mp.o);
+    p.o_bstride = mp.o_bstride > 0 ? mp.o_bstride : mp.o_rows;
+    p.o_row_map = mp.o_row_map;
+    p.tma_epi = 0;
+    if (tma_epi_enabled() && !mp.o_row_map &&
+        make_map(&p.to, mp.o, mp.d, mp.H, mp.o_rows, mp.B, p.o_bstride, 32))
+        p.tma_epi = 1;
+    p.o_rows = int(1 << 30);          // one owner: every row of O is local
+    p.o_H = mp.H;
+    p.o_h0 = 0;
+    p.wait_seg = -1;
+    for (int i = 0; i < mp.nprob; ++i) {
+        const SubProblem& sp = mp.prob[i];
+        if (sp.nseg < 1 || sp.nseg > kMaxSegments || sp.Lq <= 0) return cudaErrorInvalidValue;
+        Prob& P = p.prob[i];
+        int map[kMaxSegments] = {};
+        set_segments(P, sp.nseg, sp.seg_len, sp.seg_row0, map);
+        P.q_row0 = int(sp.q_row0);
+        P.Lq = int(sp.Lq);
+        P.o_row0 = int(sp.o_row0);
+        P.o_clip = !mp.o_row_map && sp.o_row0 + sp.Lq == mp.o_rows;
+        P.n_qpairs = int((sp.Lq + 2 * kBM - 1) / (2 * kBM));
+    }
+    // Blocks: every problem x head group, in order.  A launch holds up to
+    // kMaxBlocks blocks of up to kMaxSkClasses tail shapes, so a long list
+    // runs as several launches (each block is scheduled as if alone anyway).
+    const int C = grid_ctas(mp.max_ctas);
+    p.ctas = C;
+    const int hb = mp.sched_heads > 0 ? mp.sched_heads : mp.H;
+    if (mp.H % hb) return cudaErrorInvalidValue;
+    for (int i = 0; i < mp.nprob; ++i) {
+        for (int h0 = 0; h0 < mp.H; h0 += hb) {
+            bool full = false;
+            if (add_block(p, i, h0, hb, C, &full)) continue;
+            if (!full) return cudaErrorInvalidValue;
+            cudaError_t e = finish_and_launch(p, mp.d, launch_grid(p), scratch, stream, launches,
+                                              nullptr, false);
+            if (e != cudaSuccess) return e;
+            p.nblk = 0;
+            p.ncls = 0;
+            if (!add_block(p, i, h0, hb, C, &full)) return cudaErrorInvalidValue;
+        }
+    }
+    return finish_and_launch(p, mp.d, launch_grid(p), scratch, stream, launches, nullptr, false);
 }
 
 }  // namespace tmk

@@ -12,6 +12,9 @@ namespace tmk {
 constexpr int kMaxSegments = 5;   // {c_0, c_{t-1}, c_t}; f4 audio windows need up to 5
 constexpr int kMaxPersistentCtas = 160;   // persistent grid cap (B200: 148 SMs)
 constexpr int kMaxPeers = 8;      // peer transport: one NVSwitch node
+constexpr int kMaxProblems = 16;  // problems per attention launch (f1 window chunks, f4 frames)
+constexpr int kMaxBlocks = 8;     // schedule blocks per attention launch (see fmha_sm100.cu)
+constexpr int kMaxSkClasses = 4;  // distinct stream-K tail shapes per launch
 // Debug trace buffer (TM_TRACE build): 13 roles x 4096 clock64 events of CTA 0,
 // then 8 words per CTA: globaltimer at entry, first S seen, second item start,
 // exit, merge wait begin / end; tiles and items of the CTA.
@@ -84,6 +87,7 @@ struct AttnProblem {
     void* store_v = nullptr;
     const PeerAttnArgs* peer = nullptr;   // peer transport (sm100 path only)
     int max_ctas = 0;                     // persistent grid cap (0: one CTA per SM)
+    int sched_heads = 0;                  // heads per schedule block (0: all; see tm_config)
 };
 
 // SM count of the CURRENT device, cached per device ordinal (a process may
@@ -107,6 +111,34 @@ inline int current_sm_count() {
     }
     return n;
 }
+
+// Several attention problems in ONE launch over shared tensors (f1: the
+// query chunks of a full window over their key chunks {0, c-1, c}, P:134-143;
+// f4: the face rows of each latent frame over its clamped audio window,
+// P:123-125).  Q [B][q_rows][H][d], K/V [B][kv_rows][H][d], O
+// [B][o_rows][H][d] (batch strides in tokens, 0 = rows); problem i reads
+// query rows [q_row0, q_row0 + Lq), its keys are nseg row ranges of K/V, and
+// query q's output row is o_row0 + (o_row_map ? o_row_map[q] : q).
+struct SubProblem {
+    int64_t q_row0 = 0, Lq = 0, o_row0 = 0;
+    int nseg = 0;
+    int64_t seg_row0[kMaxSegments] = {};
+    int64_t seg_len[kMaxSegments] = {};
+};
+struct MultiProblem {
+    const void* q = nullptr;
+    const void* k = nullptr;
+    const void* v = nullptr;
+    void* o = nullptr;
+    int64_t q_rows = 0, q_bstride = 0, kv_rows = 0, kv_bstride = 0, o_rows = 0, o_bstride = 0;
+    const int32_t* o_row_map = nullptr;   // device, nullable
+    int B = 1, H = 1, d = 128;
+    float scale = 0.f;
+    int nprob = 0;
+    SubProblem prob[kMaxProblems];
+    int max_ctas = 0;
+    int sched_heads = 0;
+};
 
 // Launch with programmatic dependent launch allowed (the kernel executes
 // griddepcontrol.wait before touching global data, so its prologue overlaps the
@@ -138,9 +170,14 @@ size_t fmha_sm100_scratch_bytes(int d);
 // Host: the stream-K tail ranges of the attention schedule (fmha_sm100.cu):
 // T tail units of n KV tiles each over at most C CTAs; writes G+1 bounds, returns G.
 int tail_bounds(int T, int n, int C, int min_piece, int* bound);
+// The same over runs of units of different sizes (run r: units[r] units of
+// tiles[r] tiles each, flattened in order).
+int tail_bounds_runs(int nruns, const int* units, const int* tiles, int C, int min_piece, int* bound);
 // `trace` (debug, may be null): 4 x 4096 uint64 clock64 timeline of CTA 0.
 cudaError_t launch_fmha_sm100(const AttnProblem& p, void* scratch, cudaStream_t s, int* launches,
                               unsigned long long* trace = nullptr);
+cudaError_t launch_fmha_sm100_multi(const MultiProblem& p, void* scratch, cudaStream_t s,
+                                    int* launches);
 cudaError_t launch_fmha_fp32(const AttnProblem& p, cudaStream_t s, int* launches);
 cudaError_t launch_euler(float* x, const void* v, int v_is_bf16, int64_t n, float dt,
                          cudaStream_t s, int* launches);
@@ -151,6 +188,10 @@ cudaError_t launch_sampler(float* x, const void* v, int v_is_bf16, const float* 
 // f4: gather (scatter = 0) / scatter (1) of face-token rows, ids device int32.
 cudaError_t launch_face_rows(const void* src, void* dst, const int32_t* ids, int64_t BF, int64_t T,
                             int64_t nf, int row_bytes, int scatter, cudaStream_t s, int* launches);
+// f4 (bf16): gather the face rows of q into qf and zero the non-face rows of o
+// (the attention epilogue writes the face rows); T <= 49152.
+cudaError_t launch_audio_prep(const void* q, void* qf, void* o, const int32_t* ids, int64_t BF,
+                              int64_t T, int64_t nf, int row_bytes, cudaStream_t s, int* launches);
 // Non-finite check: sets *flag (device int) to 1 if any element is NaN/Inf.
 cudaError_t launch_nonfinite(const void* x, int is_bf16, int64_t n, int* flag, cudaStream_t s,
                              int* launches);

@@ -37,14 +37,14 @@ class tm_config(ctypes.Structure):
                 ("batch", ctypes.c_int32), ("dtype", ctypes.c_int32),
                 ("softmax_scale", ctypes.c_float), ("world_size", ctypes.c_int32),
                 ("rank", ctypes.c_int32), ("device", ctypes.c_int32),
-                ("transport", ctypes.c_int32)]
+                ("transport", ctypes.c_int32), ("sched_heads", ctypes.c_int32)]
 
 
 def make_config(heads, head_dim, ref_tokens, chunk_tokens, num_layers=1, num_steps=1, batch=1,
                 dtype=TM_BF16, softmax_scale=0.0, world_size=1, rank=0, device=0,
-                transport=TM_TRANSPORT_NCCL) -> tm_config:
+                transport=TM_TRANSPORT_NCCL, sched_heads=0) -> tm_config:
     return tm_config(heads, head_dim, ref_tokens, chunk_tokens, num_layers, num_steps, batch,
-                     dtype, softmax_scale, world_size, rank, device, transport)
+                     dtype, softmax_scale, world_size, rank, device, transport, sched_heads)
 
 
 def _load():
@@ -362,10 +362,11 @@ class ChunkAttention:
 
     def __init__(self, heads, head_dim, ref_tokens, chunk_tokens, num_layers=1, num_steps=1,
                  batch=1, dtype=TM_BF16, softmax_scale=0.0, world_size=1, rank=0, device=0,
-                 nccl_id=None, transport=TM_TRANSPORT_NCCL):
+                 nccl_id=None, transport=TM_TRANSPORT_NCCL, sched_heads=0):
         import torch
         self.cfg = make_config(heads, head_dim, ref_tokens, chunk_tokens, num_layers, num_steps,
-                               batch, dtype, softmax_scale, world_size, rank, device, transport)
+                               batch, dtype, softmax_scale, world_size, rank, device, transport,
+                               sched_heads)
         self.cache_bytes = tm_kvcache_bytes(self.cfg)
         self.ws_bytes = tm_workspace_bytes(self.cfg)
         if self.cache_bytes == 0 or self.ws_bytes == 0:

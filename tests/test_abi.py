@@ -29,7 +29,7 @@ def test_library_exports_every_declared_symbol():
 
 
 def test_version():
-    assert tm.tm_version() == 101
+    assert tm.tm_version() == 102
 
 
 def wan512(**kw):
@@ -74,8 +74,9 @@ def test_invalid_configs_are_rejected(bad):
 
 
 def test_workspace_sizes():
-    # bf16: debug flag + split-KV scratch: 1 partial slot per persistent CTA (<= 160) + counters
-    scratch = 160 * (256 * 128 + 512) * 4 + 160 * 4
+    # bf16: debug flag + split-KV scratch: 1 partial slot per (schedule block <= 8, persistent
+    # CTA <= 160) + counters
+    scratch = 8 * 160 * (256 * 128 + 512) * 4 + 8 * 160 * 4
     assert tm.tm_workspace_bytes(wan512()) == 1024 + (scratch + 1023) // 1024 * 1024
     assert tm.tm_workspace_bytes(wan512(dtype=tm.TM_FP32)) == 1024
     ws8 = tm.tm_workspace_bytes(wan512(world_size=8))
@@ -116,7 +117,7 @@ def test_peer_workspace_layout():
     counters, Q/K/V windows [B][max(Lc,Lr)][H/P][d] and the O window
     [B][ceil(Lc/P)][H][d], each 1024-B aligned; no NCCL staging."""
     al = lambda x: (x + 1023) // 1024 * 1024
-    scratch = 1024 + al(160 * (256 * 128 + 512) * 4 + 160 * 4)
+    scratch = 1024 + al(8 * 160 * (256 * 128 + 512) * 4 + 8 * 160 * 4)
     for P in (1, 2, 8):
         c = wan512(world_size=P, transport=tm.TM_TRANSPORT_PEER)
         win = 4096 + 3 * al(3072 * (40 // P) * 128 * 2) + al(-(-3072 // P) * 40 * 128 * 2)
@@ -126,5 +127,16 @@ def test_peer_workspace_layout():
     assert tm.tm_workspace_bytes(c) == scratch + win
     # Lr > Lc: the K/V windows also carry the reference push
     c = tm.make_config(4, 64, 500, 100, 1, 1, world_size=2, transport=tm.TM_TRANSPORT_PEER)
-    scratch64 = 1024 + al(160 * (256 * 64 + 512) * 4 + 160 * 4)
+    scratch64 = 1024 + al(8 * 160 * (256 * 64 + 512) * 4 + 8 * 160 * 4)
     assert tm.tm_workspace_bytes(c) == scratch64 + 4096 + 3 * al(500 * 2 * 64 * 2) + al(50 * 4 * 64 * 2)
+
+
+def test_sched_heads_validation_host():
+    """tm_config.sched_heads must be 0 or divide the heads per rank."""
+    assert tm.tm_kvcache_bytes(tm.make_config(40, 128, 1024, 3072, 1, 1, sched_heads=5)) > 0
+    assert tm.tm_kvcache_bytes(tm.make_config(40, 128, 1024, 3072, 1, 1, sched_heads=3)) == 0
+    assert tm.tm_kvcache_bytes(tm.make_config(40, 128, 1024, 3072, 1, 1, world_size=8,
+                                              sched_heads=5)) > 0
+    assert tm.tm_kvcache_bytes(tm.make_config(40, 128, 1024, 3072, 1, 1, world_size=8,
+                                              sched_heads=10)) == 0
+    assert tm.tm_kvcache_bytes(tm.make_config(40, 128, 1024, 3072, 1, 1, sched_heads=-1)) == 0
