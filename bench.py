@@ -400,13 +400,13 @@ def cpu_baseline(c, rows):
                                          "one_core": dt1 * c["Lc"] / one_rows}}
 
 
-def attention_loop(tm, torch, H, d, Lr, Lc, K, stream, zero_copy=False, NL=8, NB=4):
+def attention_loop(tm, torch, H, d, Lr, Lc, K, stream, zero_copy=False, NL=8, NB=4, sched_heads=0):
     """ms per chunk-attention call (t >= 2) of a fresh H-head context: K calls
     back to back between one event pair, operands rotated over NL layer caches
     and NB input sets (larger than L2); fused c_t append unless zero_copy."""
     bf = torch.bfloat16
     g = torch.Generator(device="cuda").manual_seed(2506030990 + 55 + H)
-    ca = tm.ChunkAttention(H, d, Lr, Lc, NL, 1)
+    ca = tm.ChunkAttention(H, d, Lr, Lc, NL, 1, sched_heads=sched_heads)
     sets = [[torch.randn(Lc, H, d, device="cuda", dtype=bf, generator=g) for _ in range(3)]
             for _ in range(NB)]
     o = torch.empty(Lc, H, d, device="cuda", dtype=bf)
@@ -489,6 +489,13 @@ def measure_shards(tm, torch, c, K, stream, t1_ms):
                          "tflops_zero_copy": fl / (ms_zc * 1e-3) / 1e12,
                          "q_push_us_model": q_push_us, "t_model_ms": t,
                          "E_model": t1_ms / (P * t)}
+    # P-invariant schedule (tm_config.sched_heads = H/8: every 5 heads scheduled
+    # as a block of their own, bitwise equal outputs for P = 1, 2, 4, 8): its
+    # cost at P = 1 against the default schedule, the same loop back to back.
+    base = attention_loop(tm, torch, H, d, Lr, Lc, K, stream)
+    inv = attention_loop(tm, torch, H, d, Lr, Lc, K, stream, sched_heads=H // 8)
+    out["p_invariant_p1"] = {"sched_heads": H // 8, "ms_default": base, "ms_p_invariant": inv,
+                             "cost_frac": inv / base - 1.0}
     return out
 
 

@@ -671,6 +671,19 @@ tm_status tm_kvcache_put_reference_phases(tm_ctx* ctx, int32_t layer, int32_t st
     return TM_OK;
 }
 
+// Debug builds (TM_TRACE=<file>): append the launch's trace words to the file
+// (synchronises).  No-op otherwise.
+static void dump_trace(tm_ctx* ctx, cudaStream_t cs) {
+    if (!ctx->trace) return;
+    std::vector<unsigned long long> h(kTraceWords);
+    cudaMemcpyAsync(h.data(), ctx->trace, h.size() * 8, cudaMemcpyDeviceToHost, cs);
+    cudaStreamSynchronize(cs);
+    if (FILE* f = fopen(ctx->trace_path.c_str(), "ab")) {
+        fwrite(h.data(), 8, h.size(), f);
+        fclose(f);
+    }
+}
+
 tm_status tm_chunk_attention(tm_ctx* ctx, int32_t layer, int32_t step, int64_t chunk,
                              const void* q, const void* k, const void* v, void* o, void* stream) {
     return tm_chunk_attention_phases(ctx, layer, step, chunk, q, k, v, o, TM_PHASE_ALL, stream);
@@ -862,15 +875,7 @@ tm_status tm_chunk_attention_phases(tm_ctx* ctx, int32_t layer, int32_t step, in
     st = cuda_check(e, "attention kernel launch");
     if (st) return st;
     }
-    if (attend && ctx->trace) {   // debug only: dump CTA 0's timeline (synchronises)
-        std::vector<unsigned long long> h(kTraceWords);
-        cudaMemcpyAsync(h.data(), ctx->trace, h.size() * 8, cudaMemcpyDeviceToHost, cs);
-        cudaStreamSynchronize(cs);
-        if (FILE* f = fopen(ctx->trace_path.c_str(), "ab")) {
-            fwrite(h.data(), 8, h.size(), f);
-            fclose(f);
-        }
-    }
+    if (attend) dump_trace(ctx, cs);
 
     if (Ly.exchange) {
         // a6: head -> seq all-to-all of O (packed at the end of ATTEND into its
@@ -1016,7 +1021,7 @@ tm_status tm_window_attention(tm_ctx* ctx, const void* q, const void* k, const v
                     sp.seg_len[j] = chunk_len[kc[j]];
                 }
             }
-            tm_status st = cuda_check(launch_fmha_sm100_multi(mp, ctx->scratch(), cs, &ctx->launches),
+            tm_status st = cuda_check(launch_fmha_sm100_multi(mp, ctx->scratch(), cs, &ctx->launches, ctx->trace),
                                       "window attention launch");
             if (st) return st;
         }
@@ -1115,10 +1120,16 @@ tm_status tm_audio_cross_attention(tm_ctx* ctx, const void* q, const void* k_aud
         // (2) every frame's face rows attend its audio window as problems of
         // ONE attention launch (up to kMaxProblems frames per launch) whose
         // epilogue writes each face row straight to its token row of o.
-        st = cuda_check(launch_audio_prep(q, qf, o, face_ids, BF, tokens_per_frame, n_face, row, cs,
-                                          &ctx->launches), "audio prep (face gather, zero fill)");
-        if (st) return st;
-        for (int64_t f0 = 0; f0 < frames; f0 += kMaxProblems) {
+        static const int dbg_parts = [] {   // timing experiments only: 1 prep only, 2 attention only
+            const char* e = getenv("TM_DBG_AUDIO_PART");
+            return e ? atoi(e) : 0;
+        }();
+        if (dbg_parts != 2) {
+            st = cuda_check(launch_audio_prep(q, qf, o, face_ids, BF, tokens_per_frame, n_face, row, cs,
+                                              &ctx->launches), "audio prep (face gather, zero fill)");
+            if (st) return st;
+        }
+        for (int64_t f0 = 0; f0 < frames && dbg_parts != 1; f0 += kMaxProblems) {
             MultiProblem mp;
             mp.q = qf;
             mp.k = k_audio;
@@ -1142,9 +1153,11 @@ tm_status tm_audio_cross_attention(tm_ctx* ctx, const void* q, const void* k_aud
                 sp.o_row0 = f * tokens_per_frame;
                 sp.nseg = window_runs(f, sp.seg_row0, sp.seg_len);
             }
-            st = cuda_check(launch_fmha_sm100_multi(mp, ctx->scratch(), cs, &ctx->launches),
+            if (ctx->trace) cudaMemsetAsync(ctx->trace, 0, kTraceWords * 8, cs);
+            st = cuda_check(launch_fmha_sm100_multi(mp, ctx->scratch(), cs, &ctx->launches, ctx->trace),
                             "audio cross-attention launch");
             if (st) return st;
+            dump_trace(ctx, cs);
         }
         return debug_check(ctx, o, BF * tokens_per_frame * cf.heads * cf.head_dim, 1, cs,
                            "tm_audio_cross_attention");

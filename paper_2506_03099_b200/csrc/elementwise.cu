@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(256) face_rows_kernel(const uint4* __restrict_
 // the attention launch then writes the face rows of o itself (its epilogue
 // scatters through ids).  Each CTA builds the inverse map token -> face slot
 // in shared memory (T ints; ids outside [0, T) are ignored).
-__global__ void __launch_bounds__(256) audio_prep_kernel(const uint4* __restrict__ q,
+__global__ void __launch_bounds__(512) audio_prep_kernel(const uint4* __restrict__ q,
                                                          uint4* __restrict__ qf,
                                                          uint4* __restrict__ o,
                                                          const int32_t* __restrict__ ids,
@@ -229,16 +229,34 @@ __global__ void __launch_bounds__(256) audio_prep_kernel(const uint4* __restrict
         if (t >= 0 && t < T) inv[t] = i;      // duplicates: any one slot (same row, same output)
     }
     __syncthreads();
-    const int64_t total = BF * T * W;
-    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-    for (int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < total; idx += stride) {
-        const int w = int(idx % W);
-        const int64_t r = idx / W;
+    // One warp per token row (the branch is warp-uniform); lanes stride over
+    // the row's W 16-byte words, two in flight per lane.
+    const int lane = threadIdx.x & 31;
+    const int64_t rows = BF * T;
+    const int64_t wstride = int64_t(gridDim.x) * (blockDim.x >> 5);
+    for (int64_t r = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += wstride) {
         const int t = int(r % T);
-        const int64_t bf = r / T;
         const int i = inv[t];
-        if (i >= 0) qf[(bf * nf + i) * W + w] = __ldcs(q + idx);
-        else o[idx] = make_uint4(0, 0, 0, 0);
+        uint4* orow = o + r * W;
+        if (i >= 0) {
+            const uint4* src = q + r * W;
+            uint4* dst = qf + ((r / T) * nf + i) * W;
+            // 8 loads in flight per lane before the stores (a 10 KB row is then
+            // one L2 round trip, not W/64 dependent ones)
+            for (int w0 = lane; w0 < W; w0 += 256) {
+                uint4 v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (w0 + 32 * u < W) v[u] = __ldcs(src + w0 + 32 * u);
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (w0 + 32 * u < W) dst[w0 + 32 * u] = v[u];
+            }
+        } else {
+            const uint4 z = make_uint4(0, 0, 0, 0);
+#pragma unroll 4
+            for (int w = lane; w < W; w += 32) __stcs(orow + w, z);
+        }
     }
 }
 
@@ -338,8 +356,9 @@ cudaError_t launch_audio_prep(const void* q, void* qf, void* o, const int32_t* i
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         if (e != cudaSuccess) return e;
     }
-    const unsigned grid = grid_for(BF * T * W, 256, 8);
-    audio_prep_kernel<<<grid, 256, smem, s>>>(static_cast<const uint4*>(q), static_cast<uint4*>(qf),
+    // rows over the warps of <= 2 CTAs per SM (the face map is built once per CTA)
+    const unsigned grid = grid_for(BF * T, 16, 2);
+    audio_prep_kernel<<<grid, 512, smem, s>>>(static_cast<const uint4*>(q), static_cast<uint4*>(qf),
                                               static_cast<uint4*>(o), ids, BF, int(T), int(nf), W);
     if (launches) ++*launches;
     return cudaGetLastError();

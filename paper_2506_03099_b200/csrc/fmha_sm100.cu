@@ -157,6 +157,8 @@ struct __align__(64) FmhaParams {
     uint16_t* o_dst[kMaxPeers];       // bf16 bits [B][o_rows][o_H][d] each
     CUtensorMap to;                   // o as a TMA store map (box 32 rows x 64), one owner only
     int tma_epi;                      // 1: epilogue rows leave through TMA stores of the staging
+    int exit_wait_full;               // A/B: wait for the epilogue TMA stores' global writes at exit
+    int dbg_nomerge;                  // timing experiments only (TM_DBG_NOMERGE=1): pieces store unmerged
     int64_t o_bstride;                // rows between batch elements of an o_dst
     int o_rows, o_H, o_h0;
     // Peer transport: waits on the own counters before Q tiles (T=0)
@@ -816,7 +818,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
         Item it;
         Cursor cu;
         for (; next_item(p, cu, it); ++n_item) {
-#ifndef TM_SPANS_MERGE
+#if !defined(TM_SPANS_MERGE) && !defined(TM_SPANS_MERGE2)
             if (threadIdx.x == 0 && n_item == 1) trace_span(p, 2);   // first item's epilogue done
 #endif
             float m_run = -INFINITY, l = 0.f;
@@ -826,7 +828,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                 uint32_t r[kBN];
                 mbar_wait(&s_full[i], g & 1);
                 if (tr) trace_ev(p, 5 + warp, tn, 20);
-#ifndef TM_SPANS_MERGE
+#if !defined(TM_SPANS_MERGE) && !defined(TM_SPANS_MERGE2)
                 if (threadIdx.x == 0 && g == 0) trace_span(p, 1);
 #endif
                 tc_fence_after();
@@ -941,7 +943,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
             if (threadIdx.x == 0) trace_span(p, 2);   // (spans A/B) this item's epilogue begins
 #endif
             const int q = it.qp * 2 * kBM + row_in_pair;
-            if (!it.piece) {
+            if (!it.piece || p.dbg_nomerge) {   // (dbg_nomerge: timing bound only, wrong output)
                 store_rows_bf16<D>(p, p.prob[it.pr], tOi, 1.f / l, sEpi + warp * 4096, it.b, q - lane,
                                    it.h, lane);
 #ifdef TM_SPANS_MERGE
@@ -1060,6 +1062,9 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                     }
                 }
                 const float inv = 1.f / wsum;
+#ifdef TM_SPANS_MERGE2
+                if (threadIdx.x == 0) trace_span(p, 1);      // (spans A/B) weights ready
+#endif
                 float m_cur = mm[0];
                 for (int k = 1; k < np; ++k) {
                     // piece k+1's m, consumed one piece later (latency hidden)
@@ -1116,13 +1121,23 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                     m_cur = m_nxt;
                 }
                 tmem_wait_st();
+#ifdef TM_SPANS_MERGE2
+                if (threadIdx.x == 0) trace_span(p, 2);      // (spans A/B) partials merged
+#endif
                 store_rows_bf16<D>(p, p.prob[it.pr], tOi, inv, sEpi + warp * 4096, it.b, q - lane, it.h,
                                    lane);
                 tc_fence_before();
                 mbar_arrive(&o_empty[i]);
             }
         }
-        if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");   // epilogue stores done
+        // The epilogue's TMA stores must have READ their staging buffers before
+        // the CTA's shared memory goes away; their global writes complete with
+        // the grid (what a dependent launch waits for).  exit_wait_full (A/B,
+        // TM_EXIT_WAIT_FULL=1) waits for the writes themselves.
+        if (lane == 0) {
+            if (p.exit_wait_full) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+            else asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        }
 #ifdef TM_SPANS_MERGE
         if (threadIdx.x == 0) trace_span(p, 4);   // (spans A/B) softmax loop left, before the final barrier
 #endif
@@ -1255,6 +1270,12 @@ int tail_bounds_runs(int nruns, const int* units, const int* tiles, int C, int m
         const char* e = getenv("TM_SCHED_ITEM_COST");
         return e ? float(atof(e)) : 3.f;
     }();
+    // A range that starts inside a unit holds a partner piece, whose partial
+    // the merger waits for: charged kPartialCost tiles so it finishes earlier.
+    static const float partial_cost = [] {
+        const char* e = getenv("TM_SCHED_PARTIAL_COST");
+        return e ? float(atof(e)) : 0.f;
+    }();
     static const bool split_sched = [] {
         const char* e = getenv("TM_SCHED_SPLIT");
         return e && *e && strcmp(e, "0") != 0;
@@ -1290,7 +1311,7 @@ int tail_bounds_runs(int nruns, const int* units, const int* tiles, int C, int m
         while (x < W) {
             if (g == G) return G + 1;
             const int start = x;
-            float cost = 0.f;
+            float cost = (x > 0 && unit_end(x - 1) != x) ? partial_cost : 0.f;
             while (x < W) {
                 const int ue = unit_end(x);
                 const float extra = x > start ? item_cost : 0.f;
@@ -1437,6 +1458,14 @@ int launch_grid(const FmhaParams& p) {
     return p.blk[0].cls >= 0 ? p.cls[p.blk[0].cls].ctas : 0;
 }
 
+bool exit_wait_full() {
+    static const bool on = [] {
+        const char* e = getenv("TM_EXIT_WAIT_FULL");
+        return e && *e && strcmp(e, "0") != 0;
+    }();
+    return on;
+}
+
 cudaError_t finish_and_launch(FmhaParams& p, int d, int grid, void* scratch, cudaStream_t stream,
                               int* launches, unsigned long long* trace, bool peer) {
     static const int l2_prefetch_env = [] {
@@ -1444,6 +1473,12 @@ cudaError_t finish_and_launch(FmhaParams& p, int d, int grid, void* scratch, cud
         return e ? atoi(e) : 2;
     }();
     p.l2_prefetch = peer ? 0 : l2_prefetch_env;
+    p.exit_wait_full = exit_wait_full();
+    static const bool nomerge = [] {
+        const char* e = getenv("TM_DBG_NOMERGE");
+        return e && *e && strcmp(e, "0") != 0;
+    }();
+    p.dbg_nomerge = nomerge;
     p.trace = trace;
     p.part = static_cast<float*>(scratch);
     p.counters = reinterpret_cast<int*>(static_cast<uint8_t*>(scratch) +
@@ -1555,7 +1590,7 @@ cudaError_t launch_fmha_sm100(const AttnProblem& pr, void* scratch, cudaStream_t
 }
 
 cudaError_t launch_fmha_sm100_multi(const MultiProblem& mp, void* scratch, cudaStream_t stream,
-                                    int* launches) {
+                                    int* launches, unsigned long long* trace) {
     if (mp.d != 64 && mp.d != 128) return cudaErrorInvalidValue;
     if (mp.nprob < 1 || mp.nprob > kMaxProblems) return cudaErrorInvalidValue;
     FmhaParams p;
@@ -1606,14 +1641,14 @@ cudaError_t launch_fmha_sm100_multi(const MultiProblem& mp, void* scratch, cudaS
             if (add_block(p, i, h0, hb, C, &full)) continue;
             if (!full) return cudaErrorInvalidValue;
             cudaError_t e = finish_and_launch(p, mp.d, launch_grid(p), scratch, stream, launches,
-                                              nullptr, false);
+                                              trace, false);
             if (e != cudaSuccess) return e;
             p.nblk = 0;
             p.ncls = 0;
             if (!add_block(p, i, h0, hb, C, &full)) return cudaErrorInvalidValue;
         }
     }
-    return finish_and_launch(p, mp.d, launch_grid(p), scratch, stream, launches, nullptr, false);
+    return finish_and_launch(p, mp.d, launch_grid(p), scratch, stream, launches, trace, false);
 }
 
 }  // namespace tmk

@@ -177,7 +177,7 @@ int tail_bounds_runs(int nruns, const int* units, const int* tiles, int C, int m
 cudaError_t launch_fmha_sm100(const AttnProblem& p, void* scratch, cudaStream_t s, int* launches,
                               unsigned long long* trace = nullptr);
 cudaError_t launch_fmha_sm100_multi(const MultiProblem& p, void* scratch, cudaStream_t s,
-                                    int* launches);
+                                    int* launches, unsigned long long* trace = nullptr);
 cudaError_t launch_fmha_fp32(const AttnProblem& p, cudaStream_t s, int* launches);
 cudaError_t launch_euler(float* x, const void* v, int v_is_bf16, int64_t n, float dt,
                          cudaStream_t s, int* launches);
