@@ -298,6 +298,28 @@ def _time_ms(torch, fn, reps=10, warm=3):
     return statistics.median(x.elapsed_time(y) for x, y in ev)
 
 
+def _loop_ms(torch, fn, reps, warm=5):
+    """ms per call of `reps` calls back to back between one event pair."""
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps
+
+
+def measured_hbm():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"])
+    except Exception:
+        return 6650.0                  # /opt/skills/guides/B200_PROFILING.md fallback
+
+
 def measure_extras(tm, c, torch, stream):
     """SURVEY Sec 8(f) rows at WAN shapes, random data: f1 full 21-frame window,
     f2 fused sampler step (HBM roofline), f4 audio cross-attention."""
@@ -317,23 +339,59 @@ def measure_extras(tm, c, torch, stream):
     out["f1_window"] = {"workload": "21-latent-frame window, 7 chunks x 3072 tokens, 40 heads",
                         "ms": ms, "tflops": fl / (ms * 1e-3) / 1e12, "gflop": fl / 1e9}
     del q, k, v, o
-    # f2: one sampler step over 64 chunks' latents (16 ch x 3 x 64 x 64 each)
+    # f2: one sampler step over 64 chunks' latents (16 ch x 3 x 64 x 64 each).
+    # HBM-bound kernels: 4 operand sets rotated (x, v, x_bf16: 100 MB per set,
+    # 400 MB in all > the 126 MB L2), so every call streams from HBM; K calls
+    # back to back between one event pair.
     n = 64 * 16 * 3 * 64 * 64
-    x = torch.randn(n, device="cuda", generator=g)
-    vv = torch.randn(n, device="cuda", generator=g).to(bf)
-    xb = torch.empty(n, device="cuda", dtype=bf)
-    ms = _time_ms(torch, lambda: tm.tm_flow_sampler_step(ca.ctx, x, vv, tm.TM_BF16, n, 0.0, 0.5,
-                                                          seed=1, x_bf16_out=xb))
+    NS = 4
+    xs = [torch.randn(n, device="cuda", generator=g) for _ in range(NS)]
+    vs = [torch.randn(n, device="cuda", generator=g).to(bf) for _ in range(NS)]
+    xbs = [torch.empty(n, device="cuda", dtype=bf) for _ in range(NS)]
+    es = [torch.randn(n, device="cuda", generator=g) for _ in range(NS)]
+    cnt = [0]
+
+    def sampler():
+        i = cnt[0] % NS
+        cnt[0] += 1
+        tm.tm_flow_sampler_step(ca.ctx, xs[i], vs[i], tm.TM_BF16, n, 0.0, 0.5, seed=1,
+                                x_bf16_out=xbs[i])
+
+    def sampler_eps():
+        i = cnt[0] % NS
+        cnt[0] += 1
+        tm.tm_flow_sampler_step(ca.ctx, xs[i], vs[i], tm.TM_BF16, n, 0.0, 0.5, eps=es[i],
+                                x_bf16_out=xbs[i])
+
+    def euler():
+        i = cnt[0] % NS
+        cnt[0] += 1
+        tm.tm_flow_euler_step(ca.ctx, xs[i], vs[i], tm.TM_BF16, n, 0.5)
+
+    hbm = measured_hbm()
+    ms = _loop_ms(torch, sampler, 40)
     byts = n * (4 + 4 + 2 + 2)        # x read + write, v bf16, bf16 copy; noise in-kernel
     out["f2_sampler"] = {"workload": f"{n} elements (64 chunks of 16x3x64x64), in-kernel Philox",
                          "ms": ms, "gbs": byts / (ms * 1e-3) / 1e9, "bytes": byts,
-                         "bound": "hbm"}
+                         "frac_of_hbm": byts / (ms * 1e-3) / 1e9 / hbm, "bound": "hbm",
+                         "timing": f"40 calls back to back, {NS} operand sets rotated (> L2)",
+                         "note": "in-kernel Philox4x32-10 + Box-Muller with an accurate logf: "
+                                 "~50 instructions per element, issue-bound (ncu: issue slots "
+                                 "~70% busy); the caller-noise form below is the HBM-bound one"}
+    ms = _loop_ms(torch, sampler_eps, 40)
+    byts = n * (4 + 4 + 2 + 4 + 2)    # x read + write, v bf16, eps fp32, bf16 copy
+    out["f2_sampler_given_noise"] = {
+        "workload": f"{n} elements, noise eps passed by the caller (fp32)", "ms": ms,
+        "gbs": byts / (ms * 1e-3) / 1e9, "bytes": byts,
+        "frac_of_hbm": byts / (ms * 1e-3) / 1e9 / hbm, "bound": "hbm",
+        "timing": f"40 calls back to back, {NS} operand sets rotated (> L2)"}
     # a7 at the same size (report GB/s at n = 12.6 M)
-    ms = _time_ms(torch, lambda: tm.tm_flow_euler_step(ca.ctx, x, vv, tm.TM_BF16, n, 0.5))
+    ms = _loop_ms(torch, euler, 40)
     byts = n * (4 + 4 + 2)
     out["a7_euler_12.6M"] = {"ms": ms, "gbs": byts / (ms * 1e-3) / 1e9, "bytes": byts,
-                             "bound": "hbm"}
-    del x, vv, xb
+                             "frac_of_hbm": byts / (ms * 1e-3) / 1e9 / hbm, "bound": "hbm",
+                             "timing": f"40 calls back to back, {NS} operand sets rotated (> L2)"}
+    del xs, vs, xbs, es
     # f4: a chunk of 3 frames, 16x16 face region, 32 audio tokens per frame
     frames, T, A = 3, 1024, 32
     qa = torch.randn(frames, T, H, d, device="cuda", dtype=bf, generator=g)
@@ -342,11 +400,12 @@ def measure_extras(tm, c, torch, stream):
     oa = torch.empty_like(qa)
     face = torch.tensor([r * 32 + cc for r in range(8, 24) for cc in range(8, 24)], dtype=torch.int32,
                         device="cuda")
-    ms = _time_ms(torch, lambda: ca.audio(qa, ka, va, oa, face))
+    ms = _loop_ms(torch, lambda: ca.audio(qa, ka, va, oa, face), 40)
     fl = 4.0 * frames * face.numel() * 5 * A * d * H
     byts = (frames * T * H * d * 2) * 2 + 2 * frames * A * H * d * 2
     out["f4_audio"] = {"workload": "3 latent frames x 1024 tokens, 256 face tokens, window 5 x 32 "
                                    "audio tokens, 40 heads", "ms": ms,
+                       "timing": "40 calls back to back between one event pair",
                        "tflops": fl / (ms * 1e-3) / 1e12, "gbs_io": byts / (ms * 1e-3) / 1e9}
     ca.close()
     return out

@@ -1270,10 +1270,11 @@ int tail_bounds_runs(int nruns, const int* units, const int* tiles, int C, int m
         const char* e = getenv("TM_SCHED_ITEM_COST");
         return e ? float(atof(e)) : 3.f;
     }();
-    // A range that starts inside a unit holds a partner piece, whose partial
-    // the merger waits for: charged kPartialCost tiles so it finishes earlier.
-    static const float partial_cost = [] {
-        const char* e = getenv("TM_SCHED_PARTIAL_COST");
+    // A range whose LAST item is a partner piece (it starts inside its unit)
+    // ends with the partial write the unit's merger waits for: charged
+    // write_cost tiles, so the partial is in L2 when the merger is done.
+    static const float write_cost = [] {
+        const char* e = getenv("TM_SCHED_WRITE_COST");
         return e ? float(atof(e)) : 0.f;
     }();
     static const bool split_sched = [] {
@@ -1311,11 +1312,12 @@ int tail_bounds_runs(int nruns, const int* units, const int* tiles, int C, int m
         while (x < W) {
             if (g == G) return G + 1;
             const int start = x;
-            float cost = (x > 0 && unit_end(x - 1) != x) ? partial_cost : 0.f;
+            float cost = 0.f;
             while (x < W) {
                 const int ue = unit_end(x);
                 const float extra = x > start ? item_cost : 0.f;
-                const float avail = B - cost - extra;
+                const bool partner = x > 0 && unit_end(x - 1) == ue;   // starts inside its unit
+                const float avail = B - cost - extra - (partner ? write_cost : 0.f);
                 int take = int(avail);
                 if (take > ue - x) take = ue - x;
                 if (x > start && take < min_piece && take < ue - x) break;

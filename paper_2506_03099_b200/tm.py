@@ -477,22 +477,30 @@ class ChunkAttention:
 
     def audio(self, q, k_audio, v_audio, o, face_ids, window=5, stream=None):
         """q/o [B][frames][T][H][d], k/v [B][frames][A][H][d] (or without B for
-        batch 1); face_ids: torch int32 CUDA tensor.  Scratch allocated here."""
+        batch 1); face_ids: torch int32 CUDA tensor.  The scratch is allocated
+        here once per launch stream and reused (calls on one stream are
+        ordered, so a reuse never overlaps the previous call's kernels)."""
         import torch
         frames, T = q.shape[-4], q.shape[-3]
         A = k_audio.shape[-3]
         n = face_ids.numel()
         nb = tm_audio_scratch_bytes(self.ctx, frames, n)
-        scratch = torch.empty(nb + 1024, dtype=torch.uint8, device=q.device)
+        sh = _stream(stream)
+        cache = self.__dict__.setdefault("_audio_scratch", {})
+        scratch = cache.get(sh)
+        if scratch is None or scratch.numel() < nb + 1024:
+            if scratch is not None:
+                # the previous block may still be read by queued kernels of `sh`
+                scratch.record_stream(torch.cuda.ExternalStream(sh) if isinstance(sh, int)
+                                      else torch.cuda.current_stream())
+            scratch = torch.empty(nb + 1024, dtype=torch.uint8, device=q.device)
+            if isinstance(sh, int) and sh != torch.cuda.current_stream().cuda_stream:
+                # allocated on the current stream, used on `sh`
+                scratch.record_stream(torch.cuda.ExternalStream(sh))
+            cache[sh] = scratch
         ptr = (scratch.data_ptr() + 1023) // 1024 * 1024
         tm_audio_cross_attention(self.ctx, q, k_audio, v_audio, o, frames, T, A, face_ids, n,
-                                 window, ptr, nb, stream)
-        # the kernels queued on `stream` still read the scratch: keep the caching
-        # allocator from handing the block out before they are done
-        if isinstance(stream, torch.cuda.Stream):
-            scratch.record_stream(stream)
-        elif isinstance(stream, int) and stream != torch.cuda.current_stream().cuda_stream:
-            scratch.record_stream(torch.cuda.ExternalStream(stream))
+                                 window, ptr, nb, sh)
         return o
 
     def euler(self, x, v, v_dtype, dt, stream=None):
