@@ -229,11 +229,13 @@ tm_status tm_window_attention(tm_ctx* ctx, const void* q, const void* k, const v
  *   window: odd, <= 5; frames outside [0, frames) are clamped by repeating the
  *   boundary frame (SPEC S:117 design decision; frame 0 -> {0,0,0,1,2}).
  *   scratch: device, >= tm_audio_scratch_bytes(ctx, frames, n_face), 1024-B
- *   aligned (gathered face rows of q; fp32 mode also of o).
+ *   aligned (gathered face rows of q; fp32 mode also of o; bf16 mode the
+ *   inverse face map, 192 KiB).  Reused by the next call on the same stream.
  * n_face == 0 -> TM_ERR_DEGENERATE_MASK.  B, H, d, dtype, scale from
  * ctx (world_size 1).  bf16 launches: one prep kernel (gathers the face rows
- * of q, zeroes the non-face rows of o) and ONE attention launch for up to 16
- * frames whose epilogue writes each face row to o directly; T <= 49152.
+ * of q, writes the inverse face map) and ONE attention launch for up to 16
+ * frames whose epilogue writes each face row to o directly while its spare
+ * warp zeroes the non-face rows; T <= 49152.
  * fp32 mode: gather, one attention per frame, zero, scatter. */
 size_t tm_audio_scratch_bytes(const tm_ctx* ctx, int64_t frames, int64_t n_face);
 tm_status tm_audio_cross_attention(tm_ctx* ctx, const void* q, const void* k_audio,

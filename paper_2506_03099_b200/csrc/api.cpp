@@ -1051,10 +1051,13 @@ tm_status tm_window_attention(tm_ctx* ctx, const void* q, const void* k, const v
                        cs, "tm_window_attention");
 }
 
+// Layout: the gathered face rows of q | O staging of the fp32 mode (the same
+// size) | the inverse face map (bf16 mode; up to 49152 tokens per frame).
 size_t tm_audio_scratch_bytes(const tm_ctx* ctx, int64_t frames, int64_t n_face) {
     if (!ctx || frames <= 0 || n_face <= 0) return 0;
     const size_t rows = size_t(ctx->cfg.batch) * frames * n_face;
-    return 2 * align_up(rows * ctx->cfg.heads * ctx->cfg.head_dim * ctx->lay.esize);
+    return 2 * align_up(rows * ctx->cfg.heads * ctx->cfg.head_dim * ctx->lay.esize) +
+           align_up(size_t(49152) * 4);
 }
 
 tm_status tm_audio_cross_attention(tm_ctx* ctx, const void* q, const void* k_audio,
@@ -1089,7 +1092,9 @@ tm_status tm_audio_cross_attention(tm_ctx* ctx, const void* q, const void* k_aud
     const int row = cf.heads * cf.head_dim * ctx->lay.esize;          // bytes per token
     const int64_t BF = int64_t(cf.batch) * frames;
     uint8_t* qf = static_cast<uint8_t*>(scratch);
-    uint8_t* of = qf + tm_audio_scratch_bytes(ctx, frames, n_face) / 2;   // 1024-B aligned half
+    const size_t half = align_up(size_t(cf.batch) * frames * n_face * cf.heads * cf.head_dim * ctx->lay.esize);
+    uint8_t* of = qf + half;                                          // 1024-B aligned
+    int32_t* inv = reinterpret_cast<int32_t*>(qf + 2 * half);         // bf16: token -> face slot
     cudaStream_t cs = static_cast<cudaStream_t>(stream);
     ctx->launches = 0;
     const uint8_t* kb = static_cast<const uint8_t*>(k_audio);
@@ -1115,18 +1120,19 @@ tm_status tm_audio_cross_attention(tm_ctx* ctx, const void* q, const void* k_aud
     };
     tm_status st;
     if (cf.dtype == TM_BF16) {
-        // Two kinds of launch: (1) gather the face rows of q into scratch and
-        // zero the non-face rows of o (they get no audio update);
-        // (2) every frame's face rows attend its audio window as problems of
-        // ONE attention launch (up to kMaxProblems frames per launch) whose
-        // epilogue writes each face row straight to its token row of o.
+        // Two launches: (1) gather the face rows of q into scratch and write the
+        // inverse face map; (2) every frame's face rows attend its audio window
+        // as problems of ONE attention launch (up to kMaxProblems frames per
+        // launch) whose epilogue writes each face row straight to its token row
+        // of o, while its spare warp zeroes the non-face rows (they get no audio
+        // update).
         static const int dbg_parts = [] {   // timing experiments only: 1 prep only, 2 attention only
             const char* e = getenv("TM_DBG_AUDIO_PART");
             return e ? atoi(e) : 0;
         }();
         if (dbg_parts != 2) {
-            st = cuda_check(launch_audio_prep(q, qf, o, face_ids, BF, tokens_per_frame, n_face, row, cs,
-                                              &ctx->launches), "audio prep (face gather, zero fill)");
+            st = cuda_check(launch_audio_prep(q, qf, inv, face_ids, BF, tokens_per_frame, n_face, row, cs,
+                                              &ctx->launches), "audio prep (face gather, face map)");
             if (st) return st;
         }
         for (int64_t f0 = 0; f0 < frames && dbg_parts != 1; f0 += kMaxProblems) {
@@ -1139,12 +1145,16 @@ tm_status tm_audio_cross_attention(tm_ctx* ctx, const void* q, const void* k_aud
             mp.kv_rows = frames * audio_tokens_per_frame;
             mp.o_rows = frames * tokens_per_frame;
             mp.o_row_map = face_ids;
+            mp.zero_inv = dbg_parts == 2 ? nullptr : inv;
+            mp.zero_T = tokens_per_frame;
+            mp.zero_row0 = f0 * tokens_per_frame;
             mp.B = cf.batch;
             mp.H = cf.heads;
             mp.d = cf.head_dim;
             mp.scale = ctx->scale;
             mp.sched_heads = cf.sched_heads;
             mp.nprob = int(std::min<int64_t>(kMaxProblems, frames - f0));
+            mp.zero_rows = mp.nprob * tokens_per_frame;
             for (int i = 0; i < mp.nprob; ++i) {
                 const int64_t f = f0 + i;
                 SubProblem& sp = mp.prob[i];

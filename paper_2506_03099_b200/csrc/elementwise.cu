@@ -212,52 +212,47 @@ __global__ void __launch_bounds__(256) face_rows_kernel(const uint4* __restrict_
     }
 }
 
-// f4 preparation (one pass over every token row of q / o, rows of W 16-byte
-// words): face rows of q are gathered, qf[bf][i] = q[bf][ids[i]], and the
-// non-face rows of o are zeroed (they receive no audio update);
-// the attention launch then writes the face rows of o itself (its epilogue
-// scatters through ids).  Each CTA builds the inverse map token -> face slot
-// in shared memory (T ints; ids outside [0, T) are ignored).
-__global__ void __launch_bounds__(512) audio_prep_kernel(const uint4* __restrict__ q,
+// f4 preparation: the face rows of q are gathered, qf[bf][i] = q[bf][ids[i]]
+// (one warp per face row, rows of W 16-byte words), and CTA 0 writes the
+// inverse map inv[t] = a face slot of token t, or -1 (ids outside [0, T) are
+// ignored).  The attention launch then writes the face rows of o through ids
+// and zeroes the non-face rows (inv[t] < 0: no audio update)
+// with its spare warp while it attends.  Launched with PDL.
+__global__ void __launch_bounds__(128) audio_prep_kernel(const uint4* __restrict__ q,
                                                          uint4* __restrict__ qf,
-                                                         uint4* __restrict__ o,
+                                                         int32_t* __restrict__ inv_out,
                                                          const int32_t* __restrict__ ids,
                                                          int64_t BF, int T, int nf, int W) {
     extern __shared__ int inv[];
-    for (int t = threadIdx.x; t < T; t += blockDim.x) inv[t] = -1;
-    __syncthreads();
-    for (int i = threadIdx.x; i < nf; i += blockDim.x) {
-        const int t = ids[i];
-        if (t >= 0 && t < T) inv[t] = i;      // duplicates: any one slot (same row, same output)
+    asm volatile("griddepcontrol.wait;" ::: "memory");   // PDL: after the previous grid
+    if (blockIdx.x == 0) {
+        for (int t = threadIdx.x; t < T; t += blockDim.x) inv[t] = -1;
+        __syncthreads();
+        for (int i = threadIdx.x; i < nf; i += blockDim.x) {
+            const int t = ids[i];
+            if (t >= 0 && t < T) inv[t] = i;      // duplicates: any one slot (same row, same output)
+        }
+        __syncthreads();
+        for (int t = threadIdx.x; t < T; t += blockDim.x) inv_out[t] = inv[t];
     }
-    __syncthreads();
-    // One warp per token row (the branch is warp-uniform); lanes stride over
-    // the row's W 16-byte words, two in flight per lane.
+    // One warp per face row; lanes stride over the row's W 16-byte words,
+    // 8 loads in flight per lane before the stores.
     const int lane = threadIdx.x & 31;
-    const int64_t rows = BF * T;
+    const int64_t rows = BF * nf;
     const int64_t wstride = int64_t(gridDim.x) * (blockDim.x >> 5);
     for (int64_t r = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += wstride) {
-        const int t = int(r % T);
-        const int i = inv[t];
-        uint4* orow = o + r * W;
-        if (i >= 0) {
-            const uint4* src = q + r * W;
-            uint4* dst = qf + ((r / T) * nf + i) * W;
-            // 8 loads in flight per lane before the stores (a 10 KB row is then
-            // one L2 round trip, not W/64 dependent ones)
-            for (int w0 = lane; w0 < W; w0 += 256) {
-                uint4 v[8];
+        const int t = ids[r % nf];
+        if (t < 0 || t >= T) continue;
+        const uint4* src = q + ((r / nf) * T + t) * W;
+        uint4* dst = qf + r * W;
+        for (int w0 = lane; w0 < W; w0 += 256) {
+            uint4 v[8];
 #pragma unroll
-                for (int u = 0; u < 8; ++u)
-                    if (w0 + 32 * u < W) v[u] = __ldcs(src + w0 + 32 * u);
+            for (int u = 0; u < 8; ++u)
+                if (w0 + 32 * u < W) v[u] = __ldcs(src + w0 + 32 * u);
 #pragma unroll
-                for (int u = 0; u < 8; ++u)
-                    if (w0 + 32 * u < W) dst[w0 + 32 * u] = v[u];
-            }
-        } else {
-            const uint4 z = make_uint4(0, 0, 0, 0);
-#pragma unroll 4
-            for (int w = lane; w < W; w += 32) __stcs(orow + w, z);
+            for (int u = 0; u < 8; ++u)
+                if (w0 + 32 * u < W) dst[w0 + 32 * u] = v[u];
         }
     }
 }
@@ -348,7 +343,7 @@ cudaError_t launch_face_rows(const void* src, void* dst, const int32_t* ids, int
     return cudaGetLastError();
 }
 
-cudaError_t launch_audio_prep(const void* q, void* qf, void* o, const int32_t* ids, int64_t BF,
+cudaError_t launch_audio_prep(const void* q, void* qf, int32_t* inv, const int32_t* ids, int64_t BF,
                               int64_t T, int64_t nf, int row_bytes, cudaStream_t s, int* launches) {
     if (row_bytes % 16 || T <= 0 || T > 49152 || nf <= 0) return cudaErrorInvalidValue;
     const int W = row_bytes / 16;
@@ -358,12 +353,13 @@ cudaError_t launch_audio_prep(const void* q, void* qf, void* o, const int32_t* i
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         if (e != cudaSuccess) return e;
     }
-    // rows over the warps of <= 2 CTAs per SM (the face map is built once per CTA)
-    const unsigned grid = grid_for(BF * T, 16, 2);
-    audio_prep_kernel<<<grid, 512, smem, s>>>(static_cast<const uint4*>(q), static_cast<uint4*>(qf),
-                                              static_cast<uint4*>(o), ids, BF, int(T), int(nf), W);
-    if (launches) ++*launches;
-    return cudaGetLastError();
+    // face rows over the 4 warps of <= 4 CTAs per SM (one row per warp: the
+    // gather is spread over every SM)
+    const unsigned grid = grid_for(BF * nf, 4, 4);
+    return finish(launch_pdl(audio_prep_kernel, dim3(grid), dim3(128), smem, s,
+                             static_cast<const uint4*>(q), static_cast<uint4*>(qf), inv, ids, BF,
+                             int(T), int(nf), W),
+                  launches);
 }
 
 cudaError_t launch_nonfinite(const void* x, int is_bf16, int64_t n, int* flag, cudaStream_t s,

@@ -161,6 +161,12 @@ struct __align__(64) FmhaParams {
     int dbg_nomerge;                  // timing experiments only (TM_DBG_NOMERGE=1): pieces store unmerged
     int64_t o_bstride;                // rows between batch elements of an o_dst
     int o_rows, o_H, o_h0;
+    // f4 zero fill (spare warp, concurrent with the attention): rows r in
+    // [zf_row0, zf_row0 + zf_rows) of each batch element of o_dst[0] whose token
+    // r % zf_T has zf_inv[token] < 0 are zeroed (no audio update).
+    const int* zf_inv;
+    int zf_T;
+    int64_t zf_row0, zf_rows;
     // Peer transport: waits on the own counters before Q tiles (T=0)
     // and before tiles of segment wait_seg (K: T=1, V: T=2); fused push of
     // this rank's shard at kernel start; done signal at kernel end.
@@ -576,10 +582,16 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_holder;
+#ifdef TM_SPANS_PROLOGUE
+    if (threadIdx.x == 0) trace_span(p, 4);   // (spans A/B) prologue done
+#endif
     // Programmatic dependent launch: everything above (barriers, TMEM, tensor-map
     // prefetch) overlaps the previous kernel's tail; no global data is touched
     // before the previous grid has completed.  (No-op without the attribute.)
     asm volatile("griddepcontrol.wait;" ::: "memory");
+#ifdef TM_SPANS_PROLOGUE
+    if (threadIdx.x == 0) trace_span(p, 5);   // (spans A/B) previous grid complete
+#endif
     if (p.push) {
         // a2 fused.  All 384 threads store this rank's shard of Q into the owners'
         // windows (NVLink stores).  Then warp 10 alone releases Q (a system-scope
@@ -739,6 +751,19 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
             }
         }
         if (lane == 0) mbar_arrive(store_idle);   // the ring is no longer read by TMA stores
+        if (p.zf_inv != nullptr) {
+            // f4: zero the non-face rows of o, this CTA's share (warp-uniform branch)
+            const int words = p.o_H * D / 8;                  // 16-B words per token row
+            const int64_t total = int64_t(p.B) * p.zf_rows;
+            const uint4 z = make_uint4(0, 0, 0, 0);
+            for (int64_t r = blockIdx.x; r < total; r += gridDim.x) {
+                const int64_t b = r / p.zf_rows, rr = p.zf_row0 + r % p.zf_rows;
+                if (__ldg(p.zf_inv + rr % p.zf_T) >= 0) continue;
+                uint4* row = reinterpret_cast<uint4*>(p.o_dst[0] + (b * p.o_bstride + rr) * int64_t(p.o_H) * D);
+#pragma unroll 4
+                for (int w = lane; w < words; w += 32) __stcs(row + w, z);
+            }
+        }
       } else if (warp == 9 || warp == 11) {
         // ------------------------------------------------ MMA issuers
         // Two independent issuers so that neither waits behind the other:
@@ -1610,6 +1635,11 @@ cudaError_t launch_fmha_sm100_multi(const MultiProblem& mp, void* scratch, cudaS
     p.o_dst[0] = static_cast<uint16_t*>(mp.o);
     p.o_bstride = mp.o_bstride > 0 ? mp.o_bstride : mp.o_rows;
     p.o_row_map = mp.o_row_map;
+    p.zf_inv = mp.zero_inv;
+    p.zf_T = int(mp.zero_T);
+    p.zf_row0 = mp.zero_row0;
+    p.zf_rows = mp.zero_rows;
+    if (p.zf_inv && (p.zf_T <= 0 || p.zf_rows <= 0)) return cudaErrorInvalidValue;
     p.tma_epi = 0;
     if (tma_epi_enabled() && !mp.o_row_map &&
         make_map(&p.to, mp.o, mp.d, mp.H, mp.o_rows, mp.B, p.o_bstride, 32))
@@ -1645,6 +1675,7 @@ cudaError_t launch_fmha_sm100_multi(const MultiProblem& mp, void* scratch, cudaS
             cudaError_t e = finish_and_launch(p, mp.d, launch_grid(p), scratch, stream, launches,
                                               trace, false);
             if (e != cudaSuccess) return e;
+            p.zf_inv = nullptr;               // the first launch zero-filled
             p.nblk = 0;
             p.ncls = 0;
             if (!add_block(p, i, h0, hb, C, &full)) return cudaErrorInvalidValue;

@@ -132,6 +132,10 @@ struct MultiProblem {
     void* o = nullptr;
     int64_t q_rows = 0, q_bstride = 0, kv_rows = 0, kv_bstride = 0, o_rows = 0, o_bstride = 0;
     const int32_t* o_row_map = nullptr;   // device, nullable
+    // f4: rows r of o ([B][o_rows] x H x d, o_rows = frames * zero_T) whose token
+    // r % zero_T has zero_inv[token] < 0 are zeroed by the launch (device, nullable)
+    const int32_t* zero_inv = nullptr;
+    int64_t zero_T = 0, zero_row0 = 0, zero_rows = 0;   // rows [zero_row0, +zero_rows) of each batch
     int B = 1, H = 1, d = 128;
     float scale = 0.f;
     int nprob = 0;
@@ -188,9 +192,10 @@ cudaError_t launch_sampler(float* x, const void* v, int v_is_bf16, const float* 
 // f4: gather (scatter = 0) / scatter (1) of face-token rows, ids device int32.
 cudaError_t launch_face_rows(const void* src, void* dst, const int32_t* ids, int64_t BF, int64_t T,
                             int64_t nf, int row_bytes, int scatter, cudaStream_t s, int* launches);
-// f4 (bf16): gather the face rows of q into qf and zero the non-face rows of o
-// (the attention epilogue writes the face rows); T <= 49152.
-cudaError_t launch_audio_prep(const void* q, void* qf, void* o, const int32_t* ids, int64_t BF,
+// f4 (bf16): gather the face rows of q into qf and write the inverse face map
+// inv[T] (token -> face slot or -1); the attention launch writes the face rows
+// of o and zeroes the others (MultiProblem::zero_inv); T <= 49152.
+cudaError_t launch_audio_prep(const void* q, void* qf, int32_t* inv, const int32_t* ids, int64_t BF,
                               int64_t T, int64_t nf, int row_bytes, cudaStream_t s, int* launches);
 // Non-finite check: sets *flag (device int) to 1 if any element is NaN/Inf.
 cudaError_t launch_nonfinite(const void* x, int is_bf16, int64_t n, int* flag, cudaStream_t s,
