@@ -312,6 +312,31 @@ def _loop_ms(torch, fn, reps, warm=5):
     return a.elapsed_time(b) / reps
 
 
+def _graph_ms(torch, fn, reps, R=5):
+    """ms per call of `reps` calls captured in one CUDA graph, replayed R times
+    (median): the GPU time without host work between launches."""
+    fn()
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        for _ in range(reps):
+            fn()
+    g.replay()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(R):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        g.replay()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b) / reps)
+    del g
+    return statistics.median(ts)
+
+
 def measured_hbm():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -400,12 +425,16 @@ def measure_extras(tm, c, torch, stream):
     oa = torch.empty_like(qa)
     face = torch.tensor([r * 32 + cc for r in range(8, 24) for cc in range(8, 24)], dtype=torch.int32,
                         device="cuda")
-    ms = _loop_ms(torch, lambda: ca.audio(qa, ka, va, oa, face), 40)
+    ms = _loop_ms(torch, lambda: ca.audio(qa, ka, va, oa, face, stream=stream), 40)
+    ms_g = _graph_ms(torch, lambda: ca.audio(qa, ka, va, oa, face), 40)
     fl = 4.0 * frames * face.numel() * 5 * A * d * H
     byts = (frames * T * H * d * 2) * 2 + 2 * frames * A * H * d * 2
     out["f4_audio"] = {"workload": "3 latent frames x 1024 tokens, 256 face tokens, window 5 x 32 "
-                                   "audio tokens, 40 heads", "ms": ms,
-                       "timing": "40 calls back to back between one event pair",
+                                   "audio tokens, 40 heads", "ms": ms, "ms_graph": ms_g,
+                       "launches_per_call": ca.launches,
+                       "timing": "40 calls from Python back to back between one event pair (the "
+                                 "host enqueues faster than the GPU runs them); ms_graph: the same "
+                                 "40 calls captured in one CUDA graph and replayed",
                        "tflops": fl / (ms * 1e-3) / 1e12, "gbs_io": byts / (ms * 1e-3) / 1e9}
     ca.close()
     return out
@@ -459,10 +488,12 @@ def cpu_baseline(c, rows):
                                          "one_core": dt1 * c["Lc"] / one_rows}}
 
 
-def attention_loop(tm, torch, H, d, Lr, Lc, K, stream, zero_copy=False, NL=8, NB=4, sched_heads=0):
+def attention_loop(tm, torch, H, d, Lr, Lc, K, stream, zero_copy=False, NL=8, NB=4, sched_heads=0,
+                   R=3, idle=0.0):
     """ms per chunk-attention call (t >= 2) of a fresh H-head context: K calls
-    back to back between one event pair, operands rotated over NL layer caches
-    and NB input sets (larger than L2); fused c_t append unless zero_copy."""
+    back to back between one event pair (median of R such loops), operands
+    rotated over NL layer caches and NB input sets (larger than L2); fused c_t
+    append unless zero_copy."""
     bf = torch.bfloat16
     g = torch.Generator(device="cuda").manual_seed(2506030990 + 55 + H)
     ca = tm.ChunkAttention(H, d, Lr, Lc, NL, 1, sched_heads=sched_heads)
@@ -487,15 +518,20 @@ def attention_loop(tm, torch, H, d, Lr, Lc, K, stream, zero_copy=False, NL=8, NB
     for i in range(3 * NL):
         call(i)
     torch.cuda.synchronize()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record(stream)
-    for i in range(K):
-        call(i)
-    b.record(stream)
-    torch.cuda.synchronize()
+    ts = []
+    for _ in range(R):
+        if idle > 0:
+            time.sleep(idle)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for i in range(K):
+            call(i)
+        b.record(stream)
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b) / K)
     ca.close()
     del sets
-    return a.elapsed_time(b) / K
+    return statistics.median(ts)
 
 
 def measure_other_configs(tm, torch, main, K, stream):
@@ -508,13 +544,17 @@ def measure_other_configs(tm, torch, main, K, stream):
         if name == main:
             continue
         cc = CONFIGS[name]
-        ms = attention_loop(tm, torch, cc["H"], cc["d"], cc["Lr"], cc["Lc"], K, stream)
+        # as long as the main timed region (~13 ms: a burst, not power-capped),
+        # each of R = 3 loops after a 0.5 s idle
+        Kc = max(3, int(round(K * flop_per_call(CONFIGS[main]) / flop_per_call(cc))))
+        ms = attention_loop(tm, torch, cc["H"], cc["d"], cc["Lr"], cc["Lc"], Kc, stream, idle=0.5)
         fl = flop_per_call(cc)
         out[name] = {"workload": cc["workload"], "keys_attended": cc["Lr"] + 2 * cc["Lc"],
                      "ms_per_call": ms, "tflops": fl / (ms * 1e-3) / 1e12,
                      "frac_of_bf16_peak": fl / (ms * 1e-3) / 1e12 / peak,
                      "gflop_per_call": fl / 1e9,
-                     "timing": f"{K} calls (fused append) between one event pair"}
+                     "timing": f"{Kc} calls (fused append; the main region's FLOP) between one "
+                               "event pair, median of 3 loops each after a 0.5 s idle"}
         torch.cuda.empty_cache()
     return out
 
@@ -530,27 +570,37 @@ def measure_shards(tm, torch, c, K, stream, t1_ms):
     the fused append (as the P > 1 call runs it) and zero-copy, and the scaling
     MODEL E(P) = t(1) / (P t(P)), t(P) = shard kernel + exposed Q push (remote
     share of this rank's Q shard at the measured 770 GB/s peer copy) + 1 us
-    done barrier.  A model from one-GPU numbers, not a multi-GPU measurement."""
+    done barrier.  A model from one-GPU numbers, not a multi-GPU measurement.
+    t(1) is re-measured with each shard (same loop, both after a 0.5 s idle:
+    sustained loops run power-capped and a small-H loop right after a 40-head
+    loop reads up to 20 % slow while the clocks recover, so t(1) and t(P) are
+    only comparable when taken the same way; tools/dbg/shard_vs_bench.py)."""
     H, d, Lr, Lc = c["H"], c["d"], c["Lr"], c["Lc"]
     out = {"model": "t(P) = shard kernel (fused append) + exposed Q push at "
                     f"{NVLINK_PEER_GBS:.0f} GB/s + 1 us; E(P) = t(1) / (P t(P)); "
-                    "t(1) = this run's attention-only loop", "t1_ms": t1_ms}
+                    "t(1) = the 40-head loop timed with each shard, both after a 0.5 s idle",
+           "t1_ms_live": t1_ms}
     for P in (2, 4, 8):
         Hs = H // P
+        time.sleep(0.5)
         ms = attention_loop(tm, torch, Hs, d, Lr, Lc, K, stream)
         ms_zc = attention_loop(tm, torch, Hs, d, Lr, Lc, K, stream, zero_copy=True)
+        time.sleep(0.5)
+        t1 = attention_loop(tm, torch, H, d, Lr, Lc, K, stream)
         Ls = -(-Lc // P)
         q_push_us = Ls * H * d * 2 * (P - 1) / P / (NVLINK_PEER_GBS * 1e3)
         t = ms + (q_push_us + 1.0) * 1e-3
         fl = flop_per_call(c) / P
-        out[f"h{Hs}"] = {"P": P, "heads": Hs, "ms_fused_append": ms, "ms_zero_copy": ms_zc,
+        out[f"h{Hs}"] = {"P": P, "heads": Hs, "t1_ms": t1, "ms_fused_append": ms,
+                         "ms_zero_copy": ms_zc,
                          "tflops_fused_append": fl / (ms * 1e-3) / 1e12,
                          "tflops_zero_copy": fl / (ms_zc * 1e-3) / 1e12,
                          "q_push_us_model": q_push_us, "t_model_ms": t,
-                         "E_model": t1_ms / (P * t)}
+                         "E_model": t1 / (P * t), "E_kernel_only": t1 / (P * ms)}
     # P-invariant schedule (tm_config.sched_heads = H/8: every 5 heads scheduled
     # as a block of their own, bitwise equal outputs for P = 1, 2, 4, 8): its
     # cost at P = 1 against the default schedule, the same loop back to back.
+    time.sleep(0.5)
     base = attention_loop(tm, torch, H, d, Lr, Lc, K, stream)
     inv = attention_loop(tm, torch, H, d, Lr, Lc, K, stream, sched_heads=H // 8)
     out["p_invariant_p1"] = {"sched_heads": H // 8, "ms_default": base, "ms_p_invariant": inv,
@@ -874,6 +924,28 @@ def main():
                "note": "pinned host buffers, copies in the timed region, double-buffered streams; "
                        "link_bound = the step's H2D bytes alone over the measured H2D rate"}
 
+    # ---------------------------------------------------------------- SURVEY Sec 8(f) rows,
+    # the other single-GPU configs and one P = 2/4/8 rank's share: short loops,
+    # measured before the long streaming run (which holds the GPU at its power
+    # cap for seconds), each with the SM clocks sampled during it.
+    extras = others = shards = None
+    if not args.no_extras and P == 1:
+        xclk = ClockSampler(local)
+        xclk.start()
+        x0 = time.time()
+        extras = measure_extras(tm, c, torch, stream)
+        x1 = time.time()
+        others = measure_other_configs(tm, torch, args.config, max(10, args.steps), stream)
+        x2 = time.time()
+        if args.config == "wan512":
+            shards = measure_shards(tm, torch, c, max(10, args.steps), stream, live_ms)
+        x3 = time.time()
+        xclk.stop()
+        extras["clocks"] = xclk.summary(window=(x0, x1))
+        others["clocks"] = xclk.summary(window=(x1, x2))
+        if shards is not None:
+            shards["clocks"] = xclk.summary(window=(x2, x3))
+
     streaming = None
     if args.stream_chunks >= 2:
         # BJ.configs[3]: chunk-by-chunk generation in the real dependency order,
@@ -907,13 +979,6 @@ def main():
                      "attention_calls_per_chunk": NLs * NS,
                      "tflops": NLs * NS * flop_per_call(c) / (s_ms * 1e-3) / 1e12}
         sc.close()
-
-    extras = others = shards = None
-    if not args.no_extras and P == 1:
-        extras = measure_extras(tm, c, torch, stream)
-        others = measure_other_configs(tm, torch, args.config, max(10, args.steps), stream)
-        if args.config == "wan512":
-            shards = measure_shards(tm, torch, c, max(10, args.steps), stream, live_ms)
 
     fl = flop_per_call(c)
     ms_step = ms_total / args.steps

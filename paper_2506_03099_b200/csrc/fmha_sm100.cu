@@ -1260,8 +1260,8 @@ cudaError_t launch_t(const FmhaParams& p, int grid, cudaStream_t stream) {
 // (step +0.4 %, zero-copy alone +0.9 %, streaming +0.3 %;
 // profiles/r1_v21_poly_ab.txt), so the default is 1/16.
 // TM_POLY selects a split for tuning: 1 = all MUFU, 2 = 2/16, 3 = 3/16,
-// 4 = 4/16, 5 = 1/16 (default).
-constexpr uint32_t kPolyDefault = 0x0808u;   // pairs {3, 11} of every 16 (TM_POLY=2)
+// 4 = 4/16, 5 = 1/16 (the default, also when TM_POLY is unset).
+constexpr uint32_t kPoly2of16 = 0x0808u;     // pairs {3, 11} of every 16 (TM_POLY=2)
 template <int D>
 cudaError_t launch_d(const FmhaParams& p, int grid, cudaStream_t stream) {
     static int env_sel = [] {
@@ -1274,7 +1274,7 @@ cudaError_t launch_d(const FmhaParams& p, int grid, cudaStream_t stream) {
         case 3: return launch_t<D, 0x1084u>(p, grid, stream);   // {2,7,12}
         case 5: return launch_t<D, 0x0800u>(p, grid, stream);   // {11}: 1/16
         case 4: return launch_t<D, 0x4444u>(p, grid, stream);   // {2,6,10,14}
-        default: return launch_t<D, kPolyDefault>(p, grid, stream);
+        default: return launch_t<D, kPoly2of16>(p, grid, stream);
     }
 }
 

@@ -335,6 +335,30 @@ def test_philox_normal_moments():
     assert abs(np.mean(z ** 4) - 3) < 0.03            # Gaussian kurtosis
 
 
+def test_philox_normal_word_mapping_by_polar_identities():
+    """Reading Q18: element i takes word i % 4 of the Philox
+    block at counter (i // 4, 0, offset_lo, offset_hi), uniforms (w + 0.5)/2^32,
+    Box-Muller pairs (w0, w1) and (w2, w3) with the radius from the first word
+    and the angle from the second, cos on the even element.  Pinned through the
+    polar decomposition of each output pair against the KAT-pinned Philox words:
+    z_2j^2 + z_2j+1^2 = -2 ln u_2j and atan2(z_2j+1, z_2j) = 2 pi u_2j+1 (mod 2 pi),
+    so a swapped sin/cos, another word pairing, a radius/angle word swap or a
+    different counter layout fails."""
+    seed, offset, n = 0x1234ABCD5678, (7 << 32) | 3, 4096
+    z = oracle.philox_normal(n, seed, offset).reshape(-1, 4)
+    blk = np.arange(n // 4, dtype=np.uint64)
+    ctr = np.stack([(blk & np.uint64(0xFFFFFFFF)).astype(np.uint32), (blk >> np.uint64(32)).astype(np.uint32),
+                    np.full(n // 4, 3, np.uint32), np.full(n // 4, 7, np.uint32)], axis=1)
+    key = np.tile(np.array([[seed & 0xFFFFFFFF, seed >> 32]], dtype=np.uint32), (n // 4, 1))
+    u = (oracle.philox4x32_10(ctr, key).astype(np.float64) + 0.5) / 2.0 ** 32
+    for a, b in ((0, 1), (2, 3)):
+        r2 = z[:, a] ** 2 + z[:, b] ** 2
+        assert np.abs(r2 - (-2.0 * np.log(u[:, a]))).max() < 1e-9 * np.maximum(1.0, r2).max()
+        ang = np.mod(np.arctan2(z[:, b], z[:, a]), 2 * np.pi)
+        d = np.abs(ang - 2 * np.pi * u[:, b])
+        assert np.minimum(d, 2 * np.pi - d).max() < 1e-9
+
+
 # --------------------------------------------------------------------------
 # f4: audio cross-attention with face-region query mask (P:123-125, S:112-129)
 # --------------------------------------------------------------------------
@@ -417,3 +441,32 @@ def test_sampler_u_one_fixture_matches_oracle_philox():
         key = np.array([[g["seed"] & 0xFFFFFFFF, g["seed"] >> 32]], dtype=np.uint32)
         w = int(oracle.philox4x32_10(ctr, key)[0, h["word"]])
         assert w == h["w"] and w >= 2**32 - 128
+
+
+def test_philox_normal_pin_catches_mapping_mutants():
+    """Pin strength for the word mapping: sin/cos swapped, pairs (w0, w2) /
+    (w1, w3), radius and angle words swapped -- each breaks an identity of
+    test_philox_normal_word_mapping_by_polar_identities."""
+    n = 1024
+    z = oracle.philox_normal(n, 99, 5).reshape(-1, 4)
+    blk = np.arange(n // 4, dtype=np.uint32)
+    ctr = np.stack([blk, np.zeros_like(blk), np.full_like(blk, 5), np.zeros_like(blk)], axis=1)
+    key = np.tile(np.array([[99, 0]], dtype=np.uint32), (n // 4, 1))
+    u = (oracle.philox4x32_10(ctr, key).astype(np.float64) + 0.5) / 2.0 ** 32
+
+    def ok(zz):
+        r2 = zz[:, 0] ** 2 + zz[:, 1] ** 2
+        ang = np.mod(np.arctan2(zz[:, 1], zz[:, 0]), 2 * np.pi)
+        d = np.abs(ang - 2 * np.pi * u[:, 1])
+        return (np.abs(r2 + 2.0 * np.log(u[:, 0])).max() < 1e-9 and np.minimum(d, 2 * np.pi - d).max() < 1e-9)
+
+    assert ok(z)
+    r_a, r_b = np.sqrt(-2 * np.log(u[:, 0])), np.sqrt(-2 * np.log(u[:, 1]))
+    mutants = {
+        "sin_cos_swapped": np.stack([r_a * np.sin(2 * np.pi * u[:, 1]), r_a * np.cos(2 * np.pi * u[:, 1])], 1),
+        "radius_angle_words_swapped": np.stack([r_b * np.cos(2 * np.pi * u[:, 0]),
+                                                r_b * np.sin(2 * np.pi * u[:, 0])], 1),
+        "pairing_w0_w2": np.stack([r_a * np.cos(2 * np.pi * u[:, 2]), r_a * np.sin(2 * np.pi * u[:, 2])], 1),
+    }
+    for name, zz in mutants.items():
+        assert not ok(zz), name

@@ -13,9 +13,10 @@ import torch  # noqa: E402
 from paper_2506_03099_b200 import tm  # noqa: E402
 
 
-def stream(H, d, Lr, Lc, dtype, transport=tm.TM_TRANSPORT_NCCL, zero_copy=False):
+def stream(H, d, Lr, Lc, dtype, transport=tm.TM_TRANSPORT_NCCL, zero_copy=False, sched_heads=0):
     dt = torch.bfloat16 if dtype == tm.TM_BF16 else torch.float32
-    ca = tm.ChunkAttention(H, d, Lr, Lc, 1, 1, dtype=dtype, transport=transport)
+    ca = tm.ChunkAttention(H, d, Lr, Lc, 1, 1, dtype=dtype, transport=transport,
+                           sched_heads=sched_heads)
     mk = lambda L: torch.randn(L, H, d, device="cuda", dtype=dt)
     ca.put_reference(0, 0, mk(Lr), mk(Lr))
     for t in (1, 2, 3):
@@ -41,6 +42,8 @@ stream(2, 128, 200, 300, tm.TM_BF16, transport=tm.TM_TRANSPORT_PEER)
 stream(1, 128, 1024, 512, tm.TM_BF16)
 stream(1, 64, 1024, 512, tm.TM_BF16)
 stream(1, 128, 8192, 256, tm.TM_BF16)
+# schedule blocks (tm_config.sched_heads): 4 blocks of one head in one launch
+stream(4, 128, 1024, 512, tm.TM_BF16, sched_heads=1)
 # f1 window, f4 audio, a7 Euler, f2 sampler
 H, d = 2, 128
 ca = tm.ChunkAttention(H, d, 16, 16, 1, 1)
