@@ -95,6 +95,26 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
     return c;
 }
 
+// t = -2 ln u for u = (w + 0.5) 2^-32 with relative accuracy ~2^-21 over the
+// whole range, in ~12 instructions instead of the accurate logf's ~25: MUFU
+// lg2 where u <= 15/16 (|ln u| >= 0.065, so its 2^-22 relative error stays
+// relative); near 1 the series -ln(1 - d) = d + d^2/2 + ... + d^6/6 with
+// d = 1 - u taken from the integer ~w = 2^32 - 1 - w (no cancellation;
+// truncation < 1e-8 relative for d < 1/16).  Also finite where u itself
+// rounds to 1 in fp32 (d = 2^-33 for w = 2^32 - 1).
+__device__ __forceinline__ float neg2_log_u(uint32_t w, float u) {
+    constexpr float k32 = 2.3283064365386963e-10f;      // 2^-32
+    float lg;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(lg) : "f"(u));
+    const float d = fmaf(float(~w), k32, 0.5f * k32);
+    float sr = fmaf(d, 1.f / 6.f, 0.2f);
+    sr = fmaf(d, sr, 0.25f);
+    sr = fmaf(d, sr, 1.f / 3.f);
+    sr = fmaf(d, sr, 0.5f);
+    sr = fmaf(d, sr, 1.f);
+    return d < 0.0625f ? 2.f * d * sr : -1.3862943611198906f * lg;
+}
+
 // S:224 one schedule entry of the few-step student, fused with the
 // noise draw and the bf16 cast of the next NFE's input:
 //   x1_hat = x + (1 - t_cur) v ;  x <- t_next x1_hat + (1 - t_next) eps  (Eq 1)
@@ -141,14 +161,14 @@ __global__ void __launch_bounds__(256) sampler_kernel(float* __restrict__ x,
                 const float k32 = 2.3283064365386963e-10f;      // 2^-32
                 const float u0 = fmaf(float(w.x), k32, 0.5f * k32), u1 = fmaf(float(w.y), k32, 0.5f * k32);
                 const float u2 = fmaf(float(w.z), k32, 0.5f * k32), u3 = fmaf(float(w.w), k32, 0.5f * k32);
-                // r = sqrt(-2 ln u) as t * rsqrt(t) (MUFU, rel. error ~2^-23).  u
-                // rounds to exactly 1 for the top 128 words (t = 0, r = 0): the
-                // clamp keeps 0 * rsqrt(0) from being NaN.  ln stays the accurate
-                // logf: near u = 1 an absolute log error is amplified by 1/r.
+                // r = sqrt(-2 ln u) as t * rsqrt(t) (MUFU, rel. error ~2^-23); t from
+                // neg2_log_u (relative accuracy everywhere, also where u rounds
+                // to 1 in fp32: an absolute log error would be amplified by 1/r
+                // there).  The clamp keeps 0 * rsqrt(0) from being NaN.
                 // The angle 2 pi u is taken as pi (2u - 1) + pi, inside MUFU
                 // sin/cos's accurate range [-pi, pi] (abs. error ~2^-21), so
                 // sin and cos flip sign.
-                const float t0 = -2.f * logf(u0), t2 = -2.f * logf(u2);
+                const float t0 = neg2_log_u(w.x, u0), t2 = neg2_log_u(w.z, u2);
                 const float r0 = t0 * rsqrtf(fmaxf(t0, 1e-30f)), r1 = t2 * rsqrtf(fmaxf(t2, 1e-30f));
                 const float a1 = 3.14159265358979f * fmaf(2.f, u1, -1.f);
                 const float a3 = 3.14159265358979f * fmaf(2.f, u3, -1.f);
