@@ -1146,6 +1146,7 @@ tm_status tm_audio_cross_attention(tm_ctx* ctx, const void* q, const void* k_aud
             mp.o_rows = frames * tokens_per_frame;
             mp.o_row_map = face_ids;
             mp.zero_inv = dbg_parts == 2 ? nullptr : inv;
+            mp.pack_keys = !getenv("TM_AUDIO_NOPACK");   // A/B switch (timing only)
             mp.zero_T = tokens_per_frame;
             mp.zero_row0 = f0 * tokens_per_frame;
             mp.B = cf.batch;

@@ -109,6 +109,13 @@ struct Prob {
     int seg_len[kMaxSegments];
     int seg_row0[kMaxSegments];       // first key row of the segment in its map
     int seg_map[kMaxSegments];        // tensor map (tk / tv index) of the segment
+    // PACKED keys (f4 audio windows): the segments are concatenated without
+    // padding -- tile j holds keys [128 j, 128 j + 128) of the concatenation,
+    // loaded as 128 / packed_R boxes of packed_R rows (tk_sub / tv_sub), each
+    // from the segment its first key falls in.  0: every segment tile-padded.
+    int packed_R;
+    int Lk;                           // packed: total keys
+    int seg_key0[kMaxSegments];       // packed: first key of each segment in the concatenation
 };
 
 // SCHEDULE BLOCKS.  A launch runs a sequence of blocks; block = (problem,
@@ -141,6 +148,7 @@ struct __align__(64) FmhaParams {
     CUtensorMap tk[kMaxSegments];     // K maps [B][len][H][d]
     CUtensorMap tv[kMaxSegments];     // V maps
     CUtensorMap tk_store, tv_store;   // a3: cache slot that the current segment is copied to
+    CUtensorMap tk_sub, tv_sub;       // packed problems: the tk[0] / tv[0] tensors with packed_R-row boxes
     int store_seg;                    // segment whose tiles are appended to the slot (-1: none; one problem only)
     int nmaps;                        // tk / tv maps in use
     int nprob;
@@ -297,9 +305,23 @@ __device__ __forceinline__ bool next_item(const FmhaParams& p, Cursor& cu, Item&
 
 // KV tile j of a unit of problem `pr`: its segment, first key row within the
 // segment, valid keys (ragged tail masked), and the row in the segment's map.
+__device__ __forceinline__ int packed_seg(const Prob& P, int key) {   // segment holding `key`
+    int seg = 0;
+#pragma unroll
+    for (int s = 1; s < kMaxSegments; ++s)
+        if (s < P.nseg && key >= P.seg_key0[s]) seg = s;
+    return seg;
+}
 __device__ __forceinline__ void tile_info(const FmhaParams& p, int pr, int j, int& seg, int& row,
                                           int& valid) {
     const Prob& P = p.prob[pr];
+    if (P.packed_R) {
+        const int k0 = j * kBN;
+        seg = packed_seg(P, k0);
+        row = k0 - P.seg_key0[seg];            // key offset within its segment
+        valid = min(kBN, P.Lk - k0);
+        return;
+    }
     seg = 0;
 #pragma unroll
     for (int s = 1; s < kMaxSegments; ++s)
@@ -555,6 +577,10 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
             tma_prefetch(&p.tk[s]);
             tma_prefetch(&p.tv[s]);
         }
+        if (p.prob[0].packed_R) {
+            tma_prefetch(&p.tk_sub);
+            tma_prefetch(&p.tv_sub);
+        }
         // The first item's Q tiles and first K/V tiles into L2 while the
         // previous grid drains (one-GPU problems; peer windows are filled by
         // other ranks during the launch).  TM_L2_PREFETCH=n: n K/V tiles (0: off).
@@ -684,12 +710,30 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                     if (p.peer && seg == p.wait_seg) peer_ready(p, ok, 1 + kv, row, valid);
                     trace_ev(p, 0, tn, 1 + kv);
                     const Prob& P = p.prob[it.pr];
-                    const int mi = P.seg_map[seg];
-                    const CUtensorMap* m = kv ? &p.tv[mi] : &p.tk[mi];
                     mbar_arrive_expect_tx(&kv_full[s], kTileBytes);
-                    for (int hf = 0; hf < D / 64; ++hf)
-                        tma_load_4d(sKV + s * kTileBytes + hf * kHalfBytes, m, &kv_full[s],
-                                    hf * 64, it.h, P.seg_row0[seg] + row, it.b);
+                    if (P.packed_R) {
+                        // packed keys: 128 / R boxes of R rows, each from its own
+                        // segment (box offsets are multiples of 1024 B, so the
+                        // 128-B swizzle matches a whole-tile load); boxes past the
+                        // last key reload key 0 (finite data, masked to -inf)
+                        const int R = P.packed_R;
+                        const CUtensorMap* m = kv ? &p.tv_sub : &p.tk_sub;
+                        for (int r = 0; r < kBN / R; ++r) {
+                            int kk = (it.lo + jj) * kBN + r * R;
+                            if (kk >= P.Lk) kk = 0;
+                            const int sg = packed_seg(P, kk);
+                            const int rr = P.seg_row0[sg] + kk - P.seg_key0[sg];
+                            for (int hf = 0; hf < D / 64; ++hf)
+                                tma_load_4d(sKV + s * kTileBytes + hf * kHalfBytes + r * R * 128, m,
+                                            &kv_full[s], hf * 64, it.h, rr, it.b);
+                        }
+                    } else {
+                        const int mi = P.seg_map[seg];
+                        const CUtensorMap* m = kv ? &p.tv[mi] : &p.tk[mi];
+                        for (int hf = 0; hf < D / 64; ++hf)
+                            tma_load_4d(sKV + s * kTileBytes + hf * kHalfBytes, m, &kv_full[s],
+                                        hf * 64, it.h, P.seg_row0[seg] + row, it.b);
+                    }
                     ++kv_it;
                 }
             }
@@ -1659,6 +1703,34 @@ cudaError_t launch_fmha_sm100_multi(const MultiProblem& mp, void* scratch, cudaS
         P.o_row0 = int(sp.o_row0);
         P.o_clip = !mp.o_row_map && sp.o_row0 + sp.Lq == mp.o_rows;
         P.n_qpairs = int((sp.Lq + 2 * kBM - 1) / (2 * kBM));
+    }
+    // Packed keys (MultiProblem::pack_keys): the largest box height R in {32,
+    // 16, 8} dividing every segment length (R >= 8 keeps every box at a
+    // 1024-B-aligned offset of the tile, where the 128-B swizzle repeats).
+    int R = 0;
+    if (mp.pack_keys) {
+        R = 32;
+        for (int i = 0; i < mp.nprob; ++i)
+            for (int sg = 0; sg < mp.prob[i].nseg; ++sg)
+                while (R >= 8 && mp.prob[i].seg_len[sg] % R) R /= 2;
+        if (R < 8) R = 0;
+    }
+    if (R) {
+        if (!make_map(&p.tk_sub, mp.k, mp.d, mp.H, mp.kv_rows, mp.B, mp.kv_bstride, R) ||
+            !make_map(&p.tv_sub, mp.v, mp.d, mp.H, mp.kv_rows, mp.B, mp.kv_bstride, R))
+            return cudaErrorInvalidValue;
+        for (int i = 0; i < mp.nprob; ++i) {
+            Prob& P = p.prob[i];
+            const SubProblem& sp = mp.prob[i];
+            int64_t k0 = 0;
+            for (int sg = 0; sg < sp.nseg; ++sg) {
+                P.seg_key0[sg] = int(k0);
+                k0 += sp.seg_len[sg];
+            }
+            P.packed_R = R;
+            P.Lk = int(k0);
+            P.n_tiles = int((k0 + kBN - 1) / kBN);
+        }
     }
     // Blocks: every problem x head group, in order.  A launch holds up to
     // kMaxBlocks blocks of up to kMaxSkClasses tail shapes, so a long list

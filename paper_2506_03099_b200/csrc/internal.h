@@ -142,6 +142,9 @@ struct MultiProblem {
     SubProblem prob[kMaxProblems];
     int max_ctas = 0;
     int sched_heads = 0;
+    // keys of a problem = its segments concatenated without tile padding (when
+    // every segment length is a multiple of 8; else padded as usual)
+    bool pack_keys = false;
 };
 
 // Launch with programmatic dependent launch allowed (the kernel executes

@@ -617,7 +617,8 @@ def _audio_case(frames, T, A, H, d, n_face, dtype, seed, B=1):
 
 
 @pytest.mark.parametrize("dtype", ["bf16", "fp32"])
-@pytest.mark.parametrize("frames,T,A,n_face", [(3, 64, 8, 20), (7, 40, 5, 40), (1, 33, 3, 1), (2, 50, 16, 7)])
+@pytest.mark.parametrize("frames,T,A,n_face", [(3, 64, 8, 20), (7, 40, 5, 40), (1, 33, 3, 1), (2, 50, 16, 7),
+                                                  (7, 40, 48, 13), (4, 300, 40, 150)])
 def test_audio_cross_attention_vs_oracle(dtype, frames, T, A, n_face):
     """f4: face rows attend the clamped 5-frame audio
     window; non-face rows are exactly zero."""
