@@ -148,7 +148,8 @@ def test_peer_virtual_ranks_bitwise_per_head_block(P, Lr, Lc):
     assembled output equal a direct context over those heads bit for bit
     (same kernel, same schedule); the whole output is within the bf16 bar of
     the oracle.  (8, 300, 1000): shards of 125 rows, so Q and K/V tiles span
-    two source ranks; (8, 2025, 6075): the 720^2 shape, ragged shards."""
+    two source ranks; (8, 2025, 6075): the 720^2 shape, ragged shards, also
+    checked against the oracle on sampled rows."""
     H, d = 40 if Lc >= 3072 else (6 if P == 3 else 8), 128
     host, dev = make_inputs(H, d, Lr, Lc, 3, syn.seed_for(12, P))
     outs = _run_virtual(P, H, d, Lr, Lc, dev)
@@ -158,8 +159,7 @@ def test_peer_virtual_ranks_bitwise_per_head_block(P, Lr, Lc):
         ref = direct_stream(H, d, Lr, Lc, dev, heads=hb)
         for a, b in zip(outs, ref):
             assert (bits(a[:, hb].contiguous()) == bits(b)).all(), f"rank {r}"
-    if Lc <= 3072:
-        oracle_check(host, outs)
+    oracle_check(host, outs)             # row-sampled at the large shapes (incl. 720^2)
 
 
 def test_peer_virtual_ranks_batch_layers_steps_d64():
