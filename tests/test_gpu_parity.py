@@ -652,7 +652,34 @@ def test_audio_cross_attention_wan512_chunk_batch2():
     o = torch.empty_like(qd)
     ca.audio(qd, to_dev(ka).view(B, frames, A, H, d), to_dev(va).view(B, frames, A, H, d), o,
              torch.from_numpy(face).cuda())
-    assert ca.launches == 2                          # prep (gather + zero fill) + one attention
+    assert ca.launches == 2                          # prep (gather, face map) + one attention
+    got = from_dev(o)
+    non_face = np.setdiff1d(np.arange(T), face)
+    assert (got[:, :, non_face] == 0).all()
+    for b in range(B):
+        ref = oracle.audio_cross_attention(qs.f64.reshape(B, frames, T, H, d)[b],
+                                           ka.f64.reshape(B, frames, A, H, d)[b],
+                                           va.f64.reshape(B, frames, A, H, d)[b], face)
+        assert rel_err(got[b][:, face], ref[:, face]) <= BF16_ALARM
+    ca.close()
+
+
+def test_audio_cross_attention_more_frames_than_one_launch():
+    """f4 with 20 frames: the bf16 path takes the frames 16 problems at a time,
+    and a launch holds at most 8 schedule blocks, so the attention runs as
+    three launches (8 + 8 + 4 frames); the first launch of each group zeroes
+    that group's non-face rows.  Batch 2, d = 64, packed 8-row key boxes."""
+    frames, T, A, H, d, B, n_face = 20, 48, 8, 3, 64, 2, 11
+    rng = np.random.default_rng(syn.seed_for(12, 77))
+    qs, _, _ = syn.chunk_qkv(rng, B * frames * T, H, d, "bf16", "D0")
+    ka, va, _ = syn.chunk_qkv(rng, B * frames * A, H, d, "bf16", "D0")
+    face = np.sort(rng.choice(T, size=n_face, replace=False)).astype(np.int32)
+    ca = tm.ChunkAttention(H, d, 16, 16, 1, 1, batch=B)
+    qd = to_dev(qs).view(B, frames, T, H, d)
+    o = torch.full_like(qd, 7.0)
+    ca.audio(qd, to_dev(ka).view(B, frames, A, H, d), to_dev(va).view(B, frames, A, H, d), o,
+             torch.from_numpy(face).cuda())
+    assert ca.launches == 4                          # prep + three attention launches
     got = from_dev(o)
     non_face = np.setdiff1d(np.arange(T), face)
     assert (got[:, :, non_face] == 0).all()
