@@ -312,10 +312,11 @@ __device__ __forceinline__ int packed_seg(const Prob& P, int key) {   // segment
         if (s < P.nseg && key >= P.seg_key0[s]) seg = s;
     return seg;
 }
+template <bool kMulti>
 __device__ __forceinline__ void tile_info(const FmhaParams& p, int pr, int j, int& seg, int& row,
                                           int& valid) {
     const Prob& P = p.prob[pr];
-    if (P.packed_R) {
+    if (kMulti && P.packed_R) {
         const int k0 = j * kBN;
         seg = packed_seg(P, k0);
         row = k0 - P.seg_key0[seg];            // key offset within its segment
@@ -519,7 +520,10 @@ __device__ __forceinline__ void softmax_bar() {   // the 256 softmax threads onl
     asm volatile("bar.sync 1, 256;" ::: "memory");
 }
 
-template <int D, uint32_t kPolyMask>
+// kMulti: launches of several problems (f1 window, f4 audio) -- the only ones
+// with packed keys or the f4 zero fill; the chunk-attention launches compile
+// without that code.
+template <int D, uint32_t kPolyMask, bool kMulti>
 __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_constant__ FmhaParams p) {
     constexpr int kTileBytes = kBN * D * 2;
     constexpr uint32_t kIdescS = make_idesc_bf16(kBM, kBN, 0, 0);   // Q, K both K-major
@@ -541,7 +545,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
     uint64_t* o_empty = o_final + 2;         // [2]  epilogue done reading O_i
     uint64_t* o_done = o_empty + 2;          // [2]  each PV_i complete (P_i reusable)
     uint64_t* s_free = o_done + 2;           // [1]  S buffer loaded into registers
-    uint64_t* store_done = s_free + 1;       // [kStages] append-store finished reading a slot
+    uint64_t* store_done = s_free + 1;       // [kStages] append warp done with a slot's fill
     uint64_t* store_idle = store_done + kStages;   // [1] append warp done (one phase per launch)
     uint64_t* merge_bar = store_idle + 1;          // [3] a half partial landed in merge buffer j
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(merge_bar + 3);
@@ -577,7 +581,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
             tma_prefetch(&p.tk[s]);
             tma_prefetch(&p.tv[s]);
         }
-        if (p.prob[0].packed_R) {
+        if (kMulti && p.prob[0].packed_R) {
             tma_prefetch(&p.tk_sub);
             tma_prefetch(&p.tv_sub);
         }
@@ -593,7 +597,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                                        p.prob[it0.pr].q_row0 + it0.qp * 2 * kBM + i * kBM, it0.b);
             for (int j = it0.lo; j < it0.hi && j < it0.lo + p.l2_prefetch; ++j) {
                 int seg, row, valid;
-                tile_info(p, it0.pr, j, seg, row, valid);
+                tile_info<kMulti>(p, it0.pr, j, seg, row, valid);
                 const Prob& P0 = p.prob[it0.pr];
                 const int m = P0.seg_map[seg], r = P0.seg_row0[seg] + row;
                 for (int hf = 0; hf < D / 64; ++hf) {
@@ -646,7 +650,6 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
         if (lane == 0) {
             int tn = 0;
             uint32_t kv_it = 0, n_item = 0;
-            uint32_t pending_store = 0, store_par = 0;   // per slot: pending bit / phase parity bit
             uint32_t ok = 0;                               // peer (tensor, source) pairs already landed
             bool kv_released = !p.push;                    // fused push: K/V not yet released
 #ifdef TM_SPANS_PROD
@@ -679,7 +682,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                     int jj, kv;
                     load_order(q, nkv, jj, kv);
                     int seg, row, valid;
-                    tile_info(p, it.pr, it.lo + jj, seg, row, valid);
+                    tile_info<kMulti>(p, it.pr, it.lo + jj, seg, row, valid);
                     const int s = kv_it % kStages;
                     trace_ev(p, 0, tn, 3 + kv);
 #ifdef TM_SPANS_PROD
@@ -690,16 +693,21 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                     long long tw1 = clock64();
                     cyc_empty += tw1 - tw0;
 #endif
-                    if ((pending_store >> s) & 1) {       // previous occupant being appended
-                        mbar_wait(&store_done[s], (store_par >> s) & 1);
+                    // With the a3 append active, a slot is refilled only after the
+                    // append warp has passed its previous fill (stored it, or seen
+                    // that it needs no store): the append warp waits on EVERY fill's
+                    // kv_full phase in order, and without this gate the producer
+                    // could complete two fills of a slot whose store is not pending
+                    // while the append warp is still blocked on an earlier store --
+                    // a parity ABA that desynchronised it (a hang, seen at 10 and 20
+                    // heads under some timings).
+                    if (p.store_seg >= 0 && kv_it >= uint32_t(kStages)) {
+                        mbar_wait(&store_done[s], ((kv_it / kStages) - 1) & 1);
 #ifdef TM_SPANS_PROD
                         cyc_store += clock64() - tw1;
 #endif
-                        store_par ^= 1u << s;
-                        pending_store &= ~(1u << s);
                         trace_ev(p, 0, tn, 5);
                     }
-                    if (stores_tile(p, it, seg, row)) pending_store |= 1u << s;
                     // Release this CTA's K/V pushes before the first wait on K/V
                     // (own rank included) or after a few loads, whichever first:
                     // by then the stores have drained and the fence is cheap.
@@ -711,7 +719,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                     trace_ev(p, 0, tn, 1 + kv);
                     const Prob& P = p.prob[it.pr];
                     mbar_arrive_expect_tx(&kv_full[s], kTileBytes);
-                    if (P.packed_R) {
+                    if (kMulti && P.packed_R) {
                         // packed keys: 128 / R boxes of R rows, each from its own
                         // segment (box offsets are multiples of 1024 B, so the
                         // 128-B swizzle matches a whole-tile load); boxes past the
@@ -768,6 +776,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
         if (lane == 0 && p.store_seg >= 0) {
             uint32_t kv_it = 0;
             int tn = 0;
+            int pend = -1;                 // slot of the last stored fill, its read maybe in flight
             Item it;
             Cursor cu;
             while (next_item(p, cu, it)) {
@@ -776,26 +785,46 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                     int jj, kv;
                     load_order(q, nkv, jj, kv);
                     int seg, row, valid;
-                    tile_info(p, it.pr, it.lo + jj, seg, row, valid);
-                    // Observe EVERY position's kv_full phase in order: waiting only on
-                    // stored tiles could run two phases ahead on a slot (parity ABA).
+                    tile_info<kMulti>(p, it.pr, it.lo + jj, seg, row, valid);
+                    // Observe EVERY position's kv_full phase in order, and release
+                    // every fill (stored or not) through store_done: the producer
+                    // refills a slot only after that, so no slot can complete two
+                    // phases ahead of this warp (parity ABA either way).  A stored
+                    // fill is released once the TMA store has read it; up to one
+                    // such read stays in flight while this warp moves on, flushed
+                    // before its slot comes round again.
                     const int s = kv_it % kStages;
+                    if (pend == s) {
+                        tma_store_wait_read();
+                        mbar_arrive(&store_done[pend]);
+                        pend = -1;
+                    }
                     mbar_wait(&kv_full[s], (kv_it / kStages) & 1);
                     trace_ev(p, 2, tn, 40 + kv);
-                    if (!stores_tile(p, it, seg, row)) continue;
-                    fence_proxy_async_smem();
-                    const CUtensorMap* m = kv ? &p.tv_store : &p.tk_store;
-                    for (int hf = 0; hf < D / 64; ++hf)
-                        tma_store_4d(m, sKV + s * kTileBytes + hf * kHalfBytes, hf * 64, it.h, row,
-                                     it.b);
-                    tma_store_commit();
-                    tma_store_wait_read();
-                    mbar_arrive(&store_done[s]);
+                    if (stores_tile(p, it, seg, row)) {
+                        fence_proxy_async_smem();
+                        const CUtensorMap* m = kv ? &p.tv_store : &p.tk_store;
+                        for (int hf = 0; hf < D / 64; ++hf)
+                            tma_store_4d(m, sKV + s * kTileBytes + hf * kHalfBytes, hf * 64, it.h, row,
+                                         it.b);
+                        tma_store_commit();
+                        if (pend >= 0) {
+                            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                            mbar_arrive(&store_done[pend]);
+                        }
+                        pend = s;
+                    } else {
+                        mbar_arrive(&store_done[s]);
+                    }
                 }
+            }
+            if (pend >= 0) {
+                tma_store_wait_read();
+                mbar_arrive(&store_done[pend]);
             }
         }
         if (lane == 0) mbar_arrive(store_idle);   // the ring is no longer read by TMA stores
-        if (p.zf_inv != nullptr) {
+        if (kMulti && p.zf_inv != nullptr) {
             // f4: zero the non-face rows of o, this CTA's share (warp-uniform branch)
             const int words = p.o_H * D / 8;                  // 16-B words per token row
             const int64_t total = int64_t(p.B) * p.zf_rows;
@@ -893,7 +922,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
             float m_run = -INFINITY, l = 0.f;
             for (int j = it.lo; j < it.hi; ++j, ++g) {
                 int seg, row, valid;
-                tile_info(p, it.pr, j, seg, row, valid);
+                tile_info<kMulti>(p, it.pr, j, seg, row, valid);
                 uint32_t r[kBN];
                 mbar_wait(&s_full[i], g & 1);
                 if (tr) trace_ev(p, 5 + warp, tn, 20);
@@ -1267,7 +1296,7 @@ constexpr int smem_bytes() {
 
 int sm_count() { return current_sm_count(); }
 
-template <int D, uint32_t kPolyMask>
+template <int D, uint32_t kPolyMask, bool kMulti>
 cudaError_t launch_t(const FmhaParams& p, int grid, cudaStream_t stream) {
     // The max-dynamic-shared-memory attribute is per device: set once per
     // device ordinal (bit per device; ordinals >= 64 set it on every launch).
@@ -1276,13 +1305,13 @@ cudaError_t launch_t(const FmhaParams& p, int grid, cudaStream_t stream) {
     if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
     const unsigned long long bit = dev < 64 ? 1ull << dev : 0;
     if (!bit || !(__atomic_load_n(&attr_set, __ATOMIC_RELAXED) & bit)) {
-        cudaError_t e = cudaFuncSetAttribute(fmha_sm100_kernel<D, kPolyMask>,
+        cudaError_t e = cudaFuncSetAttribute(fmha_sm100_kernel<D, kPolyMask, kMulti>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              smem_bytes<D>());
         if (e != cudaSuccess) return e;
         __atomic_fetch_or(&attr_set, bit, __ATOMIC_RELAXED);
     }
-    return launch_pdl(fmha_sm100_kernel<D, kPolyMask>, dim3(grid), dim3(kThreads), smem_bytes<D>(),
+    return launch_pdl(fmha_sm100_kernel<D, kPolyMask, kMulti>, dim3(grid), dim3(kThreads), smem_bytes<D>(),
                       stream, p);
 }
 
@@ -1306,7 +1335,7 @@ cudaError_t launch_t(const FmhaParams& p, int grid, cudaStream_t stream) {
 // TM_POLY selects a split for tuning: 1 = all MUFU, 2 = 2/16, 3 = 3/16,
 // 4 = 4/16, 5 = 1/16 (the default, also when TM_POLY is unset).
 constexpr uint32_t kPoly2of16 = 0x0808u;     // pairs {3, 11} of every 16 (TM_POLY=2)
-template <int D>
+template <int D, bool kMulti>
 cudaError_t launch_d(const FmhaParams& p, int grid, cudaStream_t stream) {
     static int env_sel = [] {
         const char* e = getenv("TM_POLY");
@@ -1314,11 +1343,11 @@ cudaError_t launch_d(const FmhaParams& p, int grid, cudaStream_t stream) {
     }();
     const int sel = env_sel ? env_sel : 5;
     switch (sel) {
-        case 1: return launch_t<D, 0x0000u>(p, grid, stream);   // all MUFU
-        case 3: return launch_t<D, 0x1084u>(p, grid, stream);   // {2,7,12}
-        case 5: return launch_t<D, 0x0800u>(p, grid, stream);   // {11}: 1/16
-        case 4: return launch_t<D, 0x4444u>(p, grid, stream);   // {2,6,10,14}
-        default: return launch_t<D, kPoly2of16>(p, grid, stream);
+        case 1: return launch_t<D, 0x0000u, kMulti>(p, grid, stream);   // all MUFU
+        case 3: return launch_t<D, 0x1084u, kMulti>(p, grid, stream);   // {2,7,12}
+        case 5: return launch_t<D, 0x0800u, kMulti>(p, grid, stream);   // {11}: 1/16
+        case 4: return launch_t<D, 0x4444u, kMulti>(p, grid, stream);   // {2,6,10,14}
+        default: return launch_t<D, kPoly2of16, kMulti>(p, grid, stream);
     }
 }
 
@@ -1538,7 +1567,7 @@ bool exit_wait_full() {
 }
 
 cudaError_t finish_and_launch(FmhaParams& p, int d, int grid, void* scratch, cudaStream_t stream,
-                              int* launches, unsigned long long* trace, bool peer) {
+                              int* launches, unsigned long long* trace, bool peer, bool multi) {
     static const int l2_prefetch_env = [] {
         const char* e = getenv("TM_L2_PREFETCH");
         return e ? atoi(e) : 2;
@@ -1556,7 +1585,8 @@ cudaError_t finish_and_launch(FmhaParams& p, int d, int grid, void* scratch, cud
                                         size_t(kMaxBlocks) * kMaxPersistentCtas *
                                             (256 * size_t(d) + 512) * 4);
     if (grid <= 0) return cudaErrorInvalidValue;
-    cudaError_t e = d == 128 ? launch_d<128>(p, grid, stream) : launch_d<64>(p, grid, stream);
+    cudaError_t e = multi ? (d == 128 ? launch_d<128, true>(p, grid, stream) : launch_d<64, true>(p, grid, stream))
+                          : (d == 128 ? launch_d<128, false>(p, grid, stream) : launch_d<64, false>(p, grid, stream));
     if (e == cudaSuccess && launches) ++*launches;
     return e;
 }
@@ -1657,7 +1687,7 @@ cudaError_t launch_fmha_sm100(const AttnProblem& pr, void* scratch, cudaStream_t
     }
     (void)tiles;
     return finish_and_launch(p, pr.d, launch_grid(p), scratch, stream, launches, trace,
-                             pr.peer != nullptr);
+                             pr.peer != nullptr, false);
 }
 
 cudaError_t launch_fmha_sm100_multi(const MultiProblem& mp, void* scratch, cudaStream_t stream,
@@ -1745,7 +1775,7 @@ cudaError_t launch_fmha_sm100_multi(const MultiProblem& mp, void* scratch, cudaS
             if (add_block(p, i, h0, hb, C, &full)) continue;
             if (!full) return cudaErrorInvalidValue;
             cudaError_t e = finish_and_launch(p, mp.d, launch_grid(p), scratch, stream, launches,
-                                              trace, false);
+                                              trace, false, true);
             if (e != cudaSuccess) return e;
             p.zf_inv = nullptr;               // the first launch zero-filled
             p.nblk = 0;
@@ -1753,7 +1783,7 @@ cudaError_t launch_fmha_sm100_multi(const MultiProblem& mp, void* scratch, cudaS
             if (!add_block(p, i, h0, hb, C, &full)) return cudaErrorInvalidValue;
         }
     }
-    return finish_and_launch(p, mp.d, launch_grid(p), scratch, stream, launches, trace, false);
+    return finish_and_launch(p, mp.d, launch_grid(p), scratch, stream, launches, trace, false, true);
 }
 
 }  // namespace tmk
