@@ -348,10 +348,10 @@ __device__ __forceinline__ bool stores_tile(const FmhaParams& p, const Item& it,
 
 // Destination of output row q of head h (row a6: the owner's O window when the
 // path is Ulysses-sharded over peer memory, else o itself); null for pad rows.
-template <int D>
+template <int D, int kKind>
 __device__ __forceinline__ uint16_t* out_row(const FmhaParams& p, const Prob& P, int b, int q, int h) {
     if (q >= P.Lq) return nullptr;
-    if (p.o_rows >= P.Lq) {   // one owner (P = 1): no division
+    if (kKind != 2 || p.o_rows >= P.Lq) {   // one owner (P = 1): no division
         const int row = P.o_row0 + (p.o_row_map ? p.o_row_map[q] : q);
         return p.o_dst[0] + ((int64_t(b) * p.o_bstride + row) * p.o_H + p.o_h0 + h) * D;
     }
@@ -365,7 +365,7 @@ __device__ __forceinline__ uint16_t* out_row(const FmhaParams& p, const Prob& P,
 // bf16 and store.  Through a 4 KB per-warp staging buffer (32 rows x 64
 // columns, 16-B chunks XOR-swizzled by row: conflict-free both ways) each
 // store instruction writes 4 rows x 128 B instead of 32 rows x 16 B.
-template <int D>
+template <int D, int kKind>
 __device__ __forceinline__ void store_rows_bf16(const FmhaParams& p, const Prob& P, uint32_t tsrc,
                                                 float scale, uint8_t* stg, int b, int q0, int h,
                                                 int lane) {
@@ -409,7 +409,7 @@ __device__ __forceinline__ void store_rows_bf16(const FmhaParams& p, const Prob&
 #pragma unroll
     for (int t = 0; t < 8; ++t) {
         const int q = q0 + t * 4 + (lane >> 3);
-        dsts[t] = out_row<D>(p, P, b, q, h);
+        dsts[t] = out_row<D, kKind>(p, P, b, q, h);
     }
 #pragma unroll 1
     for (int half = 0; half < D / 64; ++half) {
@@ -520,11 +520,14 @@ __device__ __forceinline__ void softmax_bar() {   // the 256 softmax threads onl
     asm volatile("bar.sync 1, 256;" ::: "memory");
 }
 
-// kMulti: launches of several problems (f1 window, f4 audio) -- the only ones
-// with packed keys or the f4 zero fill; the chunk-attention launches compile
-// without that code.
-template <int D, uint32_t kPolyMask, bool kMulti>
+// kKind: 0 one-GPU chunk attention; 1 launches of several problems (f1 window,
+// f4 audio) -- the only ones with packed keys or the f4 zero fill; 2 the peer
+// transport (fused push, window waits, routed O rows, done signal).  Each kind
+// compiles only its own paths: code the chunk-attention kernel never runs
+// measured 1-3 % slower when compiled in (layout).
+template <int D, uint32_t kPolyMask, int kKind>
 __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_constant__ FmhaParams p) {
+    constexpr bool kMulti = kKind == 1, kPeerKind = kKind == 2;
     constexpr int kTileBytes = kBN * D * 2;
     constexpr uint32_t kIdescS = make_idesc_bf16(kBM, kBN, 0, 0);   // Q, K both K-major
     constexpr uint32_t kIdescO = make_idesc_bf16(kBM, D, 0, 1);     // P (TMEM), V MN-major
@@ -622,7 +625,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
 #ifdef TM_SPANS_PROLOGUE
     if (threadIdx.x == 0) trace_span(p, 5);   // (spans A/B) previous grid complete
 #endif
-    if (p.push) {
+    if (kPeerKind && p.push) {
         // a2 fused.  All 384 threads store this rank's shard of Q into the owners'
         // windows (NVLink stores).  Then warp 10 alone releases Q (a system-scope
         // fence waits until the CTA's stores have landed; the grid's last CTA
@@ -651,7 +654,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
             int tn = 0;
             uint32_t kv_it = 0, n_item = 0;
             uint32_t ok = 0;                               // peer (tensor, source) pairs already landed
-            bool kv_released = !p.push;                    // fused push: K/V not yet released
+            bool kv_released = !kPeerKind || !p.push;      // fused push: K/V not yet released
 #ifdef TM_SPANS_PROD
             long long cyc_empty = 0, cyc_store = 0;
 #endif
@@ -666,7 +669,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                 for (int step = 0; step < 2 * nkv + 2; ++step) {
                     if (step == 0 || step == 2) {
                         const int i = step >> 1;
-                        if (p.peer) {
+                        if (kPeerKind && p.peer) {
                             const int r0 = it.qp * 2 * kBM + i * kBM;
                             peer_ready(p, ok, 0, r0, min(kBM, p.prob[0].Lq - r0));
                         }
@@ -715,7 +718,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                         peer_release(p.pp.ctr, p.pp.own, p.pp.P, p.pp.rank, 1);
                         kv_released = true;
                     }
-                    if (p.peer && seg == p.wait_seg) peer_ready(p, ok, 1 + kv, row, valid);
+                    if (kPeerKind && p.peer && seg == p.wait_seg) peer_ready(p, ok, 1 + kv, row, valid);
                     trace_ev(p, 0, tn, 1 + kv);
                     const Prob& P = p.prob[it.pr];
                     mbar_arrive_expect_tx(&kv_full[s], kTileBytes);
@@ -1042,7 +1045,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
 #endif
             const int q = it.qp * 2 * kBM + row_in_pair;
             if (!it.piece || p.dbg_nomerge) {   // (dbg_nomerge: timing bound only, wrong output)
-                store_rows_bf16<D>(p, p.prob[it.pr], tOi, 1.f / l, sEpi + warp * 4096, it.b, q - lane,
+                store_rows_bf16<D, kKind>(p, p.prob[it.pr], tOi, 1.f / l, sEpi + warp * 4096, it.b, q - lane,
                                    it.h, lane);
 #ifdef TM_SPANS_MERGE
                 if (threadIdx.x == 0) trace_span(p, 5);
@@ -1222,7 +1225,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
 #ifdef TM_SPANS_MERGE2
                 if (threadIdx.x == 0) trace_span(p, 2);      // (spans A/B) partials merged
 #endif
-                store_rows_bf16<D>(p, p.prob[it.pr], tOi, inv, sEpi + warp * 4096, it.b, q - lane, it.h,
+                store_rows_bf16<D, kKind>(p, p.prob[it.pr], tOi, inv, sEpi + warp * 4096, it.b, q - lane, it.h,
                                    lane);
                 tc_fence_before();
                 mbar_arrive(&o_empty[i]);
@@ -1255,7 +1258,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
     }
     // a6 fused: this rank's O rows are in the owners' windows once every CTA
     // is here; the last CTA bumps done[rank] at each owner.
-    if (p.signal_done) peer_signal(p.done_ctr, p.own, p.P, p.rank, 3, p.wait_done);
+    if (kPeerKind && p.signal_done) peer_signal(p.done_ctr, p.own, p.P, p.rank, 3, p.wait_done);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -1296,7 +1299,7 @@ constexpr int smem_bytes() {
 
 int sm_count() { return current_sm_count(); }
 
-template <int D, uint32_t kPolyMask, bool kMulti>
+template <int D, uint32_t kPolyMask, int kKind>
 cudaError_t launch_t(const FmhaParams& p, int grid, cudaStream_t stream) {
     // The max-dynamic-shared-memory attribute is per device: set once per
     // device ordinal (bit per device; ordinals >= 64 set it on every launch).
@@ -1305,13 +1308,13 @@ cudaError_t launch_t(const FmhaParams& p, int grid, cudaStream_t stream) {
     if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
     const unsigned long long bit = dev < 64 ? 1ull << dev : 0;
     if (!bit || !(__atomic_load_n(&attr_set, __ATOMIC_RELAXED) & bit)) {
-        cudaError_t e = cudaFuncSetAttribute(fmha_sm100_kernel<D, kPolyMask, kMulti>,
+        cudaError_t e = cudaFuncSetAttribute(fmha_sm100_kernel<D, kPolyMask, kKind>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              smem_bytes<D>());
         if (e != cudaSuccess) return e;
         __atomic_fetch_or(&attr_set, bit, __ATOMIC_RELAXED);
     }
-    return launch_pdl(fmha_sm100_kernel<D, kPolyMask, kMulti>, dim3(grid), dim3(kThreads), smem_bytes<D>(),
+    return launch_pdl(fmha_sm100_kernel<D, kPolyMask, kKind>, dim3(grid), dim3(kThreads), smem_bytes<D>(),
                       stream, p);
 }
 
@@ -1335,7 +1338,7 @@ cudaError_t launch_t(const FmhaParams& p, int grid, cudaStream_t stream) {
 // TM_POLY selects a split for tuning: 1 = all MUFU, 2 = 2/16, 3 = 3/16,
 // 4 = 4/16, 5 = 1/16 (the default, also when TM_POLY is unset).
 constexpr uint32_t kPoly2of16 = 0x0808u;     // pairs {3, 11} of every 16 (TM_POLY=2)
-template <int D, bool kMulti>
+template <int D, int kKind>
 cudaError_t launch_d(const FmhaParams& p, int grid, cudaStream_t stream) {
     static int env_sel = [] {
         const char* e = getenv("TM_POLY");
@@ -1343,11 +1346,11 @@ cudaError_t launch_d(const FmhaParams& p, int grid, cudaStream_t stream) {
     }();
     const int sel = env_sel ? env_sel : 5;
     switch (sel) {
-        case 1: return launch_t<D, 0x0000u, kMulti>(p, grid, stream);   // all MUFU
-        case 3: return launch_t<D, 0x1084u, kMulti>(p, grid, stream);   // {2,7,12}
-        case 5: return launch_t<D, 0x0800u, kMulti>(p, grid, stream);   // {11}: 1/16
-        case 4: return launch_t<D, 0x4444u, kMulti>(p, grid, stream);   // {2,6,10,14}
-        default: return launch_t<D, kPoly2of16, kMulti>(p, grid, stream);
+        case 1: return launch_t<D, 0x0000u, kKind>(p, grid, stream);   // all MUFU
+        case 3: return launch_t<D, 0x1084u, kKind>(p, grid, stream);   // {2,7,12}
+        case 5: return launch_t<D, 0x0800u, kKind>(p, grid, stream);   // {11}: 1/16
+        case 4: return launch_t<D, 0x4444u, kKind>(p, grid, stream);   // {2,6,10,14}
+        default: return launch_t<D, kPoly2of16, kKind>(p, grid, stream);
     }
 }
 
@@ -1567,7 +1570,7 @@ bool exit_wait_full() {
 }
 
 cudaError_t finish_and_launch(FmhaParams& p, int d, int grid, void* scratch, cudaStream_t stream,
-                              int* launches, unsigned long long* trace, bool peer, bool multi) {
+                              int* launches, unsigned long long* trace, bool peer, int kind) {
     static const int l2_prefetch_env = [] {
         const char* e = getenv("TM_L2_PREFETCH");
         return e ? atoi(e) : 2;
@@ -1585,8 +1588,12 @@ cudaError_t finish_and_launch(FmhaParams& p, int d, int grid, void* scratch, cud
                                         size_t(kMaxBlocks) * kMaxPersistentCtas *
                                             (256 * size_t(d) + 512) * 4);
     if (grid <= 0) return cudaErrorInvalidValue;
-    cudaError_t e = multi ? (d == 128 ? launch_d<128, true>(p, grid, stream) : launch_d<64, true>(p, grid, stream))
-                          : (d == 128 ? launch_d<128, false>(p, grid, stream) : launch_d<64, false>(p, grid, stream));
+    cudaError_t e;
+    switch (kind) {
+        case 1: e = d == 128 ? launch_d<128, 1>(p, grid, stream) : launch_d<64, 1>(p, grid, stream); break;
+        case 2: e = d == 128 ? launch_d<128, 2>(p, grid, stream) : launch_d<64, 2>(p, grid, stream); break;
+        default: e = d == 128 ? launch_d<128, 0>(p, grid, stream) : launch_d<64, 0>(p, grid, stream);
+    }
     if (e == cudaSuccess && launches) ++*launches;
     return e;
 }
@@ -1687,7 +1694,7 @@ cudaError_t launch_fmha_sm100(const AttnProblem& pr, void* scratch, cudaStream_t
     }
     (void)tiles;
     return finish_and_launch(p, pr.d, launch_grid(p), scratch, stream, launches, trace,
-                             pr.peer != nullptr, false);
+                             pr.peer != nullptr, pr.peer != nullptr ? 2 : 0);
 }
 
 cudaError_t launch_fmha_sm100_multi(const MultiProblem& mp, void* scratch, cudaStream_t stream,
@@ -1775,7 +1782,7 @@ cudaError_t launch_fmha_sm100_multi(const MultiProblem& mp, void* scratch, cudaS
             if (add_block(p, i, h0, hb, C, &full)) continue;
             if (!full) return cudaErrorInvalidValue;
             cudaError_t e = finish_and_launch(p, mp.d, launch_grid(p), scratch, stream, launches,
-                                              trace, false, true);
+                                              trace, false, 1);
             if (e != cudaSuccess) return e;
             p.zf_inv = nullptr;               // the first launch zero-filled
             p.nblk = 0;
@@ -1783,7 +1790,7 @@ cudaError_t launch_fmha_sm100_multi(const MultiProblem& mp, void* scratch, cudaS
             if (!add_block(p, i, h0, hb, C, &full)) return cudaErrorInvalidValue;
         }
     }
-    return finish_and_launch(p, mp.d, launch_grid(p), scratch, stream, launches, trace, false, true);
+    return finish_and_launch(p, mp.d, launch_grid(p), scratch, stream, launches, trace, false, 1);
 }
 
 }  // namespace tmk
