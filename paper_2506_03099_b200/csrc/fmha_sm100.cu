@@ -548,8 +548,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
     uint64_t* o_empty = o_final + 2;         // [2]  epilogue done reading O_i
     uint64_t* o_done = o_empty + 2;          // [2]  each PV_i complete (P_i reusable)
     uint64_t* s_free = o_done + 2;           // [1]  S buffer loaded into registers
-    uint64_t* store_done = s_free + 1;       // [kStages] append warp done with a slot's fill
-    uint64_t* store_idle = store_done + kStages;   // [1] append warp done (one phase per launch)
+    uint64_t* store_idle = s_free + 1;       // [1] append warp done (one phase per launch)
     uint64_t* merge_bar = store_idle + 1;          // [3] a half partial landed in merge buffer j
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(merge_bar + 3);
 
@@ -571,8 +570,9 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
         mbar_init(s_free, 128);
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&kv_full[s], 1);
-            mbar_init(&kv_empty[s], 1);
-            mbar_init(&store_done[s], 1);
+            // with the a3 append active, a fill is released by the MMA commit AND
+            // by the append warp (which has then passed it, stored or not)
+            mbar_init(&kv_empty[s], p.store_seg >= 0 ? 2 : 1);
         }
         mbar_init(store_idle, 1);
         for (int j = 0; j < 3; ++j) mbar_init(&merge_bar[j], 1);
@@ -696,21 +696,14 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                     long long tw1 = clock64();
                     cyc_empty += tw1 - tw0;
 #endif
-                    // With the a3 append active, a slot is refilled only after the
-                    // append warp has passed its previous fill (stored it, or seen
-                    // that it needs no store): the append warp waits on EVERY fill's
-                    // kv_full phase in order, and without this gate the producer
-                    // could complete two fills of a slot whose store is not pending
-                    // while the append warp is still blocked on an earlier store --
-                    // a parity ABA that desynchronised it (a hang, seen at 10 and 20
-                    // heads under some timings).
-                    if (p.store_seg >= 0 && kv_it >= uint32_t(kStages)) {
-                        mbar_wait(&store_done[s], ((kv_it / kStages) - 1) & 1);
-#ifdef TM_SPANS_PROD
-                        cyc_store += clock64() - tw1;
-#endif
-                        trace_ev(p, 0, tn, 5);
-                    }
+                    // (With the a3 append active, kv_empty also counts the append
+                    // warp's release of the slot's previous fill, stored or not:
+                    // the append warp waits on EVERY fill's kv_full phase in order,
+                    // and were a slot refillable without it, two fills of a slot
+                    // whose store is not pending could complete while the append
+                    // warp is still blocked on an earlier store -- a parity ABA
+                    // that desynchronised it: a hang, seen at 10 and 20 heads under
+                    // some timings.)
                     // Release this CTA's K/V pushes before the first wait on K/V
                     // (own rank included) or after a few loads, whichever first:
                     // by then the stores have drained and the fence is cheap.
@@ -790,7 +783,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                     int seg, row, valid;
                     tile_info<kMulti>(p, it.pr, it.lo + jj, seg, row, valid);
                     // Observe EVERY position's kv_full phase in order, and release
-                    // every fill (stored or not) through store_done: the producer
+                    // every fill (stored or not) through kv_empty: the producer
                     // refills a slot only after that, so no slot can complete two
                     // phases ahead of this warp (parity ABA either way).  A stored
                     // fill is released once the TMA store has read it; up to one
@@ -799,7 +792,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                     const int s = kv_it % kStages;
                     if (pend == s) {
                         tma_store_wait_read();
-                        mbar_arrive(&store_done[pend]);
+                        mbar_arrive(&kv_empty[pend]);
                         pend = -1;
                     }
                     mbar_wait(&kv_full[s], (kv_it / kStages) & 1);
@@ -813,17 +806,17 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                         tma_store_commit();
                         if (pend >= 0) {
                             asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-                            mbar_arrive(&store_done[pend]);
+                            mbar_arrive(&kv_empty[pend]);
                         }
                         pend = s;
                     } else {
-                        mbar_arrive(&store_done[s]);
+                        mbar_arrive(&kv_empty[s]);
                     }
                 }
             }
             if (pend >= 0) {
                 tma_store_wait_read();
-                mbar_arrive(&store_done[pend]);
+                mbar_arrive(&kv_empty[pend]);
             }
         }
         if (lane == 0) mbar_arrive(store_idle);   // the ring is no longer read by TMA stores
