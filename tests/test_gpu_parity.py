@@ -712,3 +712,31 @@ def test_running_max_moves_every_tile(dtype, growth):
     ref = oracle.window_attention(q.f64, k.f64, v.f64, [L])
     assert rel_err(from_dev(o), ref) <= (FP32_TOL if dtype == "fp32" else BF16_ALARM)
     ca.close()
+
+
+def test_fused_append_stress_small_head_counts():
+    """Regression guard for the producer / append-warp parity ABA (DESIGN Sec 6,
+    a3 store warp): fresh contexts at 10 and 20 heads (stream-K tails with
+    merges, fused c_t append), a sync after every call; the broken protocol
+    trapped within ~30 calls at 10 heads (this test caught it in 2 of 3 runs
+    at 48 calls per context; now 96, twice at 10 heads).  Also checks the last
+    output is finite."""
+    H_list, d, Lr, Lc, NL = (10, 20, 10), 128, 1024, 3072, 8
+    for H in H_list:
+        g = torch.Generator(device="cuda").manual_seed(2506030990 + 3 * H)
+        ca = tm.ChunkAttention(H, d, Lr, Lc, NL, 1)
+        mk = lambda L: torch.randn(L, H, d, device="cuda", dtype=torch.bfloat16, generator=g)
+        sets = [(mk(Lc), mk(Lc), mk(Lc)) for _ in range(3)]
+        kr, vr = mk(Lr), mk(Lr)
+        for layer in range(NL):
+            ca.put_reference(layer, 0, kr, vr)
+        o = torch.empty(Lc, H, d, device="cuda", dtype=torch.bfloat16)
+        chunk = [0] * NL
+        for i in range(96):
+            layer = i % NL
+            chunk[layer] += 1
+            q, k, v = sets[i % 3]
+            ca.attend(layer, 0, chunk[layer], q, k, v, o)
+            torch.cuda.synchronize()
+        assert torch.isfinite(o.float()).all()
+        ca.close()
