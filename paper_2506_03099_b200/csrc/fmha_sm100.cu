@@ -715,11 +715,15 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                     trace_ev(p, 0, tn, 1 + kv);
                     const Prob& P = p.prob[it.pr];
                     mbar_arrive_expect_tx(&kv_full[s], kTileBytes);
-                    if (kMulti && P.packed_R) {
-                        // packed keys: 128 / R boxes of R rows, each from its own
-                        // segment (box offsets are multiples of 1024 B, so the
-                        // 128-B swizzle matches a whole-tile load); boxes past the
-                        // last key reload key 0 (finite data, masked to -inf)
+                    const int k0t = (it.lo + jj) * kBN;
+                    if (kMulti && P.packed_R &&
+                        !(k0t + kBN <= P.Lk && packed_seg(P, k0t) == packed_seg(P, k0t + kBN - 1))) {
+                        // packed keys across segments: 128 / R boxes of R rows,
+                        // each from its own segment (box offsets are multiples of
+                        // 1024 B, so the 128-B swizzle matches a whole-tile load);
+                        // boxes past the last key reload key 0 (finite data,
+                        // masked to -inf).  A tile inside one segment is one
+                        // 128-row box per half, as below.
                         const int R = P.packed_R;
                         const CUtensorMap* m = kv ? &p.tv_sub : &p.tk_sub;
                         for (int r = 0; r < kBN / R; ++r) {
@@ -738,6 +742,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                             tma_load_4d(sKV + s * kTileBytes + hf * kHalfBytes, m, &kv_full[s],
                                         hf * 64, it.h, P.seg_row0[seg] + row, it.b);
                     }
+                    (void)k0t;
                     ++kv_it;
                 }
             }
@@ -751,19 +756,24 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
 #ifdef TM_TRACE_ENABLED
         if (lane == 1) {
         // ------------------------------------------------ trace observer (debug build)
-        // Records when each S MMA group lands (30+i = S_i(j) complete).  Only
-        // s_full is observed: its phases are strictly ordered S0(j), S1(j),
-        // S0(j+1) by the shared S buffer, so a lagging observer cannot alias.
+        // Records when each S MMA group lands (30+i = S_i(j) complete).  The
+        // observer gates nothing, so it can lag two phases behind s_full and
+        // alias; it then stops observing after a bounded wait instead of
+        // trapping (debug instrumentation only).
         if (p.trace != nullptr && blockIdx.x == 0) {
             int tn = 0;
             uint32_t g = 0;
             Item it;
             Cursor cu;
-            while (next_item(p, cu, it))
-                for (int j = it.lo; j < it.hi; ++j, ++g)
-                    for (int i = 0; i < 2; ++i) {
-                        mbar_wait(&s_full[i], g & 1);
-                        trace_ev(p, 4, tn, 30 + i);
+            bool live = true;
+            while (live && next_item(p, cu, it))
+                for (int j = it.lo; live && j < it.hi; ++j, ++g)
+                    for (int i = 0; live && i < 2; ++i) {
+                        const uint32_t a = smem_u32(&s_full[i]);
+                        const long long t0 = clock64();
+                        while (!mbar_try_wait(a, g & 1))
+                            if (clock64() - t0 > (1ll << 24)) { live = false; break; }
+                        if (live) trace_ev(p, 4, tn, 30 + i);
                     }
         }
         }
@@ -1568,7 +1578,10 @@ cudaError_t finish_and_launch(FmhaParams& p, int d, int grid, void* scratch, cud
         const char* e = getenv("TM_L2_PREFETCH");
         return e ? atoi(e) : 2;
     }();
-    p.l2_prefetch = peer ? 0 : l2_prefetch_env;
+    // (no L2 prefetch for peer windows, filled during the launch, nor for the
+    // packed f4 launches, whose operands a prep kernel just wrote: their first
+    // real loads would queue behind the prefetches)
+    p.l2_prefetch = (peer || p.prob[0].packed_R) ? 0 : l2_prefetch_env;
     p.exit_wait_full = exit_wait_full();
     static const bool nomerge = [] {
         const char* e = getenv("TM_DBG_NOMERGE");

@@ -29,16 +29,20 @@ face = torch.tensor([r * 32 + c for r in range(8, 24) for c in range(8, 24)], dt
 for _ in range(3):
     ca.audio(qa, ka, va, oa, face)
 torch.cuda.synchronize()
-ts = []
+import time  # noqa: E402
+ts, hs = [], []
 for _ in range(5):
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
+    t0 = time.perf_counter()
     for _ in range(reps):
         ca.audio(qa, ka, va, oa, face)
+    hs.append((time.perf_counter() - t0) * 1e6 / reps)
     b.record()
     torch.cuda.synchronize()
     ts.append(a.elapsed_time(b) * 1e3 / reps)
-print(f"f4 audio: {statistics.median(ts):.1f} us/call ({ca.launches} launches/call), eager loop")
+print(f"f4 audio: {statistics.median(ts):.1f} us/call ({ca.launches} launches/call), eager loop; "
+      f"host enqueue {statistics.median(hs):.1f} us/call")
 # the same calls captured in a CUDA graph: no host work between launches
 s = torch.cuda.Stream()
 s.wait_stream(torch.cuda.current_stream())
