@@ -46,6 +46,7 @@
 // TMEM: S [0,128) (shared), P0 [128,192) P1 [192,256), O0 [256,256+d) O1 [256+d,256+2d).
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
@@ -53,6 +54,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -187,8 +189,8 @@ struct __align__(64) FmhaParams {
     // persistent schedule
     int ctas;                         // C: persistent CTAs the blocks are scheduled over
     int l2_prefetch;                  // K/V tiles of the first item prefetched into L2 (with its Q) before the PDL wait
-    float* part;                      // piece partials: per (block, CTA) slot [d/4][256] float4 + m[256] + l[256]
-    int* counters;                    // per (block, first CTA of a split unit), zero between launches
+    float* part;                      // piece partials: per (block, CTA) slot [d/8][256] fp16x8 + m, l, m-s [256]
+    unsigned long long* counters;     // per (block, first CTA of a split unit, Q tile): bit n = contributor n in; zero between launches
     unsigned long long* trace;        // debug timeline (TM_TRACE=1), CTA 0 only; may be null
 };
 
@@ -464,6 +466,16 @@ __device__ __forceinline__ uint32_t merge_elem(uint32_t o, float wo, float wk, f
     return __float_as_uint(__fmaf_rn(wk, x, __fmul_rn(__uint_as_float(o), wo)));
 }
 
+__device__ __forceinline__ uint32_t pack_f16x2(float lo, float hi) {   // RN, lo in the low half
+    uint32_t r;
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
+}
+__device__ __forceinline__ float2 unpack_f16x2(uint32_t v) {
+    const __half2 h = *reinterpret_cast<const __half2*>(&v);
+    return __half22float2(h);
+}
+
 __device__ __forceinline__ float max3(float a, float b, float c) {
     float d;
     asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
@@ -516,8 +528,32 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
         : "memory");
 }
 
-__device__ __forceinline__ void softmax_bar() {   // the 256 softmax threads only
-    asm volatile("bar.sync 1, 256;" ::: "memory");
+// Stream-K piece publication: release by the publishing thread after a
+// barrier over its warpgroup (cumulative), acquire by the merger's poller.
+__device__ __forceinline__ void red_release_or(unsigned long long* a, unsigned long long v) {
+    asm volatile("red.release.gpu.global.or.b64 [%0], %1;" ::"l"(a), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* a) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void wg_bar(int i) {   // the 128 threads of softmax warpgroup i
+    asm volatile("bar.sync %0, 128;" ::"r"(2 + i) : "memory");
+}
+
+// Stream-K partials (scratch, zeroed at context creation).  Per (block, CTA)
+// slot of 256 d + 512 floats: three TILE PARTIALS of 64 d + 384 floats, each
+// 128 fp16 O rows as [d/8][128] uint4 (row-fastest: a warp's 16-B accesses are
+// contiguous) followed by m[128], l[128], (m - s)[128]:  kind 0 / 1 = the
+// CTA's first item (a piece k >= 1) for Q tile 0 / 1; kind 2 = its last item
+// (piece 0 of a co-merged unit) for Q tile 1.  Counters: two per (block,
+// first CTA of a split unit), one per Q tile, after the slots.
+template <int D>
+__device__ __forceinline__ float* part_tile(const FmhaParams& p, int blk, int cta, int kind) {
+    constexpr int kTileFloats = 64 * D + 3 * 128;
+    static_assert(3 * kTileFloats <= 256 * D + 512, "tile partials fit the slot");
+    return p.part + (size_t(blk) * kMaxPersistentCtas + cta) * (256 * D + 512) + kind * kTileFloats;
 }
 
 // kKind: 0 one-GPU chunk attention; 1 launches of several problems (f1 window,
@@ -529,6 +565,7 @@ template <int D, uint32_t kPolyMask, int kKind>
 __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_constant__ FmhaParams p) {
     constexpr bool kMulti = kKind == 1, kPeerKind = kKind == 2;
     constexpr int kTileBytes = kBN * D * 2;
+    constexpr int kTileO = 64 * D;   // floats of a tile partial's fp16 O rows (then m, l, m - s)
     constexpr uint32_t kIdescS = make_idesc_bf16(kBM, kBN, 0, 0);   // Q, K both K-major
     constexpr uint32_t kIdescO = make_idesc_bf16(kBM, D, 0, 1);     // P (TMEM), V MN-major
 
@@ -549,8 +586,8 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
     uint64_t* o_done = o_empty + 2;          // [2]  each PV_i complete (P_i reusable)
     uint64_t* s_free = o_done + 2;           // [1]  S buffer loaded into registers
     uint64_t* store_idle = s_free + 1;       // [1] append warp done (one phase per launch)
-    uint64_t* merge_bar = store_idle + 1;          // [3] a half partial landed in merge buffer j
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(merge_bar + 3);
+    uint64_t* merge_bar = store_idle + 1;    // [6] merge buffer j of warpgroup i: 3 i + j
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(merge_bar + 6);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -568,14 +605,14 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
             mbar_init(&o_done[i], 1);
         }
         mbar_init(s_free, 128);
+        mbar_init(store_idle, 1);
+        for (int j = 0; j < 6; ++j) mbar_init(&merge_bar[j], 1);
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&kv_full[s], 1);
             // with the a3 append active, a fill is released by the MMA commit AND
             // by the append warp (which has then passed it, stored or not)
             mbar_init(&kv_empty[s], p.store_seg >= 0 ? 2 : 1);
         }
-        mbar_init(store_idle, 1);
-        for (int j = 0; j < 3; ++j) mbar_init(&merge_bar[j], 1);
         fence_mbar_init();
     }
     if (warp == 8 && lane == 0) {
@@ -1047,6 +1084,19 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
             if (threadIdx.x == 0) trace_span(p, 2);   // (spans A/B) this item's epilogue begins
 #endif
             const int q = it.qp * 2 * kBM + row_in_pair;
+            // Split units (stream-K pieces).  Each softmax warpgroup
+            // (Q tile i of the unit) is its own merge participant: tile i's
+            // merger keeps O_i in TMEM, waits until the unit's other pieces have
+            // published their tile-i partials, merges them in piece order and
+            // stores the rows; every other piece publishes its tile-i partial.
+            // Tile 0 is merged by piece 0 (its CTA's last item).  With >= 3
+            // pieces, piece 1 spans its CTA's whole range, so it also ends with
+            // the launch: it merges tile 1 (ROW-SPLIT CO-MERGE), and piece 0
+            // publishes its tile-1 partial instead.  Each leg of the chain that
+            // follows the last tile -- partial write, partial reads, output store
+            // -- then moves 32 KB through one SM instead of 64-128 KB.
+            const bool co = it.piece && it.npieces >= 3;
+            const int merger_piece = (i == 1 && co) ? 1 : 0;
             if (!it.piece || p.dbg_nomerge) {   // (dbg_nomerge: timing bound only, wrong output)
                 store_rows_bf16<D, kKind>(p, p.prob[it.pr], tOi, 1.f / l, sEpi + warp * 4096, it.b, q - lane,
                                    it.h, lane);
@@ -1055,113 +1105,146 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
 #endif
                 tc_fence_before();
                 mbar_arrive(&o_empty[i]);
-            } else if (it.pidx > 0) {
-                // piece k >= 1 of a split unit (this CTA's first item): unnormalised
-                // O, running max m (log2 units) and l to this CTA's partial slot,
-                // then count it in for the unit's merger (piece 0).
-                constexpr int kPieceFloats = 256 * D + 512;
-                // the slot of this piece's block-local CTA (where the merger looks)
-                float* base = p.part + (size_t(it.blk) * kMaxPersistentCtas + it.cl) * kPieceFloats;
-                float4* po = reinterpret_cast<float4*>(base);
+            } else if (it.pidx != merger_piece) {
+                // Publish this piece's tile-i partial: the unnormalised O row
+                // scaled by 2^s into fp16 (s per row, a power of two so the
+                // scaling is exact: the row's largest |O| lands in [2^14, 2^15),
+                // relative rounding <= 2^-11 of it), the running max m (log2
+                // units), l and m - s (the exponent of the O weight); then count
+                // it in for the tile's merger.  A first item (piece >= 1) uses its
+                // CTA's first-item slot; piece 0 (co-merge) the last-item slot.
+#ifdef TM_SPANS_PUB
+                if (threadIdx.x == 0) trace_span(p, 4);   // (spans A/B) partner's tiles done
+#endif
+                float* tp = part_tile<D>(p, it.blk, it.cl, it.pidx == 0 ? 2 : i);
+                uint4* po = reinterpret_cast<uint4*>(tp);
+                const int r = wq * 32 + lane;             // row within the tile
+                uint32_t o[D];
 #pragma unroll
-                for (int c = 0; c < D; c += 32) {
-                    uint32_t o[32];
-                    tmem_ld32(tOi + c, o);
-                    tmem_wait_ld();
-#pragma unroll
-                    for (int e = 0; e < 8; ++e)
-                        po[((c >> 2) + e) * 256 + row_in_pair] =
-                            make_float4(__uint_as_float(o[4 * e]), __uint_as_float(o[4 * e + 1]),
-                                        __uint_as_float(o[4 * e + 2]), __uint_as_float(o[4 * e + 3]));
-                }
+                for (int c = 0; c < D; c += 32) tmem_ld32(tOi + c, o + c);
+                tmem_wait_ld();
                 tc_fence_before();
-                mbar_arrive(&o_empty[i]);
-                base[256 * D + row_in_pair] = m_run;
-                base[256 * D + 256 + row_in_pair] = l;
-                softmax_bar();                // every thread's partial stores precede ...
-                if (threadIdx.x == 0) {       // ... this one fence (cumulative) and the count
-                    __threadfence();
-                    atomicAdd(&p.counters[it.blk * kMaxPersistentCtas + it.cfirst], 1);
+                mbar_arrive(&o_empty[i]);     // O_i read out: the next item's PV may write it
+                float amax = 0.f;
+#pragma unroll
+                for (int c = 0; c < D; ++c) amax = fmaxf(amax, fabsf(__uint_as_float(o[c])));
+                int sx = 141 - int((__float_as_uint(amax) >> 23) & 0xffu);
+                sx = sx < -100 ? -100 : (sx > 100 ? 100 : sx);
+                const float sc = __uint_as_float(uint32_t(127 + sx) << 23);   // 2^s exactly
+#pragma unroll
+                for (int c = 0; c < D; c += 8) {
+                    uint4 v;
+                    v.x = pack_f16x2(__uint_as_float(o[c]) * sc, __uint_as_float(o[c + 1]) * sc);
+                    v.y = pack_f16x2(__uint_as_float(o[c + 2]) * sc, __uint_as_float(o[c + 3]) * sc);
+                    v.z = pack_f16x2(__uint_as_float(o[c + 4]) * sc, __uint_as_float(o[c + 5]) * sc);
+                    v.w = pack_f16x2(__uint_as_float(o[c + 6]) * sc, __uint_as_float(o[c + 7]) * sc);
+                    po[(c >> 3) * kBM + r] = v;
+                }
+                tp[kTileO + r] = m_run;
+                tp[kTileO + kBM + r] = l;
+                tp[kTileO + 2 * kBM + r] = m_run - float(sx);
+                wg_bar(i);                    // the warpgroup's partial stores precede ...
+                if (wq == 0 && lane == 0) {   // ... this one release (cumulative over the barrier)
+                    const int mp = (i == 1 && co) ? 1 : 0;          // the tile's merger piece
+                    const int n = it.pidx < mp ? it.pidx : it.pidx - 1;   // contributor index
+                    red_release_or(&p.counters[(it.blk * kMaxPersistentCtas + it.cfirst) * 2 + i], 1ull << n);
+#ifdef TM_SPANS_PUB
+                    trace_span(p, 6);                 // (spans A/B) partial published
+#endif
                 }
             } else {
-                // piece 0 of a split unit = this CTA's LAST item of the block (its
-                // range ends inside the unit), so O_i stays in TMEM: wait until
-                // the other pieces (first tail items of the next CTAs, long
-                // finished) are in, then merge them into the TMEM accumulator in
-                // piece order (deterministic) and store the output.  No partial
-                // of its own.
-                constexpr int kPieceFloats = 256 * D + 512;
+                // Tile i's merger (its CTA's last item of the block), O_i in TMEM:
+                // wait for the other np - 1 pieces' tile-i partials, merge them
+                // in piece order (deterministic, no float atomics) and store.
                 if (threadIdx.x == 0) trace_span(p, 4);
-                if (threadIdx.x == 0) {
-                    volatile int* ctr = p.counters + it.blk * kMaxPersistentCtas + it.cfirst;
-                    const long long t0 = clock64();
-                    while (*ctr != it.npieces - 1)
-                        if (clock64() - t0 > (1ll << 33)) __trap();
-                    *ctr = 0;                               // ready for the next launch
-                }
-                __threadfence();
-                softmax_bar();
-                if (threadIdx.x == 0) trace_span(p, 5);
-                auto piece_base = [&](int k) {
-                    return p.part + (size_t(it.blk) * kMaxPersistentCtas + it.cfirst + k) * kPieceFloats;
-                };
-                // If this is the CTA's last item overall: no more Q or K/V loads,
-                // and once store_idle has completed no append store reads the
-                // ring.  The pieces' O partials are then pulled in column halves
-                // (chunk j = piece 1 + j/2, half j%2) by bulk copies into three
-                // buffers over the Q tiles and the ring, three chunks in flight;
-                // each thread reads its row from shared memory (conflict-free
-                // [d/4][256] float4 layout) and accumulates into O_i in TMEM.
-                // Otherwise (a later schedule block follows, its loads already in
-                // flight) each thread loads its row of the partials from L2
-                // directly.  Both apply the same per-element update in the same
-                // piece order (merge_elem), so the result is the same bits.  The
-                // weights need every piece's m and l first: loaded from global,
-                // up to 8 pieces per batch of independent loads, overlapping the
-                // first copies.
-                constexpr uint32_t kChunkBytes = 256 * (D / 2) * 4;
-                static_assert(3 * kChunkBytes <= (2 + kStages) * kTileBytes,
-                              "three merge buffers fit the Q tiles + the ring");
                 const int np = it.npieces;
-                const int nchunks = 2 * (np - 1);
+                const int nc = np - 1;            // contributors (<= 64: cached_class caps pieces)
+                const int r = wq * 32 + lane;
+                // contributor n (0 .. np-2) in piece order, skipping the merger
+                auto contrib = [&](int n) -> const float* {
+                    const int k = n < merger_piece ? n : n + 1;
+                    return k == 0 ? part_tile<D>(p, it.blk, it.cfirst, 2)     // piece 0's last-item slot
+                                  : part_tile<D>(p, it.blk, it.cfirst + k, i);
+                };
+                // If this is the CTA's last item overall (no more Q or K/V loads),
+                // the contributors' O rows (32 KB each) are pulled by bulk copies
+                // into three buffers of this warpgroup -- its Q tile and two ring
+                // slots -- three in flight, each issued as soon as its
+                // contributor's bit is in (early pieces copy while the late one
+                // finishes); each thread reads its row from shared memory
+                // ([d/8][128] uint4: conflict-free).  The ring is reused once both
+                // tiles' last MMAs are complete (o_final of the other tile too) and
+                // no append store reads it (store_idle).  Otherwise (a later
+                // schedule block follows, its loads already in flight) each thread
+                // loads its row from L2 directly.  Both apply the same per-element
+                // update in the same piece order (merge_elem): the same bits.
+                constexpr uint32_t kRowsBytes = kBM * D * 2;
+                static_assert(kRowsBytes == kTileBytes && kStages >= 4, "merge buffers: Q tile + 2 ring slots");
                 Cursor cpeek = cu;
                 Item nx;
                 const bool smem_merge = !next_item(p, cpeek, nx);
-                auto issue_chunk = [&](int j) {
-                    mbar_arrive_expect_tx(&merge_bar[j % 3], kChunkBytes);
-                    bulk_g2s(smem + (j % 3) * kChunkBytes, piece_base(1 + j / 2) + (j & 1) * 128 * D,
-                             kChunkBytes, &merge_bar[j % 3]);
+                auto buf = [&](int j) -> uint8_t* {
+                    return j == 0 ? sQ + i * kTileBytes : sKV + (2 * i + j - 1) * kTileBytes;
                 };
-                if (smem_merge && threadIdx.x == 0) {
-                    mbar_wait(store_idle, 0);
-                    fence_proxy_async_global();
-                    for (int j = 0; j < 3 && j < nchunks; ++j) issue_chunk(j);
+                auto issue = [&](int n) {
+                    uint64_t* bar = &merge_bar[3 * i + n % 3];
+                    mbar_arrive_expect_tx(bar, kRowsBytes);
+                    fence_proxy_async_global();        // generic-proxy writes -> bulk-copy reads
+                    bulk_g2s(buf(n % 3), contrib(n), kRowsBytes, bar);
+                };
+                if (wq == 0 && lane == 0) {
+                    unsigned long long* vc = p.counters + (it.blk * kMaxPersistentCtas + it.cfirst) * 2 + i;
+                    const unsigned long long all = nc >= 64 ? ~0ull : (1ull << nc) - 1;
+                    const int pre = nc < 3 ? nc : 3;             // copies issued while waiting
+                    unsigned long long issued = 0;
+                    if (smem_merge) {
+                        mbar_wait(&o_final[i ^ 1], n_item & 1);   // the other tile's MMAs are done too
+                        mbar_wait(store_idle, 0);
+                        tc_fence_after();
+                    }
+                    const long long t0 = clock64();
+                    for (;;) {
+                        const unsigned long long m = ld_acquire_u64(vc);
+                        if (smem_merge) {
+                            const unsigned long long nw = m & ~issued & ((1ull << pre) - 1);
+                            if (nw) {
+                                for (int n = 0; n < pre; ++n)
+                                    if ((nw >> n) & 1) issue(n);
+                                issued |= nw;
+                            }
+                        }
+                        if (m == all) break;
+                        if (clock64() - t0 > (1ll << 33)) __trap();
+                    }
+                    *vc = 0;                                // ready for the next launch
                 }
+                wg_bar(i);                    // thread 0's acquire covers the warpgroup's reads
+                if (threadIdx.x == 0) trace_span(p, 5);
                 float mm[8], ll[8];
 #pragma unroll
                 for (int e = 0; e < 8; ++e) {
-                    const bool in = 1 + e < np;
-                    mm[e] = in ? __ldcg(piece_base(1 + e) + 256 * D + row_in_pair) : -INFINITY;
-                    ll[e] = in ? __ldcg(piece_base(1 + e) + 256 * D + 256 + row_in_pair) : 0.f;
+                    const bool in = e < nc;
+                    mm[e] = in ? __ldcg(contrib(e) + kTileO + r) : -INFINITY;
+                    ll[e] = in ? __ldcg(contrib(e) + kTileO + kBM + r) : 0.f;
                 }
                 float mstar = m_run;
 #pragma unroll
                 for (int e = 0; e < 8; ++e) mstar = fmaxf(mstar, mm[e]);
-                for (int k0 = 9; k0 < np; k0 += 8) {        // more than 9 pieces (long units)
+                for (int k0 = 8; k0 < nc; k0 += 8) {        // more than 9 pieces (long units)
 #pragma unroll
                     for (int e = 0; e < 8; ++e)
-                        if (k0 + e < np) mstar = fmaxf(mstar, __ldcg(piece_base(k0 + e) + 256 * D + row_in_pair));
+                        if (k0 + e < nc) mstar = fmaxf(mstar, __ldcg(contrib(k0 + e) + kTileO + r));
                 }
                 const float w0 = ex2(m_run - mstar);
                 float wsum = w0 * l;
 #pragma unroll
                 for (int e = 0; e < 8; ++e) wsum += ex2(mm[e] - mstar) * ll[e];
-                for (int k0 = 9; k0 < np; k0 += 8) {
+                for (int k0 = 8; k0 < nc; k0 += 8) {
 #pragma unroll
                     for (int e = 0; e < 8; ++e) {
-                        const bool in = k0 + e < np;
-                        const float m2 = in ? __ldcg(piece_base(k0 + e) + 256 * D + row_in_pair) : -INFINITY;
-                        const float l2 = in ? __ldcg(piece_base(k0 + e) + 256 * D + 256 + row_in_pair) : 0.f;
+                        const bool in = k0 + e < nc;
+                        const float m2 = in ? __ldcg(contrib(k0 + e) + kTileO + r) : -INFINITY;
+                        const float l2 = in ? __ldcg(contrib(k0 + e) + kTileO + kBM + r) : 0.f;
                         wsum += ex2(m2 - mstar) * l2;
                     }
                 }
@@ -1169,60 +1252,46 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
 #ifdef TM_SPANS_MERGE2
                 if (threadIdx.x == 0) trace_span(p, 1);      // (spans A/B) weights ready
 #endif
-                float m_cur = mm[0];
-                for (int k = 1; k < np; ++k) {
-                    // piece k+1's m, consumed one piece later (latency hidden)
-                    const float m_nxt = k + 1 < np ? __ldcg(piece_base(k + 1) + 256 * D + row_in_pair) : 0.f;
-                    const float wk = ex2(m_cur - mstar);
-                    const float wo = k == 1 ? w0 : 1.f;
-                    if (!smem_merge) {
-                        const float4* gp = reinterpret_cast<const float4*>(piece_base(k));
-#pragma unroll 1
-                        for (int c = 0; c < D; c += 32) {
-                            uint32_t o[32];
-                            tmem_ld32(tOi + c, o);
-                            float4 x[8];
+                // O <- O * wo + wk * x per contributor; wk = 2^(m_k - s_k - m*)
+                // (its fp16 rows carry 2^s_k); wo = w0 once, then 1.
+                float mo_nxt = __ldcg(contrib(0) + kTileO + 2 * kBM + r);
+                for (int n = 0; n < nc; ++n) {
+                    const float wk = ex2(mo_nxt - mstar);
+                    if (n + 1 < nc) mo_nxt = __ldcg(contrib(n + 1) + kTileO + 2 * kBM + r);
+                    const float wo = n == 0 ? w0 : 1.f;
+                    uint4 x[D / 8];
+                    if (smem_merge) {
+                        mbar_wait(&merge_bar[3 * i + n % 3], (n / 3) & 1);
+                        const uint4* sp = reinterpret_cast<const uint4*>(buf(n % 3));
 #pragma unroll
-                            for (int e = 0; e < 8; ++e) x[e] = __ldcg(gp + ((c >> 2) + e) * 256 + row_in_pair);
-                            tmem_wait_ld();
-#pragma unroll
-                            for (int e = 0; e < 8; ++e) {
-                                o[4 * e] = merge_elem(o[4 * e], wo, wk, x[e].x);
-                                o[4 * e + 1] = merge_elem(o[4 * e + 1], wo, wk, x[e].y);
-                                o[4 * e + 2] = merge_elem(o[4 * e + 2], wo, wk, x[e].z);
-                                o[4 * e + 3] = merge_elem(o[4 * e + 3], wo, wk, x[e].w);
-                            }
-                            tmem_st32(tOi + c, o);
+                        for (int c = 0; c < D / 8; ++c) x[c] = sp[c * kBM + r];
+                        if (n + 3 < nc) {
+                            wg_bar(i);              // the warpgroup is done with this buffer
+                            if (wq == 0 && lane == 0) issue(n + 3);
                         }
-                        m_cur = m_nxt;
-                        continue;
+                    } else {
+                        const uint4* gp = reinterpret_cast<const uint4*>(contrib(n));
+#pragma unroll
+                        for (int c = 0; c < D / 8; ++c) x[c] = __ldcg(gp + c * kBM + r);
                     }
-#pragma unroll 1
-                    for (int h = 0; h < 2; ++h) {
-                        const int j = 2 * (k - 1) + h;
-                        mbar_wait(&merge_bar[j % 3], (j / 3) & 1);
-                        const float4* sp = reinterpret_cast<const float4*>(smem + (j % 3) * kChunkBytes);
-#pragma unroll 1
-                        for (int c = 0; c < D / 2; c += 32) {
-                            uint32_t o[32];
-                            tmem_ld32(tOi + h * (D / 2) + c, o);
-                            tmem_wait_ld();
 #pragma unroll
-                            for (int e = 0; e < 8; ++e) {
-                                const float4 x = sp[((c >> 2) + e) * 256 + row_in_pair];
-                                o[4 * e] = merge_elem(o[4 * e], wo, wk, x.x);
-                                o[4 * e + 1] = merge_elem(o[4 * e + 1], wo, wk, x.y);
-                                o[4 * e + 2] = merge_elem(o[4 * e + 2], wo, wk, x.z);
-                                o[4 * e + 3] = merge_elem(o[4 * e + 3], wo, wk, x.w);
+                    for (int c = 0; c < D; c += 32) {
+                        uint32_t o[32];
+                        tmem_ld32(tOi + c, o);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const uint4 v = x[(c >> 3) + e];
+                            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                            for (int t = 0; t < 4; ++t) {
+                                const float2 f = unpack_f16x2(w[t]);
+                                o[8 * e + 2 * t] = merge_elem(o[8 * e + 2 * t], wo, wk, f.x);
+                                o[8 * e + 2 * t + 1] = merge_elem(o[8 * e + 2 * t + 1], wo, wk, f.y);
                             }
-                            tmem_st32(tOi + h * (D / 2) + c, o);
                         }
-                        if (j + 3 < nchunks) {
-                            softmax_bar();          // everyone done with buffer j % 3
-                            if (threadIdx.x == 0) issue_chunk(j + 3);
-                        }
+                        tmem_st32(tOi + c, o);
                     }
-                    m_cur = m_nxt;
                 }
                 tmem_wait_st();
 #ifdef TM_SPANS_MERGE2
@@ -1246,7 +1315,9 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
         if (threadIdx.x == 0) trace_span(p, 4);   // (spans A/B) softmax loop left, before the final barrier
 #endif
         if (threadIdx.x == 0) {
+#ifndef TM_SPANS_PUB
             trace_span(p, 6, g);
+#endif
             uint32_t smid;
             asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
             trace_span(p, 7, n_item | (long long)smid << 16);
@@ -1464,7 +1535,7 @@ bool pdl_enabled() {
 
 size_t fmha_sm100_scratch_bytes(int d) {
     return size_t(kMaxBlocks) * kMaxPersistentCtas * (256 * size_t(d) + 512) * 4 +
-           size_t(kMaxBlocks) * kMaxPersistentCtas * 4;
+           size_t(kMaxBlocks) * kMaxPersistentCtas * 2 * 8;
 }
 
 namespace {
@@ -1500,9 +1571,20 @@ bool cached_class(int T, int n, int C, SkClass& k) {
     std::lock_guard<std::mutex> lock(mu);
     std::vector<int>& b = cache[std::make_tuple(T, n, C)];
     if (b.empty()) {
-        b.assign(kMaxPersistentCtas + 1, 0);
-        const int g = tail_bounds(T, n, C, kMinPiece, b.data());
-        b.resize(g + 1);
+        // A split unit's merger tracks its contributors in a 64-bit mask:
+        // raise the minimum piece until no unit has more than 65 pieces.
+        for (int min_piece = kMinPiece;; min_piece *= 2) {
+            b.assign(kMaxPersistentCtas + 1, 0);
+            const int g = tail_bounds(T, n, C, min_piece, b.data());
+            b.resize(g + 1);
+            int worst = 1;
+            for (int u = 0; u < T; ++u) {
+                const int first = int(std::upper_bound(b.begin(), b.end(), u * n) - b.begin()) - 1;
+                const int last = int(std::upper_bound(b.begin(), b.end(), u * n + n - 1) - b.begin()) - 1;
+                worst = std::max(worst, last - first + 1);
+            }
+            if (worst <= 65 || min_piece >= n) break;
+        }
     }
     const int G = int(b.size()) - 1;
     if (G <= 0) return false;
@@ -1590,7 +1672,7 @@ cudaError_t finish_and_launch(FmhaParams& p, int d, int grid, void* scratch, cud
     p.dbg_nomerge = nomerge;
     p.trace = trace;
     p.part = static_cast<float*>(scratch);
-    p.counters = reinterpret_cast<int*>(static_cast<uint8_t*>(scratch) +
+    p.counters = reinterpret_cast<unsigned long long*>(static_cast<uint8_t*>(scratch) +
                                         size_t(kMaxBlocks) * kMaxPersistentCtas *
                                             (256 * size_t(d) + 512) * 4);
     if (grid <= 0) return cudaErrorInvalidValue;

@@ -90,6 +90,40 @@ def test_many_pieces_d64_bf16(Lr, Lc):
     assert err <= BF16_ALARM, err
 
 
+def test_more_pieces_than_the_contributor_mask():
+    """One unit over ~630 KV tiles: at the default minimum piece it would be
+    cut into ~148 pieces; the merger tracks contributors in a 64-bit mask, so
+    the schedule raises the minimum piece until a unit has <= 65 pieces."""
+    err = run_stream(1, 128, 80000, 130, "bf16", chunks=1)
+    assert err <= BF16_ALARM, err
+
+
+@pytest.mark.parametrize("vscale_log2", [15, -20])
+def test_many_pieces_extreme_value_scales(vscale_log2):
+    """Stream-K partials are fp16 rows with a per-row power-of-two scale (the
+    row's max |O| lands in [2^14, 2^15)).  V scaled by 2^15 (unscaled fp16
+    partials of the unnormalised O would overflow 65504) and by 2^-20 (they
+    would underflow) still merge within the bf16 alarm; co-merged units
+    (>= 3 pieces) and 13-partial merges both occur at Lr = 7000."""
+    H, d, Lr, Lc = 2, 128, 7000, 300
+    f = 2.0 ** vscale_log2
+    si = syn.StreamInputs(H, d, Lr, Lc, "bf16", "D0", syn.SEED_BASE + 77)
+    ca = tm.ChunkAttention(H, d, Lr, Lc, 1, 1)
+    so = oracle.StreamOracle()
+    _, k, v = si.chunk(0, 0, 0)
+    ca.put_reference(0, 0, to_dev(k), to_dev(v) * f)          # power-of-two scale: exact in bf16
+    so.put_reference(0, 0, k.f64, v.f64 * f)
+    worst = 0.0
+    for t in (1, 2):
+        q, k, v = si.chunk(0, 0, t)
+        o = torch.empty_like(to_dev(q))
+        ca.attend(0, 0, t, to_dev(q), to_dev(k), to_dev(v) * f, o)
+        ref = so.attend(0, 0, t, q.f64, k.f64, v.f64 * f)
+        worst = max(worst, rel_err(from_dev(o), ref))
+    ca.close()
+    assert worst <= BF16_ALARM, worst
+
+
 @pytest.mark.parametrize("dist", ["D1", "D2", "D3", "D6"])
 def test_distributions_bf16(dist):
     err = run_stream(4, 128, 256, 640, "bf16", dist=dist, chunks=3)
