@@ -169,6 +169,7 @@ struct __align__(64) FmhaParams {
     int tma_epi;                      // 1: epilogue rows leave through TMA stores of the staging
     int exit_wait_full;               // A/B: wait for the epilogue TMA stores' global writes at exit
     int dbg_nomerge;                  // timing experiments only (TM_DBG_NOMERGE=1): pieces store unmerged
+    int dbg_nolatestore;              // timing bound only (TM_DBG_NOLATESTORE=1): no append stores in a CTA's last item
     int64_t o_bstride;                // rows between batch elements of an o_dst
     int o_rows, o_H, o_h0;
     // f4 zero fill (spare warp, concurrent with the attention): rows r in
@@ -824,6 +825,12 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
             Cursor cu;
             while (next_item(p, cu, it)) {
                 const int nkv = it.hi - it.lo;
+                bool skip_store = false;
+                if (p.dbg_nolatestore) {
+                    Cursor pk = cu;
+                    Item nx;
+                    skip_store = !next_item(p, pk, nx);
+                }
                 for (int q = 0; q < 2 * nkv; ++q, ++kv_it) {
                     int jj, kv;
                     load_order(q, nkv, jj, kv);
@@ -844,7 +851,7 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                     }
                     mbar_wait(&kv_full[s], (kv_it / kStages) & 1);
                     trace_ev(p, 2, tn, 40 + kv);
-                    if (stores_tile(p, it, seg, row)) {
+                    if (!skip_store && stores_tile(p, it, seg, row)) {
                         fence_proxy_async_smem();
                         const CUtensorMap* m = kv ? &p.tv_store : &p.tk_store;
                         for (int hf = 0; hf < D / 64; ++hf)
@@ -1670,6 +1677,11 @@ cudaError_t finish_and_launch(FmhaParams& p, int d, int grid, void* scratch, cud
         return e && *e && strcmp(e, "0") != 0;
     }();
     p.dbg_nomerge = nomerge;
+    static const bool nolatestore = [] {
+        const char* e = getenv("TM_DBG_NOLATESTORE");
+        return e && *e && strcmp(e, "0") != 0;
+    }();
+    p.dbg_nolatestore = nolatestore;
     p.trace = trace;
     p.part = static_cast<float*>(scratch);
     p.counters = reinterpret_cast<unsigned long long*>(static_cast<uint8_t*>(scratch) +
