@@ -75,8 +75,8 @@ def test_invalid_configs_are_rejected(bad):
 
 def test_workspace_sizes():
     # bf16: debug flag + split-KV scratch: 1 partial slot per (schedule block <= 8, persistent
-    # CTA <= 160) + counters
-    scratch = 8 * 160 * (256 * 128 + 512) * 4 + 8 * 160 * 4
+    # CTA <= 160; three fp16 tile partials fit it) + two 64-bit contributor masks (one per Q tile)
+    scratch = 8 * 160 * (256 * 128 + 512) * 4 + 8 * 160 * 2 * 8
     assert tm.tm_workspace_bytes(wan512()) == 1024 + (scratch + 1023) // 1024 * 1024
     assert tm.tm_workspace_bytes(wan512(dtype=tm.TM_FP32)) == 1024
     ws8 = tm.tm_workspace_bytes(wan512(world_size=8))
@@ -117,7 +117,7 @@ def test_peer_workspace_layout():
     counters, Q/K/V windows [B][max(Lc,Lr)][H/P][d] and the O window
     [B][ceil(Lc/P)][H][d], each 1024-B aligned; no NCCL staging."""
     al = lambda x: (x + 1023) // 1024 * 1024
-    scratch = 1024 + al(8 * 160 * (256 * 128 + 512) * 4 + 8 * 160 * 4)
+    scratch = 1024 + al(8 * 160 * (256 * 128 + 512) * 4 + 8 * 160 * 2 * 8)
     for P in (1, 2, 8):
         c = wan512(world_size=P, transport=tm.TM_TRANSPORT_PEER)
         win = 4096 + 3 * al(3072 * (40 // P) * 128 * 2) + al(-(-3072 // P) * 40 * 128 * 2)
@@ -127,7 +127,7 @@ def test_peer_workspace_layout():
     assert tm.tm_workspace_bytes(c) == scratch + win
     # Lr > Lc: the K/V windows also carry the reference push
     c = tm.make_config(4, 64, 500, 100, 1, 1, world_size=2, transport=tm.TM_TRANSPORT_PEER)
-    scratch64 = 1024 + al(8 * 160 * (256 * 64 + 512) * 4 + 8 * 160 * 4)
+    scratch64 = 1024 + al(8 * 160 * (256 * 64 + 512) * 4 + 8 * 160 * 2 * 8)
     assert tm.tm_workspace_bytes(c) == scratch64 + 4096 + 3 * al(500 * 2 * 64 * 2) + al(50 * 4 * 64 * 2)
 
 
