@@ -1797,6 +1797,15 @@ cudaError_t launch_fmha_sm100(const AttnProblem& pr, void* scratch, cudaStream_t
                              pr.peer != nullptr, pr.peer != nullptr ? 2 : 0);
 }
 
+// The kMulti kernel variant only for launches that use its code (packed keys,
+// the f4 zero fill); the f1 window's problems run on the chunk-attention kernel
+// (the extra code measured 1-3 % slower where it is compiled in but unused).
+int multi_kind(const FmhaParams& p) {
+    bool packed = false;
+    for (int i = 0; i < p.nprob; ++i) packed |= p.prob[i].packed_R != 0;
+    return (packed || p.zf_inv != nullptr) ? 1 : 0;
+}
+
 cudaError_t launch_fmha_sm100_multi(const MultiProblem& mp, void* scratch, cudaStream_t stream,
                                     int* launches, unsigned long long* trace) {
     if (mp.d != 64 && mp.d != 128) return cudaErrorInvalidValue;
@@ -1882,7 +1891,7 @@ cudaError_t launch_fmha_sm100_multi(const MultiProblem& mp, void* scratch, cudaS
             if (add_block(p, i, h0, hb, C, &full)) continue;
             if (!full) return cudaErrorInvalidValue;
             cudaError_t e = finish_and_launch(p, mp.d, launch_grid(p), scratch, stream, launches,
-                                              trace, false, 1);
+                                              trace, false, multi_kind(p));
             if (e != cudaSuccess) return e;
             p.zf_inv = nullptr;               // the first launch zero-filled
             p.nblk = 0;
@@ -1890,7 +1899,7 @@ cudaError_t launch_fmha_sm100_multi(const MultiProblem& mp, void* scratch, cudaS
             if (!add_block(p, i, h0, hb, C, &full)) return cudaErrorInvalidValue;
         }
     }
-    return finish_and_launch(p, mp.d, launch_grid(p), scratch, stream, launches, trace, false, 1);
+    return finish_and_launch(p, mp.d, launch_grid(p), scratch, stream, launches, trace, false, multi_kind(p));
 }
 
 }  // namespace tmk
