@@ -876,15 +876,26 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
         if (lane == 0) mbar_arrive(store_idle);   // the ring is no longer read by TMA stores
         if (kMulti && p.zf_inv != nullptr) {
             // f4: zero the non-face rows of o, this CTA's share (warp-uniform branch)
+            // 32 of this CTA's rows per batch: each lane loads one row's face-map
+            // entry (one L2 round trip per batch, not per row), then the warp
+            // zeroes the batch's non-face rows.
             const int words = p.o_H * D / 8;                  // 16-B words per token row
             const int64_t total = int64_t(p.B) * p.zf_rows;
             const uint4 z = make_uint4(0, 0, 0, 0);
-            for (int64_t r = blockIdx.x; r < total; r += gridDim.x) {
-                const int64_t b = r / p.zf_rows, rr = p.zf_row0 + r % p.zf_rows;
-                if (__ldg(p.zf_inv + rr % p.zf_T) >= 0) continue;
-                uint4* row = reinterpret_cast<uint4*>(p.o_dst[0] + (b * p.o_bstride + rr) * int64_t(p.o_H) * D);
+            for (int64_t r0 = blockIdx.x; r0 < total; r0 += 32 * int64_t(gridDim.x)) {
+                const int64_t rl = r0 + int64_t(lane) * gridDim.x;
+                bool zero = false;
+                if (rl < total) zero = __ldg(p.zf_inv + (p.zf_row0 + rl % p.zf_rows) % p.zf_T) < 0;
+                uint32_t m = __ballot_sync(0xffffffffu, zero);
+                while (m) {
+                    const int k = __ffs(m) - 1;
+                    m &= m - 1;
+                    const int64_t r = r0 + int64_t(k) * gridDim.x;
+                    const int64_t b = r / p.zf_rows, rr = p.zf_row0 + r % p.zf_rows;
+                    uint4* row = reinterpret_cast<uint4*>(p.o_dst[0] + (b * p.o_bstride + rr) * int64_t(p.o_H) * D);
 #pragma unroll 4
-                for (int w = lane; w < words; w += 32) __stcs(row + w, z);
+                    for (int w = lane; w < words; w += 32) __stcs(row + w, z);
+                }
             }
         }
       } else if (warp == 9 || warp == 11) {
