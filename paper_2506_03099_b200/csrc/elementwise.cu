@@ -255,8 +255,10 @@ __global__ void __launch_bounds__(128) audio_prep_kernel(const uint4* __restrict
         __syncthreads();
         for (int t = threadIdx.x; t < T; t += blockDim.x) inv_out[t] = inv[t];
     }
-    // One warp per face row; lanes stride over the row's W 16-byte words,
-    // 8 loads in flight per lane before the stores.
+    // One warp per face row; lanes stride over the row's W 16-byte words, 20
+    // loads in flight per lane before the stores (a 40-head d = 128 row, 640
+    // words, is one round trip).
+    constexpr int kU = 20;
     const int lane = threadIdx.x & 31;
     const int64_t rows = BF * nf;
     const int64_t wstride = int64_t(gridDim.x) * (blockDim.x >> 5);
@@ -265,13 +267,13 @@ __global__ void __launch_bounds__(128) audio_prep_kernel(const uint4* __restrict
         if (t < 0 || t >= T) continue;
         const uint4* src = q + ((r / nf) * T + t) * W;
         uint4* dst = qf + r * W;
-        for (int w0 = lane; w0 < W; w0 += 256) {
-            uint4 v[8];
+        for (int w0 = lane; w0 < W; w0 += 32 * kU) {
+            uint4 v[kU];
 #pragma unroll
-            for (int u = 0; u < 8; ++u)
+            for (int u = 0; u < kU; ++u)
                 if (w0 + 32 * u < W) v[u] = __ldcs(src + w0 + 32 * u);
 #pragma unroll
-            for (int u = 0; u < 8; ++u)
+            for (int u = 0; u < kU; ++u)
                 if (w0 + 32 * u < W) dst[w0 + 32 * u] = v[u];
         }
     }
