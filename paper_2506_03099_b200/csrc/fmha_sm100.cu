@@ -1280,6 +1280,9 @@ __global__ void __launch_bounds__(kThreads, 1) fmha_sm100_kernel(const __grid_co
                     uint4 x[D / 8];
                     if (smem_merge) {
                         mbar_wait(&merge_bar[3 * i + n % 3], (n / 3) & 1);
+#ifdef TM_SPANS_PUB
+                        if (threadIdx.x == 0 && n == nc - 1) trace_span(p, 6);   // (spans A/B) last buffer landed
+#endif
                         const uint4* sp = reinterpret_cast<const uint4*>(buf(n % 3));
 #pragma unroll
                         for (int c = 0; c < D / 8; ++c) x[c] = sp[c * kBM + r];

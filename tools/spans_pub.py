@@ -12,8 +12,8 @@ rows = json.load(open(sys.argv[1]))
 t0 = min(r["raw"][0] for r in rows)
 us = lambda r, j: (r["raw"][j] - t0) / 1e3 if r["raw"][j] else None
 mer = [r for r in rows if r["raw"][5]]
-par = [r for r in rows if r["raw"][6] and not r["raw"][5]]
-both = [r for r in rows if r["raw"][6] and r["raw"][5]]
+par = [r for r in rows if r["raw"][6] and not r["raw"][5]]  # (mergers stamp 6 = last buffer landed)
+both = []
 med = lambda v: f"median {st.median(v):6.2f} min {min(v):6.2f} max {max(v):6.2f}" if v else "-"
 print(f"{len(rows)} CTAs: {len(mer)} mergers, {len(par)} partner-only, {len(both)} partner+merger")
 print("  partner write (tiles done -> published)", med([us(r, 6) - us(r, 4) for r in par if r["raw"][4]]))
@@ -22,6 +22,8 @@ print("  merger own done (abs)                  ", med([us(r, 4) for r in mer]))
 print("  merger wait (own done -> counted in)   ", med([us(r, 5) - us(r, 4) for r in mer]))
 print("  weights (counted in -> weights)        ", med([us(r, 1) - us(r, 5) for r in mer if r["raw"][1]]))
 print("  merge loop (weights -> merged)         ", med([us(r, 2) - us(r, 1) for r in mer if r["raw"][2]]))
+print("  last buffer landed (counted in -> 6)   ", med([us(r, 6) - us(r, 5) for r in mer if r["raw"][6]]))
+print("  merge after landing (6 -> merged)      ", med([us(r, 2) - us(r, 6) for r in mer if r["raw"][6] and r["raw"][2]]))
 print("  store+exit (merged -> exit)            ", med([us(r, 3) - us(r, 2) for r in mer if r["raw"][2]]))
 print("  exit: mergers", med([us(r, 3) for r in mer]), "| others", med([us(r, 3) for r in rows if not r["raw"][5]]))
 # per merger: its partners are the following CTAs that published, up to the next merger's CTA
