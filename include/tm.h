@@ -366,8 +366,10 @@ tm_status tm_peer_route_host(int32_t mode, const void* src, void* dst, int32_t b
 /* Host reference of the attention kernel's tail schedule (stream-K; DESIGN
  * Sec 6), for tests without a GPU: the KV tiles of `units` tail units of
  * `tiles_per_unit` tiles each, flattened, are cut into G <= ctas contiguous
- * ranges [bounds[c], bounds[c+1]) (bounds: >= ctas + 1 ints).  Returns G, or
- * -1 on invalid arguments (ctas <= 160). */
+ * ranges [bounds[c], bounds[c+1]) (bounds: >= ctas + 1 ints), the minimum
+ * piece raised until no unit is cut into more than 65 pieces (a split unit's
+ * merger tracks its contributors in a 64-bit mask).  Returns G, or -1 on
+ * invalid arguments (ctas <= 160). */
 int32_t tm_schedule_tail_host(int32_t units, int32_t tiles_per_unit, int32_t ctas, int32_t* bounds);
 
 /* Introspection for tests / bench: number of device kernels the last call

@@ -1254,7 +1254,7 @@ int32_t tm_schedule_tail_host(int32_t units, int32_t tiles_per_unit, int32_t cta
         fail(TM_ERR_INVALID_ARG, "invalid schedule query");
         return -1;
     }
-    return tail_bounds(units, tiles_per_unit, ctas, 4, bounds);
+    return tail_bounds_capped(units, tiles_per_unit, ctas, bounds);
 }
 
 tm_status tm_peer_route_host(int32_t mode, const void* src, void* dst, int32_t batch,

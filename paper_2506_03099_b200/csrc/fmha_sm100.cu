@@ -1546,6 +1546,27 @@ int tail_bounds(int T, int n, int C, int min_piece, int* bound) {
     return tail_bounds_runs(1, &T, &n, C, min_piece, bound);
 }
 
+// The schedule the kernel runs: tail_bounds from kMinPiece, the minimum piece
+// raised (in proportion to the excess) until no unit is cut into more than
+// kMaxUnitPieces pieces (a split unit's merger tracks its contributors in a
+// 64-bit mask).
+int tail_bounds_capped(int T, int n, int C, int* bound) {
+    constexpr int kMinPiece = 4;
+    int g = 0;
+    for (int min_piece = kMinPiece;;) {
+        g = tail_bounds(T, n, C, min_piece, bound);
+        int worst = 1;
+        for (int u = 0; u < T; ++u) {
+            const int first = int(std::upper_bound(bound, bound + g + 1, u * n) - bound) - 1;
+            const int last = int(std::upper_bound(bound, bound + g + 1, u * n + n - 1) - bound) - 1;
+            worst = std::max(worst, last - first + 1);
+        }
+        if (worst <= kMaxUnitPieces || min_piece >= n) break;
+        min_piece = std::max(min_piece + 1, (min_piece * worst + kMaxUnitPieces - 1) / kMaxUnitPieces);
+    }
+    return g;
+}
+
 bool pdl_enabled() {
     static const bool on = [] {
         const char* e = getenv("TM_PDL");
@@ -1585,27 +1606,14 @@ int grid_ctas(int max_ctas) {
 // The stream-K bounds of T tail units of n tiles over C CTAs, cached per
 // (T, n, C): a shape's schedule is computed once.
 bool cached_class(int T, int n, int C, SkClass& k) {
-    constexpr int kMinPiece = 4;
     if ((long long)T * n >= (1ll << 30)) return false;
     static std::mutex mu;
     static std::map<std::tuple<int, int, int>, std::vector<int>> cache;
     std::lock_guard<std::mutex> lock(mu);
     std::vector<int>& b = cache[std::make_tuple(T, n, C)];
     if (b.empty()) {
-        // A split unit's merger tracks its contributors in a 64-bit mask:
-        // raise the minimum piece until no unit has more than 65 pieces.
-        for (int min_piece = kMinPiece;; min_piece *= 2) {
-            b.assign(kMaxPersistentCtas + 1, 0);
-            const int g = tail_bounds(T, n, C, min_piece, b.data());
-            b.resize(g + 1);
-            int worst = 1;
-            for (int u = 0; u < T; ++u) {
-                const int first = int(std::upper_bound(b.begin(), b.end(), u * n) - b.begin()) - 1;
-                const int last = int(std::upper_bound(b.begin(), b.end(), u * n + n - 1) - b.begin()) - 1;
-                worst = std::max(worst, last - first + 1);
-            }
-            if (worst <= 65 || min_piece >= n) break;
-        }
+        b.assign(kMaxPersistentCtas + 1, 0);
+        b.resize(tail_bounds_capped(T, n, C, b.data()) + 1);
     }
     const int G = int(b.size()) - 1;
     if (G <= 0) return false;

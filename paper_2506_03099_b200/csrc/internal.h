@@ -180,6 +180,10 @@ int tail_bounds(int T, int n, int C, int min_piece, int* bound);
 // The same over runs of units of different sizes (run r: units[r] units of
 // tiles[r] tiles each, flattened in order).
 int tail_bounds_runs(int nruns, const int* units, const int* tiles, int C, int min_piece, int* bound);
+// The kernel's schedule: tail_bounds with the minimum piece raised until no
+// unit has more than kMaxUnitPieces pieces (64 contributors + the merger).
+constexpr int kMaxUnitPieces = 65;
+int tail_bounds_capped(int T, int n, int C, int* bound);
 // `trace` (debug, may be null): 4 x 4096 uint64 clock64 timeline of CTA 0.
 cudaError_t launch_fmha_sm100(const AttnProblem& p, void* scratch, cudaStream_t s, int* launches,
                               unsigned long long* trace = nullptr);

@@ -41,6 +41,24 @@ def test_tail_ranges_are_balanced(units, n):
     assert max(costs) <= mean + n, (max(costs), mean)
 
 
+@pytest.mark.parametrize("units,n", [(1, 630), (1, 2000), (2, 1000), (3, 300)])
+def test_long_units_have_at_most_65_pieces(units, n):
+    """A split unit's merger tracks its contributors in a 64-bit mask: however
+    long a unit, the schedule never cuts it into more than 65 pieces (the
+    minimum piece is raised from 4 until that holds), the ranges still
+    partition the tiles, and the cap does not collapse the parallelism (a
+    one-unit problem keeps more than 32 ranges)."""
+    b = tm.tm_schedule_tail_host(units, n, 148)
+    assert b[0] == 0 and b[-1] == units * n
+    assert all(b[i + 1] > b[i] for i in range(len(b) - 1))
+    for u in range(units):
+        first = max(i for i in range(len(b) - 1) if b[i] <= u * n)
+        last = max(i for i in range(len(b) - 1) if b[i] <= u * n + n - 1)
+        assert last - first + 1 <= 65, (u, last - first + 1)
+    if units * n // 4 > 148:                   # enough work for every CTA at the first minimum
+        assert len(b) - 1 > 32
+
+
 def test_invalid_query():
     with pytest.raises(tm.TMError):
         tm.tm_schedule_tail_host(0, 56, 148)
