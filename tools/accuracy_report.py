@@ -28,6 +28,10 @@ CASES = [  # (name, H, Lr, Lc, dtype, dist, rows)
     ("wan512_bf16_D6_large_logits", 40, 1024, 3072, "bf16", "D6", None),
     ("wan512_fp32_D0", 40, 1024, 3072, "fp32", "D0", None),
     ("wan720_bf16_D0_sampled", 40, 2025, 6075, "bf16", "D0", 512),
+    # one P = 8 rank's heads: every unit is cut into 3 pieces and co-merged from fp16 partials
+    ("wan512_h5_bf16_D0", 5, 1024, 3072, "bf16", "D0", None),
+    ("wan512_h5_bf16_D1_peaky", 5, 1024, 3072, "bf16", "D1", None),
+    ("wan512_h5_bf16_D6_large_logits", 5, 1024, 3072, "bf16", "D6", None),
 ]
 
 out = {"measure": "max|O-O_ref|/max|O_ref| over all rows and heads (rows: sampled where noted)",
